@@ -1,0 +1,1158 @@
+// wt_gpu.cu -- host orchestration and the C-ABI (include/wt_gpu.h) of the
+// B200 tracking path. One wt_gpu_ctx owns the uploaded model, the per-
+// sequence state (theta, Phi) and one CUDA stream; every frame is one
+// captured CUDA graph of fixed shape (iteration counts are static), so the
+// host issues a single graph launch per track_frame.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "wt_gpu.h"
+#include "wt_kernels.cuh"
+
+namespace wt {
+void render_launch(cudaStream_t st, int V, int L, int T, const double* offsets, const double* v0,
+                   const double* phi, const double* wgt, const int* wlink, const int* wcount,
+                   const int* tri, const int* dom, double fx, double fy, double cx, double cy,
+                   int W, int H, double sigma, double dropout, double quant, uint64_t base,
+                   double* vpos, unsigned long long* zbits, int* owner, float* depth,
+                   uint8_t* vis);
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError {
+  int code;
+  std::string msg;
+};
+
+#define WT_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      throw CudaError{WT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};   \
+  } while (0)
+
+struct ApiError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw ApiError{code, msg}; }
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  const cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+  if (e != cudaSuccess)
+    throw CudaError{WT_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e)};
+  return static_cast<T*>(p);
+}
+
+template <class T>
+void upload(T* dst, const T* src, size_t n, cudaStream_t st) {
+  if (n) WT_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+struct DevBuf {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* alloc(size_t n) {
+    T* p = dalloc<T>(n);
+    ptrs.push_back(p);
+    return p;
+  }
+  ~DevBuf() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+struct GraphKey {
+  std::vector<double> v;
+  bool operator<(const GraphKey& o) const { return v < o.v; }
+};
+
+}  // namespace
+
+struct wt_gpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int V = 0, L = 0, NP = 0, K = 0, T = 0;
+  wt_intrinsics intr{};
+  wt::DevIntr din{};
+  int P = 0, NB = 0, NTILE = 0;
+
+  // host model copies
+  std::vector<wt::LinkDesc> links;
+  std::vector<int> pair_off, pair_theta, pair_link;
+  std::vector<double> s_diag;
+  std::vector<int> dominant;
+
+  DevBuf mem;
+  wt::DevModel dm{};
+  wt::DevState ds{};   // tracking state
+  wt::DevState hs{};   // stage-hook state (scratch theta / fk / offsets / dchain)
+  double4* phi[2] = {nullptr, nullptr};
+  double4* phi_scratch = nullptr;
+  int cur = 0;
+  int frame_index = 0;
+
+  // frame
+  float* d_depth = nullptr;
+  uint8_t* d_valid = nullptr;
+  double* d_pts_hi = nullptr;
+  int* d_active = nullptr;
+  int* d_nactive = nullptr;
+  int* d_winners = nullptr;
+  bool frame_loaded = false;
+
+  // stats
+  int cap_kin = 0, cap_shape = 0;
+  wt::KinStat* h_kin = nullptr;
+  wt::ShapeStat* h_shape = nullptr;
+
+  // renderer (fp64 copies, lazily built)
+  double* r_v0 = nullptr;
+  double* r_wgt = nullptr;
+  int* r_wlink = nullptr;
+  int* r_wcount = nullptr;
+  int* r_tri = nullptr;
+  int* r_dom = nullptr;
+  double* r_off = nullptr;
+  double* r_phi = nullptr;
+  double* r_vpos = nullptr;
+  unsigned long long* r_zbits = nullptr;
+  int* r_owner = nullptr;
+  float* r_depth = nullptr;
+  uint8_t* r_vis = nullptr;
+  std::vector<double> h_v0, h_wgt;
+  std::vector<int> h_wlink, h_wcount, h_tri;
+
+  int* hook_cnt = nullptr;
+  double* hook_res = nullptr;
+
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+
+  ~wt_gpu_ctx() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    if (h_kin) cudaFreeHost(h_kin);
+    if (h_shape) cudaFreeHost(h_shape);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+template <class F>
+int guarded(wt_gpu_ctx* ctx, F&& f) {
+  try {
+    f();
+    return WT_OK;
+  } catch (const ApiError& e) {
+    (ctx ? ctx->err : g_err) = e.msg;
+    return e.code;
+  } catch (const CudaError& e) {
+    (ctx ? ctx->err : g_err) = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    (ctx ? ctx->err : g_err) = e.what();
+    return WT_EINVAL;
+  }
+}
+
+void check_launch() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaError{WT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+int vgrid(int n) { return std::max(1, (n + wt::kVThreads - 1) / wt::kVThreads); }
+
+// ---- validation (Skeleton::build, skeleton.cpp:7-50; bundle invariants) ----
+
+void validate_model(const wt_model_desc* d) {
+  if (!d) fail(WT_EINVAL, "model is NULL");
+  const int L = d->n_links, V = d->n_vertices, T = d->n_triangles;
+  if (L <= 0) fail(WT_EINVAL, "skeleton has no links");
+  if (L > 64) fail(WT_EINVAL, "at most 64 links are supported on the GPU path");
+  if (V < 0 || T < 0) fail(WT_ELENGTH, "negative vertex / triangle count");
+  if (V >= (1 << 26)) fail(WT_EINVAL, "at most 2^26 vertices are supported");
+  int roots = 0;
+  std::vector<char> seen(static_cast<size_t>(L), 0);
+  for (int j = 0; j < L; ++j) {
+    const int p = d->parent[j];
+    if (p < 0) ++roots;
+    else if (p >= j)
+      fail(WT_EINVAL, "link " + std::to_string(j) +
+                          ": links are not topologically sorted (cycle or forward parent)");
+    const int ti = d->theta_index[j];
+    if (ti < 0 || ti >= L) fail(WT_EINVAL, "link " + std::to_string(j) + ": theta index out of range");
+    if (seen[static_cast<size_t>(ti)])
+      fail(WT_EINVAL, "link " + std::to_string(j) + ": duplicate theta index " + std::to_string(ti));
+    seen[static_cast<size_t>(ti)] = 1;
+    const double* ax = d->joint_axis + 3 * j;
+    const double n = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+    if (std::abs(n - 1.0) > 1e-9) fail(WT_EINVAL, "link " + std::to_string(j) + ": axis is not unit length");
+    if (d->joint_kind[j] != WT_JOINT_HINGE && d->joint_kind[j] != WT_JOINT_PRISMATIC)
+      fail(WT_EINVAL, "link " + std::to_string(j) + ": unknown joint kind");
+  }
+  if (roots != 1)
+    fail(WT_EINVAL, "skeleton must have exactly one root, found " + std::to_string(roots));
+  for (int i = 0; i < V; ++i) {
+    const int c = d->weight_count[i];
+    if (c < 0 || c > 4) fail(WT_EINVAL, "vertex " + std::to_string(i) + ": weight count must be 0..4");
+    for (int s = 0; s < c; ++s) {
+      const int l = d->weight_link[4 * i + s];
+      if (l < 0 || l >= L)
+        fail(WT_EINVAL, "vertex " + std::to_string(i) + ": weight references link " +
+                            std::to_string(l) + " out of range");
+    }
+  }
+  for (int t = 0; t < 3 * T; ++t)
+    if (d->triangles[t] < 0 || d->triangles[t] >= V)
+      fail(WT_EINVAL, "triangle " + std::to_string(t / 3) + ": vertex index out of range");
+  if (d->vtri_offsets[0] != 0) fail(WT_ELENGTH, "vertex->triangle CSR must start at 0");
+  for (int i = 0; i < V; ++i)
+    if (d->vtri_offsets[i + 1] < d->vtri_offsets[i]) fail(WT_ELENGTH, "vertex->triangle CSR not monotone");
+  for (int c = 0; c < d->vtri_offsets[V]; ++c)
+    if (d->vtri_items[c] < 0 || d->vtri_items[c] >= T)
+      fail(WT_EINVAL, "vertex->triangle CSR references a missing triangle");
+  if (d->nbr_offsets[0] != 0) fail(WT_ELENGTH, "neighbour CSR must start at 0");
+  for (int i = 0; i < V; ++i) {
+    if (d->nbr_offsets[i + 1] < d->nbr_offsets[i]) fail(WT_ELENGTH, "neighbour CSR not monotone");
+    for (int c = d->nbr_offsets[i]; c < d->nbr_offsets[i + 1]; ++c) {
+      const int n = d->nbr_items[c];
+      if (n < 0 || n >= V) fail(WT_EINVAL, "vertex " + std::to_string(i) + ": neighbour out of range");
+      if (n == i) fail(WT_EINVAL, "vertex " + std::to_string(i) + ": neighbor set contains the vertex itself");
+    }
+  }
+}
+
+void alloc_state(wt_gpu_ctx* c, wt::DevState& s, bool hook) {
+  s.theta = c->mem.alloc<double>(c->L);
+  s.fk = c->mem.alloc<double>(8 * c->L);
+  s.offsets = c->mem.alloc<double>(8 * c->L);
+  s.dchain = c->mem.alloc<double>(8 * std::max(1, c->NP));
+  if (!hook) {
+    s.pv = c->mem.alloc<double4>(c->V);
+    s.pn = c->mem.alloc<float4>(c->V);
+    s.vbin = c->mem.alloc<unsigned>(c->V);
+    s.vslot = c->mem.alloc<unsigned>(c->V);
+    s.bin_count = c->mem.alloc<int>(c->NB);
+    s.bin_off = c->mem.alloc<int>(c->NB + 1);
+    s.items = c->mem.alloc<double4>(c->V);
+    s.acc = c->mem.alloc<unsigned long long>(4 * static_cast<size_t>(std::max(1, c->V)));
+    const int NE = c->L * (c->L + 1) / 2 + c->L + 8;
+    s.red = c->mem.alloc<unsigned long long>(NE);
+    s.tickets = c->mem.alloc<unsigned>(8);
+    s.sys_out = c->mem.alloc<double>(c->L * c->L + c->L);
+    WT_CUDA(cudaMemsetAsync(s.bin_count, 0, sizeof(int) * c->NB, c->stream));
+    WT_CUDA(cudaMemsetAsync(s.acc, 0, sizeof(unsigned long long) * 4 * std::max(1, c->V), c->stream));
+    WT_CUDA(cudaMemsetAsync(s.red, 0, sizeof(unsigned long long) * NE, c->stream));
+    WT_CUDA(cudaMemsetAsync(s.tickets, 0, sizeof(unsigned) * 8, c->stream));
+  }
+}
+
+void ensure_stats(wt_gpu_ctx* c, int nk, int ns) {
+  if (nk > c->cap_kin) {
+    c->cap_kin = std::max(nk, 16);
+    c->ds.kin_stats = c->mem.alloc<wt::KinStat>(c->cap_kin);
+    if (c->h_kin) cudaFreeHost(c->h_kin);
+    WT_CUDA(cudaMallocHost(&c->h_kin, sizeof(wt::KinStat) * c->cap_kin));
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+  }
+  if (ns > c->cap_shape) {
+    c->cap_shape = std::max(ns, 8);
+    c->ds.shape_stats = c->mem.alloc<wt::ShapeStat>(c->cap_shape);
+    if (c->h_shape) cudaFreeHost(c->h_shape);
+    WT_CUDA(cudaMallocHost(&c->h_shape, sizeof(wt::ShapeStat) * c->cap_shape));
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+  }
+}
+
+// ---- kernel launch helpers (all on ctx->stream) ------------------------------
+
+void enq_fk(wt_gpu_ctx* c, const wt::DevState& s) {
+  wt::k_fk<<<1, 128, 0, c->stream>>>(c->dm, s);
+  check_launch();
+}
+
+void enq_skin(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi) {
+  wt::k_skin<<<vgrid(c->V), wt::kVThreads, sizeof(double) * 8 * c->L, c->stream>>>(c->dm, s, phi);
+  check_launch();
+}
+
+void enq_normals(wt_gpu_ctx* c, const wt::DevState& s, bool bucket, bool zero_acc,
+                 bool compute = true) {
+  wt::k_normals<<<vgrid(c->V), wt::kVThreads, bucket ? 4096 * sizeof(int) : 0, c->stream>>>(
+      c->dm, s, c->din, bucket ? 1 : 0, zero_acc ? 1 : 0, compute ? 1 : 0);
+  check_launch();
+}
+
+void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
+  wt::k_scatter<<<vgrid(c->V), wt::kVThreads, 0, c->stream>>>(c->dm, s);
+  check_launch();
+}
+
+size_t search_smem(int window) {
+  const int halo = wt::kTile + 2 * window;
+  return sizeof(float4) * wt::kSearchCap + sizeof(unsigned) * wt::kSearchCap +
+         sizeof(int) * (halo * halo + 1);
+}
+
+void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, int* winners) {
+  wt::DevFrame f{c->d_valid, c->d_pts_hi, c->d_active, c->d_nactive};
+  wt::SearchArgs sa;
+  sa.W = c->din.W;
+  sa.H = c->din.H;
+  sa.nbx = c->din.nbx;
+  sa.ntx = c->din.ntx;
+  sa.window = a->window_radius;
+  sa.cut2 = static_cast<float>(a->cutoff * a->cutoff);
+  sa.cut2_hi = a->cutoff * a->cutoff;
+  sa.write_winners = winners ? 1 : 0;
+  sa.winners = winners;
+  wt::k_search<<<c->NTILE, wt::kSearchThreads, search_smem(a->window_radius), c->stream>>>(s, f, sa);
+  check_launch();
+}
+
+void enq_associate(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, int* winners) {
+  enq_normals(c, s, true, true);
+  enq_scatter(c, s);
+  enq_search(c, s, a, winners);
+}
+
+int pose_grid(const wt_gpu_ctx* c) {
+  return std::max(1, std::min((c->V + wt::kPoseThreads - 1) / wt::kPoseThreads, 2 * 148));
+}
+
+void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt_kin_config* k,
+              int it, bool solve, const int* count_in, const double* res_in) {
+  wt::PoseArgs pa;
+  pa.lambda_k = k->lambda_k;
+  pa.lambda_s = k->lambda_s;
+  pa.diag_floor = k->diag_floor;
+  pa.limit = k->limit;
+  pa.clamp = k->clamp_limits;
+  pa.iteration = it;
+  pa.solve = solve ? 1 : 0;
+  pa.pad = 0;
+  pa.count_in = count_in;
+  pa.res_in = res_in;
+  wt::k_pose_system<<<pose_grid(c), wt::kPoseThreads, wt::pose_smem_bytes(c->L, c->NP), c->stream>>>(
+      c->dm, s, phi, pa);
+  check_launch();
+}
+
+int shape_grid(const wt_gpu_ctx* c) { return std::max(1, std::min(vgrid(c->V), 4 * 148)); }
+
+void enq_shape(wt_gpu_ctx* c, const wt_shape_config* sc, int it, const double4* in, double4* out) {
+  wt::ShapeArgs sa;
+  sa.lambda_phi = sc->lambda_phi;
+  sa.lambda_nbr = sc->lambda_nbr;
+  sa.lambda_w = sc->lambda_w;
+  sa.diag_floor = sc->diag_floor;
+  sa.iteration = it;
+  sa.pad = 0;
+  wt::k_shape<<<shape_grid(c), wt::kVThreads, sizeof(double) * 8 * c->L, c->stream>>>(c->dm, c->ds,
+                                                                                     in, out, sa);
+  check_launch();
+}
+
+// optimize_pose (kinopt.cpp:132-171) as a static kernel sequence.
+void enq_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* k, const wt_assoc_config* a) {
+  enq_fk(c, c->ds);
+  const int refresh = std::max(1, k->assoc_refresh);
+  for (int it = 0; it < k->iterations; ++it) {
+    enq_skin(c, c->ds, c->phi[c->cur]);
+    if (it % refresh == 0) {
+      enq_associate(c, c->ds, a, nullptr);
+    } else {
+      // correspondences kept, residuals follow the moved surface (:145-150)
+      enq_normals(c, c->ds, false, false);
+    }
+    enq_pose(c, c->ds, c->phi[c->cur], k, it, true, nullptr, nullptr);
+  }
+}
+
+// optimize_shape (shapeopt.cpp:50-130). Returns the new current phi index.
+int enq_optimize_shape(wt_gpu_ctx* c, int cur, const wt_shape_config* sc, const wt_assoc_config* a,
+                       bool stats_pass, bool need_fk) {
+  if (need_fk) enq_fk(c, c->ds);
+  for (int it = 0; it < sc->iterations; ++it) {
+    enq_skin(c, c->ds, c->phi[cur]);
+    enq_associate(c, c->ds, a, nullptr);
+    enq_shape(c, sc, it, c->phi[cur], c->phi[cur ^ 1]);
+    cur ^= 1;  // Jacobi swap (shapeopt.cpp:98)
+  }
+  if (stats_pass && sc->iterations > 0) {
+    enq_skin(c, c->ds, c->phi[cur]);
+    enq_associate(c, c->ds, a, nullptr);
+    wt::k_shape_after<<<shape_grid(c), wt::kVThreads, 0, c->stream>>>(c->dm, c->ds, sc->iterations);
+    check_launch();
+  }
+  return cur;
+}
+
+void check_assoc(const wt_assoc_config* a) {
+  if (!a) fail(WT_EINVAL, "assoc config is NULL");
+  if (a->window_radius < 0 || a->window_radius > 16)
+    fail(WT_EINVAL, "window_radius must be in [0, 16] on the GPU path");
+  if (!(a->cutoff >= 0.0)) fail(WT_EINVAL, "cutoff must be >= 0");
+}
+
+void require_frame(wt_gpu_ctx* c) {
+  if (!c->frame_loaded) fail(WT_EINVAL, "no frame loaded (call wt_gpu_load_depth / wt_gpu_load_cloud)");
+}
+
+void run_graph(wt_gpu_ctx* c, const GraphKey& key, const std::function<void()>& body) {
+  auto it = c->graphs.find(key);
+  if (it == c->graphs.end()) {
+    cudaGraph_t g;
+    WT_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      body();
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &g);
+      throw;
+    }
+    WT_CUDA(cudaStreamEndCapture(c->stream, &g));
+    cudaGraphExec_t ex;
+    WT_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    it = c->graphs.emplace(key, ex).first;
+  }
+  WT_CUDA(cudaGraphLaunch(it->second, c->stream));
+}
+
+void put_kin(const wt_gpu_ctx* c, int n, wt_kin_iter_stats* out, int cap) {
+  for (int k = 0; k < n && k < cap; ++k) {
+    out[k].iteration = k;
+    out[k].associated = c->h_kin[k].associated;
+    out[k].residual_sum = c->h_kin[k].residual_sum;
+    out[k].step_norm = c->h_kin[k].step_norm;
+    out[k].solver_skipped = c->h_kin[k].skipped;
+    out[k].pad_ = 0;
+  }
+}
+
+void put_shape(const wt_gpu_ctx* c, int n, wt_shape_iter_stats* out, int cap) {
+  for (int k = 0; k < n && k < cap; ++k) {
+    out[k].iteration = k;
+    out[k].singular = c->h_shape[k].singular;
+    out[k].mean_phi = c->h_shape[k].mean_phi;
+    out[k].max_phi = c->h_shape[k].max_phi;
+    out[k].mean_abs_r_before = c->h_shape[k].mean_abs_r_before;
+    out[k].mean_abs_r_after = c->h_shape[k].mean_abs_r_after;
+  }
+}
+
+void ensure_render(wt_gpu_ctx* c) {
+  if (c->r_v0) return;
+  const int V = c->V, P = c->P;
+  c->r_v0 = c->mem.alloc<double>(3 * V);
+  c->r_wgt = c->mem.alloc<double>(4 * V);
+  c->r_wlink = c->mem.alloc<int>(4 * V);
+  c->r_wcount = c->mem.alloc<int>(V);
+  c->r_tri = c->mem.alloc<int>(3 * std::max(1, c->T));
+  c->r_dom = c->mem.alloc<int>(V);
+  c->r_off = c->mem.alloc<double>(8 * c->L);
+  c->r_phi = c->mem.alloc<double>(3 * V);
+  c->r_vpos = c->mem.alloc<double>(3 * V);
+  c->r_zbits = c->mem.alloc<unsigned long long>(P);
+  c->r_owner = c->mem.alloc<int>(P);
+  c->r_depth = c->mem.alloc<float>(P);
+  c->r_vis = c->mem.alloc<uint8_t>(c->L);
+  upload(c->r_v0, c->h_v0.data(), 3 * V, c->stream);
+  upload(c->r_wgt, c->h_wgt.data(), 4 * V, c->stream);
+  upload(c->r_wlink, c->h_wlink.data(), 4 * V, c->stream);
+  upload(c->r_wcount, c->h_wcount.data(), V, c->stream);
+  upload(c->r_tri, c->h_tri.data(), 3 * c->T, c->stream);
+  upload(c->r_dom, c->dominant.data(), V, c->stream);
+}
+
+void host_offsets(const wt_gpu_ctx* c, const double* theta, double* out) {
+  std::vector<wt::DQ> fk(static_cast<size_t>(c->L));
+  wt::fk_all(c->links.data(), c->L, theta, fk.data());
+  for (int j = 0; j < c->L; ++j)
+    wt::dq_store(wt::dq_compose(fk[j], wt::dq_load(c->links[j].bind_inv)), out + 8 * j);
+}
+
+}  // namespace
+
+extern "C" {
+
+int wt_gpu_abi_version(void) { return WT_ABI_VERSION; }
+
+int wt_gpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+const char* wt_gpu_global_last_error(void) { return g_err.c_str(); }
+const char* wt_gpu_last_error(const wt_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr, wt_gpu_ctx** out) {
+  if (!out) {
+    g_err = "out is NULL";
+    return WT_EINVAL;
+  }
+  *out = nullptr;
+  auto* c = new wt_gpu_ctx();
+  const int rc = guarded(nullptr, [&] {
+    validate_model(d);
+    if (!intr || intr->width <= 0 || intr->height <= 0) fail(WT_EINVAL, "bad intrinsics");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      fail(WT_ENODEV, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) fail(WT_ENODEV, "device index out of range");
+    c->device = device;
+    WT_CUDA(cudaSetDevice(device));
+    WT_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->L = d->n_links;
+    c->V = d->n_vertices;
+    c->T = d->n_triangles;
+    c->intr = *intr;
+    c->din.fx = intr->fx;
+    c->din.fy = intr->fy;
+    c->din.cx = intr->cx;
+    c->din.cy = intr->cy;
+    c->din.W = intr->width;
+    c->din.H = intr->height;
+    c->din.nbx = (intr->width + wt::kBin - 1) / wt::kBin;
+    c->din.nby = (intr->height + wt::kBin - 1) / wt::kBin;
+    c->din.ntx = (intr->width + wt::kTile - 1) / wt::kTile;
+    c->din.nty = (intr->height + wt::kTile - 1) / wt::kTile;
+    c->P = intr->width * intr->height;
+    c->NB = c->din.nbx * c->din.nby;
+    c->NTILE = c->din.ntx * c->din.nty;
+    const int L = c->L, V = c->V;
+
+    // skeleton: bind pose = FK(0), ancestors, dchain pairs (skeleton.cpp:7-50)
+    c->links.resize(static_cast<size_t>(L));
+    std::vector<int> theta_to_link(static_cast<size_t>(L));
+    for (int j = 0; j < L; ++j) {
+      wt::LinkDesc& l = c->links[static_cast<size_t>(j)];
+      l.parent = d->parent[j];
+      l.kind = d->joint_kind[j];
+      l.theta_index = d->theta_index[j];
+      l.pad = 0;
+      for (int k = 0; k < 3; ++k) l.axis[k] = d->joint_axis[3 * j + k];
+      for (int k = 0; k < 8; ++k) l.offset[k] = d->parent_offset[8 * j + k];
+      theta_to_link[static_cast<size_t>(l.theta_index)] = j;
+    }
+    std::vector<double> zero(static_cast<size_t>(L), 0.0);
+    std::vector<wt::DQ> bind(static_cast<size_t>(L));
+    wt::fk_all(c->links.data(), L, zero.data(), bind.data());
+    for (int j = 0; j < L; ++j) wt::dq_store(wt::dq_inverse(bind[j]), c->links[j].bind_inv);
+    std::vector<std::vector<int>> anc(static_cast<size_t>(L));
+    c->pair_off.assign(1, 0);
+    for (int j = 0; j < L; ++j) {
+      std::vector<int> path;
+      for (int cur = j; cur >= 0; cur = d->parent[cur]) path.push_back(d->theta_index[cur]);
+      std::reverse(path.begin(), path.end());
+      anc[static_cast<size_t>(j)] = path;
+      for (int k : path) {
+        c->pair_theta.push_back(k);
+        c->pair_link.push_back(theta_to_link[static_cast<size_t>(k)]);
+      }
+      c->pair_off.push_back(static_cast<int>(c->pair_theta.size()));
+    }
+    c->NP = static_cast<int>(c->pair_theta.size());
+    // influence counts S (kinopt.cpp:58-70)
+    c->s_diag.assign(static_cast<size_t>(L), 0.0);
+    std::vector<char> hit(static_cast<size_t>(L));
+    for (int i = 0; i < V; ++i) {
+      std::fill(hit.begin(), hit.end(), 0);
+      for (int s = 0; s < d->weight_count[i]; ++s)
+        for (int k : anc[static_cast<size_t>(d->weight_link[4 * i + s])]) hit[static_cast<size_t>(k)] = 1;
+      for (int k = 0; k < L; ++k)
+        if (hit[static_cast<size_t>(k)]) c->s_diag[static_cast<size_t>(k)] += 1.0;
+    }
+
+    // per-vertex device layout
+    std::vector<double4> v0(static_cast<size_t>(V)), wg(static_cast<size_t>(V)), ph(static_cast<size_t>(V));
+    std::vector<uchar4> wl(static_cast<size_t>(V));
+    c->h_v0.assign(d->v0, d->v0 + 3 * V);
+    c->h_wgt.assign(static_cast<size_t>(4 * V), 0.0);
+    c->h_wlink.assign(static_cast<size_t>(4 * V), 0);
+    c->h_wcount.assign(d->weight_count, d->weight_count + V);
+    c->dominant.assign(static_cast<size_t>(V), -1);
+    for (int i = 0; i < V; ++i) {
+      v0[i] = make_double4(d->v0[3 * i], d->v0[3 * i + 1], d->v0[3 * i + 2], 0.0);
+      const double* p = d->phi ? d->phi + 3 * i : nullptr;
+      ph[i] = p ? make_double4(p[0], p[1], p[2], 0.0) : make_double4(0, 0, 0, 0);
+      double w[4] = {0, 0, 0, 0};
+      unsigned char lk[4] = {0xFF, 0xFF, 0xFF, 0xFF};
+      double best = -1.0;
+      for (int s = 0; s < d->weight_count[i]; ++s) {
+        w[s] = d->weight[4 * i + s];
+        lk[s] = static_cast<unsigned char>(d->weight_link[4 * i + s]);
+        c->h_wgt[4 * i + s] = d->weight[4 * i + s];
+        c->h_wlink[4 * i + s] = d->weight_link[4 * i + s];
+        // dominant link (synth.cpp:211-225): max weight, ties to lower link
+        const double e = d->weight[4 * i + s];
+        const int link = d->weight_link[4 * i + s];
+        int& dom = c->dominant[static_cast<size_t>(i)];
+        if (e > best || (e == best && link < dom)) {
+          best = e;
+          dom = link;
+        }
+      }
+      wg[i] = make_double4(w[0], w[1], w[2], w[3]);
+      wl[i] = make_uchar4(lk[0], lk[1], lk[2], lk[3]);
+    }
+    // one-ring: incident triangles in CSR order, rotated so vertex i leads
+    std::vector<int> ring_off(static_cast<size_t>(V) + 1);
+    std::vector<int2> ring(static_cast<size_t>(d->vtri_offsets[V]));
+    for (int i = 0; i < V; ++i) {
+      ring_off[i] = d->vtri_offsets[i];
+      for (int k = d->vtri_offsets[i]; k < d->vtri_offsets[i + 1]; ++k) {
+        const int* t = d->triangles + 3 * d->vtri_items[k];
+        if (t[0] == i) ring[k] = make_int2(t[1], t[2]);
+        else if (t[1] == i) ring[k] = make_int2(t[2], t[0]);
+        else if (t[2] == i) ring[k] = make_int2(t[0], t[1]);
+        else fail(WT_EINVAL, "vertex->triangle CSR lists a triangle that does not contain the vertex");
+      }
+    }
+    ring_off[V] = d->vtri_offsets[V];
+    c->h_tri.assign(d->triangles, d->triangles + 3 * c->T);
+    // neighbours as ELL [K][V]
+    int K = 0;
+    for (int i = 0; i < V; ++i) K = std::max(K, d->nbr_offsets[i + 1] - d->nbr_offsets[i]);
+    c->K = K;
+    std::vector<int> nbr(static_cast<size_t>(std::max(1, K)) * std::max(1, V), -1);
+    for (int i = 0; i < V; ++i)
+      for (int k = 0; k < d->nbr_offsets[i + 1] - d->nbr_offsets[i]; ++k)
+        nbr[static_cast<size_t>(k) * V + i] = d->nbr_items[d->nbr_offsets[i] + k];
+
+    // device model
+    double4* d_v0 = c->mem.alloc<double4>(V);
+    double4* d_wg = c->mem.alloc<double4>(V);
+    uchar4* d_wl = c->mem.alloc<uchar4>(V);
+    int* d_roff = c->mem.alloc<int>(V + 1);
+    int2* d_ring = c->mem.alloc<int2>(ring.size());
+    int* d_nbr = c->mem.alloc<int>(nbr.size());
+    wt::LinkDesc* d_links = c->mem.alloc<wt::LinkDesc>(L);
+    int* d_poff = c->mem.alloc<int>(L + 1);
+    int* d_pth = c->mem.alloc<int>(std::max(1, c->NP));
+    int* d_plk = c->mem.alloc<int>(std::max(1, c->NP));
+    double* d_s = c->mem.alloc<double>(L);
+    upload(d_v0, v0.data(), V, c->stream);
+    upload(d_wg, wg.data(), V, c->stream);
+    upload(d_wl, wl.data(), V, c->stream);
+    upload(d_roff, ring_off.data(), V + 1, c->stream);
+    upload(d_ring, ring.data(), ring.size(), c->stream);
+    upload(d_nbr, nbr.data(), nbr.size(), c->stream);
+    upload(d_links, c->links.data(), L, c->stream);
+    upload(d_poff, c->pair_off.data(), L + 1, c->stream);
+    upload(d_pth, c->pair_theta.data(), c->NP, c->stream);
+    upload(d_plk, c->pair_link.data(), c->NP, c->stream);
+    upload(d_s, c->s_diag.data(), L, c->stream);
+    c->dm = wt::DevModel{V, L, c->NP, K, d_v0, d_wg, d_wl, d_roff, d_ring, d_nbr,
+                         d_links, d_poff, d_pth, d_plk, d_s};
+
+    alloc_state(c, c->ds, false);
+    c->hs = c->ds;  // hooks share the per-vertex buffers, own theta/fk/offsets/dchain
+    alloc_state(c, c->hs, true);
+    c->phi[0] = c->mem.alloc<double4>(V);
+    c->phi[1] = c->mem.alloc<double4>(V);
+    c->phi_scratch = c->mem.alloc<double4>(V);
+    upload(c->phi[0], ph.data(), V, c->stream);
+    WT_CUDA(cudaMemsetAsync(c->ds.theta, 0, sizeof(double) * L, c->stream));
+
+    c->d_depth = c->mem.alloc<float>(c->P);
+    c->d_valid = c->mem.alloc<uint8_t>(c->P);
+    c->d_pts_hi = c->mem.alloc<double>(3 * static_cast<size_t>(c->P));
+    c->d_active = c->mem.alloc<int>(c->NTILE);
+    c->d_nactive = c->mem.alloc<int>(1);
+    c->d_winners = c->mem.alloc<int>(c->P);
+    ensure_stats(c, 16, 8);
+
+    WT_CUDA(cudaFuncSetAttribute(wt::k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(search_smem(16))));
+    WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(wt::pose_smem_bytes(L, c->NP))));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+  });
+  if (rc != WT_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return WT_OK;
+}
+
+void wt_gpu_destroy(wt_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+int wt_gpu_set_state(wt_gpu_ctx* c, const double* theta, const double* phi, int32_t frame_index) {
+  if (!c) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    if (theta) upload(c->ds.theta, theta, c->L, c->stream);
+    if (phi) {
+      std::vector<double4> ph(static_cast<size_t>(c->V));
+      for (int i = 0; i < c->V; ++i) ph[i] = make_double4(phi[3 * i], phi[3 * i + 1], phi[3 * i + 2], 0.0);
+      upload(c->phi[c->cur], ph.data(), c->V, c->stream);
+      WT_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    c->frame_index = frame_index;
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int wt_gpu_get_state(wt_gpu_ctx* c, double* theta, double* phi, int32_t* frame_index) {
+  if (!c) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    if (theta)
+      WT_CUDA(cudaMemcpyAsync(theta, c->ds.theta, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<double4> ph;
+    if (phi) {
+      ph.resize(static_cast<size_t>(c->V));
+      WT_CUDA(cudaMemcpyAsync(ph.data(), c->phi[c->cur], sizeof(double4) * c->V, cudaMemcpyDeviceToHost,
+                              c->stream));
+    }
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < ph.size(); ++i) {
+      phi[3 * i] = ph[i].x;
+      phi[3 * i + 1] = ph[i].y;
+      phi[3 * i + 2] = ph[i].z;
+    }
+    if (frame_index) *frame_index = c->frame_index;
+  });
+}
+
+static void ingest(wt_gpu_ctx* c, const float* depth_dev, double scale, const double* cloud_dev,
+                   const uint8_t* valid_dev) {
+  WT_CUDA(cudaMemsetAsync(c->d_nactive, 0, sizeof(int), c->stream));
+  const dim3 grid(c->din.ntx, c->din.nty);
+  wt::k_ingest<<<grid, wt::kSearchThreads, 0, c->stream>>>(c->din, depth_dev, scale, cloud_dev,
+                                                           valid_dev, c->d_valid, c->d_pts_hi,
+                                                           c->d_active, c->d_nactive);
+  check_launch();
+}
+
+int wt_gpu_load_depth(wt_gpu_ctx* c, const float* depth, double depth_scale) {
+  if (!c || !depth) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    WT_CUDA(cudaMemcpyAsync(c->d_depth, depth, sizeof(float) * c->P, cudaMemcpyDefault, c->stream));
+    ingest(c, c->d_depth, depth_scale, nullptr, nullptr);
+    c->frame_loaded = true;
+  });
+}
+
+int wt_gpu_load_cloud(wt_gpu_ctx* c, const double* points, const uint8_t* valid) {
+  if (!c || !points || !valid) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    WT_CUDA(cudaMemcpyAsync(c->d_pts_hi, points, sizeof(double) * 3 * c->P, cudaMemcpyDefault, c->stream));
+    WT_CUDA(cudaMemcpyAsync(c->d_valid, valid, c->P, cudaMemcpyDefault, c->stream));
+    ingest(c, nullptr, 1.0, c->d_pts_hi, c->d_valid);
+    c->frame_loaded = true;
+  });
+}
+
+int wt_gpu_track_loaded(wt_gpu_ctx* c, const wt_track_config* cfg, wt_frame_stats* stats) {
+  if (!c || !cfg) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    require_frame(c);
+    check_assoc(&cfg->assoc);
+    if (cfg->kin.iterations < 0 || cfg->shape.iterations < 0) fail(WT_EINVAL, "negative iteration count");
+    const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
+                           (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
+    ensure_stats(c, cfg->kin.iterations, cfg->shape.iterations);
+    const int start = c->cur;
+    GraphKey key{{1.0, static_cast<double>(cfg->kin.iterations), static_cast<double>(cfg->kin.assoc_refresh),
+                  cfg->kin.lambda_k, cfg->kin.lambda_s, cfg->kin.diag_floor,
+                  static_cast<double>(cfg->kin.clamp_limits), cfg->kin.limit,
+                  static_cast<double>(cfg->assoc.window_radius), cfg->assoc.cutoff,
+                  shape_now ? 1.0 : 0.0, static_cast<double>(cfg->shape.iterations),
+                  cfg->shape.lambda_phi, cfg->shape.lambda_nbr, cfg->shape.lambda_w,
+                  cfg->shape.diag_floor, static_cast<double>(cfg->shape_stats), static_cast<double>(start)}};
+    run_graph(c, key, [&] {
+      enq_optimize_pose(c, &cfg->kin, &cfg->assoc);
+      if (shape_now)
+        enq_optimize_shape(c, start, &cfg->shape, &cfg->assoc, cfg->shape_stats != 0,
+                           cfg->kin.iterations == 0);
+    });
+    c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
+    const int nk = cfg->kin.iterations, ns = shape_now ? cfg->shape.iterations : 0;
+    if (stats) {
+      if (nk) WT_CUDA(cudaMemcpyAsync(c->h_kin, c->ds.kin_stats, sizeof(wt::KinStat) * nk,
+                                      cudaMemcpyDeviceToHost, c->stream));
+      if (ns) WT_CUDA(cudaMemcpyAsync(c->h_shape, c->ds.shape_stats, sizeof(wt::ShapeStat) * ns,
+                                      cudaMemcpyDeviceToHost, c->stream));
+    }
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    if (stats) {
+      stats->frame = c->frame_index;
+      stats->n_kin = nk;
+      stats->n_shape = ns;
+      if (stats->kin) put_kin(c, nk, stats->kin, stats->cap_kin);
+      if (stats->shape) put_shape(c, ns, stats->shape, stats->cap_shape);
+    }
+    ++c->frame_index;
+  });
+}
+
+int wt_gpu_track_frame(wt_gpu_ctx* c, const float* depth, double depth_scale,
+                       const wt_track_config* cfg, wt_frame_stats* stats) {
+  const int rc = wt_gpu_load_depth(c, depth, depth_scale);
+  if (rc != WT_OK) return rc;
+  return wt_gpu_track_loaded(c, cfg, stats);
+}
+
+int wt_gpu_track_frame_cloud(wt_gpu_ctx* c, const double* points, const uint8_t* valid,
+                             const wt_track_config* cfg, wt_frame_stats* stats) {
+  const int rc = wt_gpu_load_cloud(c, points, valid);
+  if (rc != WT_OK) return rc;
+  return wt_gpu_track_loaded(c, cfg, stats);
+}
+
+int wt_gpu_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* kin, const wt_assoc_config* assoc,
+                         wt_kin_iter_stats* stats, int32_t cap, int32_t* n_out) {
+  if (!c || !kin) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    require_frame(c);
+    check_assoc(assoc);
+    if (kin->iterations < 0) fail(WT_EINVAL, "negative iteration count");
+    ensure_stats(c, kin->iterations, 0);
+    GraphKey key{{2.0, static_cast<double>(kin->iterations), static_cast<double>(kin->assoc_refresh),
+                  kin->lambda_k, kin->lambda_s, kin->diag_floor, static_cast<double>(kin->clamp_limits),
+                  kin->limit, static_cast<double>(assoc->window_radius), assoc->cutoff,
+                  static_cast<double>(c->cur)}};
+    run_graph(c, key, [&] { enq_optimize_pose(c, kin, assoc); });
+    const int nk = kin->iterations;
+    if (nk) WT_CUDA(cudaMemcpyAsync(c->h_kin, c->ds.kin_stats, sizeof(wt::KinStat) * nk,
+                                    cudaMemcpyDeviceToHost, c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    if (stats) put_kin(c, nk, stats, cap);
+    if (n_out) *n_out = nk;
+  });
+}
+
+int wt_gpu_optimize_shape(wt_gpu_ctx* c, const wt_shape_config* shape, const wt_assoc_config* assoc,
+                          int32_t with_stats_pass, wt_shape_iter_stats* stats, int32_t cap,
+                          int32_t* n_out) {
+  if (!c || !shape) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    require_frame(c);
+    check_assoc(assoc);
+    if (shape->iterations < 0) fail(WT_EINVAL, "negative iteration count");
+    ensure_stats(c, 0, shape->iterations);
+    const int start = c->cur;
+    GraphKey key{{3.0, static_cast<double>(shape->iterations), shape->lambda_phi, shape->lambda_nbr,
+                  shape->lambda_w, shape->diag_floor, static_cast<double>(assoc->window_radius),
+                  assoc->cutoff, static_cast<double>(with_stats_pass), static_cast<double>(start)}};
+    run_graph(c, key, [&] { enq_optimize_shape(c, start, shape, assoc, with_stats_pass != 0, true); });
+    c->cur = (shape->iterations % 2) ? start ^ 1 : start;
+    const int ns = shape->iterations;
+    if (ns) WT_CUDA(cudaMemcpyAsync(c->h_shape, c->ds.shape_stats, sizeof(wt::ShapeStat) * ns,
+                                    cudaMemcpyDeviceToHost, c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    if (stats) put_shape(c, ns, stats, cap);
+    if (n_out) *n_out = ns;
+  });
+}
+
+// ---- stage hooks -----------------------------------------------------------------
+
+int wt_gpu_skin(wt_gpu_ctx* c, const double* theta, const double* phi, double* v, double* n,
+                uint8_t* valid) {
+  if (!c || !theta) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    upload(c->hs.theta, theta, c->L, c->stream);
+    const double4* ph = c->phi[c->cur];
+    if (phi) {
+      std::vector<double4> tmp(static_cast<size_t>(c->V));
+      for (int i = 0; i < c->V; ++i) tmp[i] = make_double4(phi[3 * i], phi[3 * i + 1], phi[3 * i + 2], 0.0);
+      upload(c->phi_scratch, tmp.data(), c->V, c->stream);
+      WT_CUDA(cudaStreamSynchronize(c->stream));
+      ph = c->phi_scratch;
+    }
+    enq_fk(c, c->hs);
+    enq_skin(c, c->hs, ph);
+    enq_normals(c, c->hs, false, false);
+    std::vector<double4> pv(static_cast<size_t>(c->V));
+    std::vector<float4> pn(static_cast<size_t>(c->V));
+    WT_CUDA(cudaMemcpyAsync(pv.data(), c->hs.pv, sizeof(double4) * c->V, cudaMemcpyDeviceToHost, c->stream));
+    WT_CUDA(cudaMemcpyAsync(pn.data(), c->hs.pn, sizeof(float4) * c->V, cudaMemcpyDeviceToHost, c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < c->V; ++i) {
+      if (v) {
+        v[3 * i] = pv[i].x;
+        v[3 * i + 1] = pv[i].y;
+        v[3 * i + 2] = pv[i].z;
+      }
+      if (n) {
+        n[3 * i] = pn[i].x;
+        n[3 * i + 1] = pn[i].y;
+        n[3 * i + 2] = pn[i].z;
+      }
+      if (valid) valid[i] = pn[i].w != 0.0f ? 1 : 0;
+    }
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Downloads an association (accumulators + posed mesh) and forms p~, count
+// and r = n.(p~ - v) exactly as the device kernels do.
+void read_association(cudaStream_t st, int V, const wt::DevState& s, double* p_tilde, int32_t* count,
+                      double* residual) {
+  std::vector<unsigned long long> acc(4 * static_cast<size_t>(V));
+  std::vector<double4> pv(static_cast<size_t>(V));
+  std::vector<float4> pn(static_cast<size_t>(V));
+  WT_CUDA(cudaMemcpyAsync(acc.data(), s.acc, sizeof(unsigned long long) * 4 * V, cudaMemcpyDeviceToHost, st));
+  WT_CUDA(cudaMemcpyAsync(pv.data(), s.pv, sizeof(double4) * V, cudaMemcpyDeviceToHost, st));
+  WT_CUDA(cudaMemcpyAsync(pn.data(), s.pn, sizeof(float4) * V, cudaMemcpyDeviceToHost, st));
+  WT_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < V; ++i) {
+    const long long cnt = static_cast<long long>(acc[4 * i + 3]);
+    double pt[3] = {0, 0, 0}, r = 0.0;
+    if (cnt > 0) {
+      const double inv = 1.0 / static_cast<double>(cnt);
+      for (int k = 0; k < 3; ++k)
+        pt[k] = static_cast<double>(static_cast<long long>(acc[4 * i + k])) / wt::kFixPoint * inv;
+      r = static_cast<double>(pn[i].x) * (pt[0] - pv[i].x) + static_cast<double>(pn[i].y) * (pt[1] - pv[i].y) +
+          static_cast<double>(pn[i].z) * (pt[2] - pv[i].z);
+    }
+    if (p_tilde)
+      for (int k = 0; k < 3; ++k) p_tilde[3 * i + k] = pt[k];
+    if (count) count[i] = static_cast<int32_t>(cnt);
+    if (residual) residual[i] = r;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int wt_gpu_associate(wt_gpu_ctx* c, int32_t window_radius, double cutoff, int32_t* winners,
+                     double* p_tilde, int32_t* count, double* residual) {
+  if (!c) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    require_frame(c);
+    wt_assoc_config a{window_radius, 0, cutoff};
+    check_assoc(&a);
+    if (winners) WT_CUDA(cudaMemsetAsync(c->d_winners, 0xFF, sizeof(int) * c->P, c->stream));
+    enq_associate(c, c->hs, &a, winners ? c->d_winners : nullptr);
+    if (winners)
+      WT_CUDA(cudaMemcpyAsync(winners, c->d_winners, sizeof(int) * c->P, cudaMemcpyDeviceToHost, c->stream));
+    read_association(c->stream, c->V, c->hs, p_tilde, count, residual);
+  });
+}
+
+int wt_gpu_associate_posed(int device, const wt_intrinsics* intr, int32_t nv, const double* v,
+                           const double* n, const uint8_t* valid, const double* points,
+                           const uint8_t* point_valid, int32_t window_radius, double cutoff,
+                           int32_t* winners, double* p_tilde, int32_t* count, double* residual) {
+  // A throwaway context with a link-free "loose vertex" model: normals are
+  // taken as given (the reference tests' PosedMesh), so only the bucket /
+  // search / average kernels run.
+  wt_gpu_ctx* c = nullptr;
+  const int rc = guarded(nullptr, [&] {
+    if (!intr || nv < 0 || !v || !n || !valid || !points || !point_valid) fail(WT_EINVAL, "NULL argument");
+    const int par[1] = {-1};
+    const double off[8] = {1, 0, 0, 0, 0, 0, 0, 0};
+    const int kind[1] = {WT_JOINT_HINGE};
+    const double axis[3] = {0, 0, 1};
+    const int tix[1] = {0};
+    std::vector<double> v0(v, v + 3 * nv);
+    std::vector<int> wc(static_cast<size_t>(nv), 0), wlk(4 * static_cast<size_t>(nv), -1);
+    std::vector<double> w(4 * static_cast<size_t>(nv), 0.0);
+    std::vector<int> zero_off(static_cast<size_t>(nv) + 1, 0);
+    wt_model_desc d{};
+    d.n_links = 1;
+    d.n_vertices = nv;
+    d.n_triangles = 0;
+    d.parent = par;
+    d.parent_offset = off;
+    d.joint_kind = kind;
+    d.joint_axis = axis;
+    d.theta_index = tix;
+    d.v0 = v0.data();
+    d.phi = nullptr;
+    d.weight_count = wc.data();
+    d.weight_link = wlk.data();
+    d.weight = w.data();
+    d.triangles = nullptr;
+    d.vtri_offsets = zero_off.data();
+    d.vtri_items = nullptr;
+    d.nbr_offsets = zero_off.data();
+    d.nbr_items = nullptr;
+    const int r = wt_gpu_create(device, &d, intr, &c);
+    if (r != WT_OK) fail(r, g_err);
+    std::vector<double4> pv(static_cast<size_t>(nv));
+    std::vector<float4> pn(static_cast<size_t>(nv));
+    for (int i = 0; i < nv; ++i) {
+      pv[i] = make_double4(v[3 * i], v[3 * i + 1], v[3 * i + 2], 1.0);
+      pn[i] = make_float4(static_cast<float>(n[3 * i]), static_cast<float>(n[3 * i + 1]),
+                          static_cast<float>(n[3 * i + 2]), valid[i] ? 1.0f : 0.0f);
+    }
+    upload(c->ds.pv, pv.data(), nv, c->stream);
+    upload(c->ds.pn, pn.data(), nv, c->stream);
+    if (wt_gpu_load_cloud(c, points, point_valid) != WT_OK) fail(WT_ECUDA, c->err);
+    wt_assoc_config a{window_radius, 0, cutoff};
+    check_assoc(&a);
+    if (winners) WT_CUDA(cudaMemsetAsync(c->d_winners, 0xFF, sizeof(int) * c->P, c->stream));
+    enq_normals(c, c->ds, true, true, /*compute=*/false);  // bucket with the given normals
+    enq_scatter(c, c->ds);
+    enq_search(c, c->ds, &a, winners ? c->d_winners : nullptr);
+    if (winners)
+      WT_CUDA(cudaMemcpyAsync(winners, c->d_winners, sizeof(int) * c->P, cudaMemcpyDeviceToHost, c->stream));
+    read_association(c->stream, nv, c->ds, p_tilde, count, residual);
+  });
+  if (c) wt_gpu_destroy(c);
+  return rc;
+}
+
+int wt_gpu_normal_system(wt_gpu_ctx* c, const double* theta, const wt_kin_config* kin,
+                         const int32_t* count, const double* residual, double* jtj, double* jtr) {
+  if (!c || !theta || !kin || !count || !residual) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    const int V = c->V, L = c->L;
+    if (!c->hook_cnt) {
+      c->hook_cnt = c->mem.alloc<int>(V);
+      c->hook_res = c->mem.alloc<double>(V);
+    }
+    int* d_cnt = c->hook_cnt;
+    double* d_res = c->hook_res;
+    upload(d_cnt, count, V, c->stream);
+    upload(d_res, residual, V, c->stream);
+    upload(c->hs.theta, theta, L, c->stream);
+    enq_fk(c, c->hs);
+    enq_skin(c, c->hs, c->phi[c->cur]);
+    enq_normals(c, c->hs, false, false);
+    enq_pose(c, c->hs, c->phi[c->cur], kin, 0, false, d_cnt, d_res);
+    std::vector<double> out(static_cast<size_t>(L * L + L));
+    WT_CUDA(cudaMemcpyAsync(out.data(), c->hs.sys_out, sizeof(double) * out.size(), cudaMemcpyDeviceToHost,
+                            c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    std::copy(out.begin(), out.begin() + L * L, jtj);
+    std::copy(out.begin() + L * L, out.end(), jtr);
+  });
+}
+
+int wt_gpu_solve_step(int device, int32_t n, const double* jtj, const double* jtr, double lambda_k,
+                      double diag_floor, double* x) {
+  int status = WT_OK;
+  const int rc = guarded(nullptr, [&] {
+    if (n <= 0 || n > 64 || !jtj || !jtr || !x) fail(WT_EINVAL, "solve_step: bad arguments (n in 1..64)");
+    WT_CUDA(cudaSetDevice(device));
+    double* d = dalloc<double>(n * n + n + n + 1);
+    std::vector<double> out(static_cast<size_t>(n) + 1);
+    cudaError_t e = cudaMemcpy(d, jtj, sizeof(double) * n * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d + n * n, jtr, sizeof(double) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      wt::k_solve_step<<<1, 128, sizeof(double) * (n * n + 2 * n)>>>(n, d, d + n * n, lambda_k, diag_floor,
+                                                                     d + n * n + n);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out.data(), d + n * n + n, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) throw CudaError{WT_ECUDA, cudaGetErrorString(e)};
+    if (out[static_cast<size_t>(n)] == 0.0) {
+      status = WT_ENOTPD;
+      g_err = "Cholesky factorization of the damped system failed";
+      return;
+    }
+    std::copy(out.begin(), out.begin() + n, x);
+  });
+  return rc != WT_OK ? rc : status;
+}
+
+int wt_gpu_solve_vertices(int device, int32_t n, const double* dr_dphi, const double* r,
+                          const double* phi, const double* nbr_delta, const int32_t* nbr_count,
+                          const wt_shape_config* cfg, double* delta, uint8_t* singular) {
+  return guarded(nullptr, [&] {
+    if (n < 0 || !cfg) fail(WT_EINVAL, "solve_vertices: bad arguments");
+    if (n == 0) return;
+    WT_CUDA(cudaSetDevice(device));
+    DevBuf m;
+    double* d_dr = m.alloc<double>(3 * n);
+    double* d_r = m.alloc<double>(n);
+    double* d_phi = m.alloc<double>(3 * n);
+    double* d_nd = m.alloc<double>(3 * n);
+    int* d_nc = m.alloc<int>(n);
+    double* d_delta = m.alloc<double>(3 * n);
+    uint8_t* d_sing = m.alloc<uint8_t>(n);
+    WT_CUDA(cudaMemcpy(d_dr, dr_dphi, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+    WT_CUDA(cudaMemcpy(d_r, r, sizeof(double) * n, cudaMemcpyHostToDevice));
+    WT_CUDA(cudaMemcpy(d_phi, phi, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+    WT_CUDA(cudaMemcpy(d_nd, nbr_delta, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+    WT_CUDA(cudaMemcpy(d_nc, nbr_count, sizeof(int) * n, cudaMemcpyHostToDevice));
+    wt::k_solve_vertices<<<(n + 255) / 256, 256>>>(n, d_dr, d_r, d_phi, d_nd, d_nc, cfg->lambda_phi,
+                                                   cfg->lambda_nbr, cfg->lambda_w, cfg->diag_floor,
+                                                   d_delta, d_sing);
+    check_launch();
+    WT_CUDA(cudaMemcpy(delta, d_delta, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    WT_CUDA(cudaMemcpy(singular, d_sing, n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int wt_gpu_render_depth(wt_gpu_ctx* c, const double* theta, const double* phi, const wt_noise* noise,
+                        int32_t frame_index, float* depth, uint8_t* joint_visible) {
+  if (!c || !theta || !depth) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    ensure_render(c);
+    std::vector<double> off(static_cast<size_t>(8 * c->L));
+    host_offsets(c, theta, off.data());
+    upload(c->r_off, off.data(), off.size(), c->stream);
+    if (phi) upload(c->r_phi, phi, 3 * static_cast<size_t>(c->V), c->stream);
+    else WT_CUDA(cudaMemsetAsync(c->r_phi, 0, sizeof(double) * 3 * c->V, c->stream));
+    const wt_noise nz = noise ? *noise : wt_noise{0, 0, 0, 0};
+    // base = splitmix64(seed ^ frame) (synth.cpp:237)
+    uint64_t x = nz.seed ^ static_cast<uint64_t>(static_cast<int64_t>(frame_index));
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    const uint64_t base = x ^ (x >> 31);
+    wt::render_launch(c->stream, c->V, c->L, c->T, c->r_off, c->r_v0, c->r_phi, c->r_wgt, c->r_wlink,
+                      c->r_wcount, c->r_tri, c->r_dom, c->intr.fx, c->intr.fy, c->intr.cx, c->intr.cy,
+                      c->intr.width, c->intr.height, nz.sigma, nz.dropout, nz.quantization, base,
+                      c->r_vpos, c->r_zbits, c->r_owner, c->r_depth, c->r_vis);
+    check_launch();
+    WT_CUDA(cudaMemcpyAsync(depth, c->r_depth, sizeof(float) * c->P, cudaMemcpyDefault, c->stream));
+    if (joint_visible)
+      WT_CUDA(cudaMemcpyAsync(joint_visible, c->r_vis, c->L, cudaMemcpyDefault, c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,1170 @@
+// wt_kernels.cuh -- sm_100a kernels for one tracking frame.
+//
+// Per pose iteration (kinopt.cpp:139-170) the frame graph runs
+//   k_skin -> k_normals(+bin histogram, last CTA scans) -> k_scatter
+//   -> k_search(+scatter-average) -> k_pose_system(last CTA: reduce, damped
+//   Cholesky, theta update, FK/dchain for the next iteration)
+// and per shape iteration (shapeopt.cpp:58-110)
+//   k_skin -> k_normals -> k_scatter -> k_search -> k_shape(last CTA: stats).
+// Everything stays on the device; reductions are deterministic (fixed-point
+// integer atomics are associative), so a frame is bitwise reproducible.
+#pragma once
+
+#include <cstdint>
+
+#include "wt_dq.cuh"
+
+namespace wt {
+
+constexpr int kBin = 8;         // vertex-bucket bin edge in pixels (8x8 bins)
+constexpr int kTile = 16;       // search tile edge: one CTA per 16x16 pixels
+constexpr int kSearchThreads = kTile * kTile;
+constexpr int kSearchCap = 2048;  // candidates staged in shared memory per pass
+constexpr int kVThreads = 256;    // per-vertex kernels
+constexpr int kPoseThreads = 128; // rows per CTA in the normal-equation kernel
+constexpr double kFixPoint = 4294967296.0;        // 2^32: observation sums
+constexpr double kFixSys = 1099511627776.0;       // 2^40: JtJ / Jtr / shape sums
+constexpr double kFixRes = 17592186044416.0;      // 2^44: residual sum of squares
+constexpr unsigned kNoBin = 0xFFFFFFFFu;
+
+struct DevModel {
+  int V, L, NP, K;
+  const double4* v0;       // template vertices (x,y,z,0), fp64
+  const double4* wgt;      // skin weights, entry order kept (entry 0 = pivot)
+  const uchar4* wlink;     // skin links, 0xFF = unused
+  const int* ring_off;     // [V+1] incident triangles of each vertex (CSR order)
+  const int2* ring;        // (b,c): face cross = (v_b - v_i) x (v_c - v_i)
+  const int* nbr;          // [K][V] neighbour ELL, -1 padded
+  const LinkDesc* links;   // [L]
+  const int* pair_off;     // [L+1] dchain pairs of each link
+  const int* pair_theta;   // [NP] theta index k of the pair
+  const int* pair_link;    // [NP] link driven by theta k
+  const double* s_diag;    // [L] influence counts S
+};
+
+struct DevIntr {
+  double fx, fy, cx, cy;
+  int W, H;
+  int nbx, nby;   // bins
+  int ntx, nty;   // search tiles
+};
+
+struct KinStat {      // per pose iteration (device)
+  double residual_sum;
+  double step_norm;
+  int associated;
+  int skipped;
+};
+
+struct ShapeStat {    // per shape iteration (device)
+  double mean_phi, max_phi, mean_abs_r_before, mean_abs_r_after;
+  int singular;
+  int pad;
+};
+
+struct DevState {
+  double* theta;      // [L]
+  double* fk;         // [L*8]
+  double* offsets;    // [L*8] H_jD = H_0j * inverse(bind_j)
+  double* dchain;     // [NP*8]
+  double4* pv;        // posed vertices (x,y,z, blend ok), fp64
+  float4* pn;         // normals (x,y,z, valid)
+  unsigned* vbin;     // bin id or kNoBin
+  unsigned* vslot;    // slot in bin | local pixel << 26
+  int* bin_count;     // [NB] (self-cleaning)
+  int* bin_off;       // [NB+1]
+  double4* items;     // bucketed vertices (x,y,z, bits: vi<<6 | local pixel)
+  unsigned long long* acc;   // [V*4] fixed-point sum x,y,z + count
+  unsigned long long* red;   // reduction slots (self-cleaning)
+  unsigned* tickets;         // last-CTA tickets (self-cleaning)
+  KinStat* kin_stats;
+  ShapeStat* shape_stats;
+  double* sys_out;           // optional JtJ/Jtr dump [L*L + L]
+};
+
+struct DevFrame {
+  const uint8_t* valid;  // per pixel
+  const double* pts_hi;  // per pixel fp64 point (valid pixels only)
+  const int* active_tiles;
+  const int* n_active;
+};
+
+// ---------------------------------------------------------------------------
+// small helpers
+
+__device__ __forceinline__ long long fix(double x, double scale) {
+  return __double2ll_rn(x * scale);
+}
+
+__device__ __forceinline__ void red_add(unsigned long long* p, long long v) {
+  atomicAdd(p, static_cast<unsigned long long>(v));
+}
+
+__device__ __forceinline__ double unfix(unsigned long long v, double scale) {
+  return static_cast<double>(static_cast<long long>(v)) / scale;
+}
+
+// Returns true in every thread of the CTA that finished last (grid-wide),
+// after a fence; resets the ticket.
+__device__ __forceinline__ bool last_block(unsigned* ticket) {
+  __shared__ bool is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    is_last = (t == gridDim.x * gridDim.y - 1);
+    if (is_last) *ticket = 0u;
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// Block-wide exclusive scan over n ints in shared memory (in place);
+// returns the total. blockDim.x must be a multiple of 32.
+__device__ int block_exclusive_scan(int* a, int n) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int x = i < n ? a[i] : 0;
+    int s = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane == 31) warp_tot[wid] = s;
+    __syncthreads();
+    if (wid == 0) {
+      int t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      if (lane < nw) warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const int excl = carry + (wid > 0 ? warp_tot[wid - 1] : 0) + s - x;
+    if (i < n) a[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + x;
+    __syncthreads();
+  }
+  return carry;
+}
+
+// Loads link offsets (and optionally the dchain) into shared memory.
+__device__ __forceinline__ void load_offsets(const DevModel& m, const DevState& s, double* s_off) {
+  for (int i = threadIdx.x; i < m.L * 8; i += blockDim.x) s_off[i] = s.offsets[i];
+}
+
+// Dual-quaternion blend of one vertex (skinmesh.cpp:60-77): raw sum with the
+// antipodality signs. Returns false when the real part collapsed.
+__device__ __forceinline__ bool blend_vertex(const double* s_off, double4 w, uchar4 lk, DQ& raw,
+                                             double sign[4]) {
+  const unsigned char li[4] = {lk.x, lk.y, lk.z, lk.w};
+  const double wi[4] = {w.x, w.y, w.z, w.w};
+  for (int c = 0; c < 4; ++c) raw.r[c] = raw.d[c] = 0.0;
+  sign[0] = sign[1] = sign[2] = sign[3] = 1.0;
+  if (li[0] == 0xFF) return false;  // no weights: blend not ok
+  const double* pivot = s_off + 8 * li[0];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (li[e] == 0xFF) break;
+    const double* h = s_off + 8 * li[e];
+    const double dot = pivot[0] * h[0] + pivot[1] * h[1] + pivot[2] * h[2] + pivot[3] * h[3];
+    const double sg = dot < 0.0 ? -1.0 : 1.0;
+    sign[e] = sg;
+    const double k = sg * wi[e];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      raw.r[c] += h[c] * k;
+      raw.d[c] += h[4 + c] * k;
+    }
+  }
+  const double n = sqrt(raw.r[0] * raw.r[0] + raw.r[1] * raw.r[1] + raw.r[2] * raw.r[2] +
+                        raw.r[3] * raw.r[3]);
+  return n > 1e-12;
+}
+
+// ---------------------------------------------------------------------------
+// FK / link offsets / dchain for the current theta (skeleton.cpp:56-108),
+// executed by one whole CTA. Also used by the pose-solve tail.
+
+__device__ void block_fk(const DevModel& m, const DevState& s, const double* theta) {
+  __shared__ DQ fk[64];
+  if (threadIdx.x == 0) fk_all(m.links, m.L, theta, fk);
+  __syncthreads();
+  for (int j = threadIdx.x; j < m.L; j += blockDim.x) {
+    dq_store(fk[j], s.fk + 8 * j);
+    dq_store(dq_compose(fk[j], dq_load(m.links[j].bind_inv)), s.offsets + 8 * j);
+  }
+  for (int p = threadIdx.x; p < m.NP; p += blockDim.x) {
+    // link j owning pair p
+    int j = 0;
+    while (m.pair_off[j + 1] <= p) ++j;
+    dq_store(d_link_offset(m.links, fk, theta, j, m.pair_link[p]), s.dchain + 8 * p);
+  }
+}
+
+__global__ void k_fk(DevModel m, DevState s) { block_fk(m, s, s.theta); }
+
+// ---------------------------------------------------------------------------
+// frame ingest: depth_to_cloud (seqio.cpp:419-437) and the active-tile list.
+
+__global__ void __launch_bounds__(kSearchThreads) k_ingest(DevIntr in, const float* depth,
+                                                           double scale, const double* cloud,
+                                                           const uint8_t* cloud_valid, uint8_t* pvalid,
+                                                           double* pts_hi, int* active_tiles,
+                                                           int* n_active) {
+  const int u = blockIdx.x * kTile + (threadIdx.x & (kTile - 1));
+  const int v = blockIdx.y * kTile + (threadIdx.x / kTile);
+  int valid = 0;
+  if (u < in.W && v < in.H) {
+    const int i = v * in.W + u;
+    double x = 0, y = 0, z = 0;
+    if (depth) {
+      const float d = depth[i];
+      if (d > 0.0f && isfinite(d)) {
+        z = static_cast<double>(d) * scale;
+        x = (u - in.cx) / in.fx * z;
+        y = (v - in.cy) / in.fy * z;
+        valid = 1;
+      }
+    } else {
+      valid = cloud_valid[i] != 0;
+      if (valid) {
+        x = cloud[3 * i];
+        y = cloud[3 * i + 1];
+        z = cloud[3 * i + 2];
+      }
+    }
+    pvalid[i] = static_cast<uint8_t>(valid);
+    if (valid) {
+      pts_hi[3 * i] = x;
+      pts_hi[3 * i + 1] = y;
+      pts_hi[3 * i + 2] = z;
+    }
+  }
+  if (__syncthreads_or(valid) && threadIdx.x == 0)
+    active_tiles[atomicAdd(n_active, 1)] = blockIdx.y * in.ntx + blockIdx.x;
+}
+
+// ---------------------------------------------------------------------------
+// K1 skinning: v = normalize(blend)(v0 + phi) (skinmesh.cpp:112-121).
+
+__global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, const double4* phi) {
+  extern __shared__ double s_off[];
+  load_offsets(m, s, s_off);
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m.V) return;
+  const double4 a = m.v0[i];
+  const double4 f = phi[i];
+  const double rest[3] = {a.x + f.x, a.y + f.y, a.z + f.z};
+  DQ raw;
+  double sign[4];
+  double4 out;
+  if (blend_vertex(s_off, m.wgt[i], m.wlink[i], raw, sign)) {
+    double p[3];
+    dq_transform_point(dq_normalize(raw), rest, p);
+    out = make_double4(p[0], p[1], p[2], 1.0);
+  } else {
+    out = make_double4(rest[0], rest[1], rest[2], 0.0);  // placeholder, excluded downstream
+  }
+  s.pv[i] = out;
+}
+
+// ---------------------------------------------------------------------------
+// K2 normals (skinmesh.cpp:125-139) fused with K3a: back-face cull, projection
+// with lround semantics (association.cpp:29-37,49-51) and the bin histogram.
+// The last CTA scans the bin counts into offsets and clears them.
+
+__global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, DevIntr in,
+                                                       int do_bucket, int zero_acc, int compute) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m.V) {
+    const double4 v = s.pv[i];
+    const double vx = v.x, vy = v.y, vz = v.z;
+    double nx = 0, ny = 0, nz = 0;
+    bool valid;
+    if (compute) {
+      double ax = 0, ay = 0, az = 0;
+      const int r0 = m.ring_off[i], r1 = m.ring_off[i + 1];
+      for (int r = r0; r < r1; ++r) {
+        const int2 bc = m.ring[r];
+        const double4 b = s.pv[bc.x];
+        const double4 c = s.pv[bc.y];
+        const double ex = b.x - vx, ey = b.y - vy, ez = b.z - vz;
+        const double fx = c.x - vx, fy = c.y - vy, fz = c.z - vz;
+        ax += ey * fz - ez * fy;
+        ay += ez * fx - ex * fz;
+        az += ex * fy - ey * fx;
+      }
+      const double len = sqrt(ax * ax + ay * ay + az * az);
+      valid = v.w != 0.0;
+      if (len > 1e-20) {
+        nx = ax / len;
+        ny = ay / len;
+        nz = az / len;
+      } else {
+        valid = false;
+      }
+      s.pn[i] = make_float4(static_cast<float>(nx), static_cast<float>(ny), static_cast<float>(nz),
+                            valid ? 1.0f : 0.0f);
+    } else {  // normals given (loose-vertex association)
+      const float4 n = s.pn[i];
+      nx = n.x;
+      ny = n.y;
+      nz = n.z;
+      valid = n.w != 0.0f;
+    }
+    if (zero_acc) {
+      reinterpret_cast<ulonglong2*>(s.acc)[2 * i] = make_ulonglong2(0ull, 0ull);
+      reinterpret_cast<ulonglong2*>(s.acc)[2 * i + 1] = make_ulonglong2(0ull, 0ull);
+    }
+    if (do_bucket) {
+      unsigned bin = kNoBin;
+      unsigned lp = 0;
+      if (valid && !(nx * vx + ny * vy + nz * vz > 0.0) && vz > 0.0) {
+        const double pu = in.fx * vx / vz + in.cx;
+        const double pvv = in.fy * vy / vz + in.cy;
+        const double ru = round(pu), rv = round(pvv);  // half away from zero, like lround
+        if (ru >= 0.0 && rv >= 0.0 && ru < in.W && rv < in.H) {
+          const int iu = static_cast<int>(ru), iv = static_cast<int>(rv);
+          bin = static_cast<unsigned>((iv / kBin) * in.nbx + (iu / kBin));
+          lp = static_cast<unsigned>((iv % kBin) * kBin + (iu % kBin));
+        }
+      }
+      // warp-aggregated histogram update: one atomic per distinct bin
+      const unsigned peers = __match_any_sync(__activemask(), bin);
+      unsigned slot = 0;
+      if (bin != kNoBin) {
+        const int leader = __ffs(peers) - 1;
+        const int lane = threadIdx.x & 31;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(&s.bin_count[bin], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        slot = base + __popc(peers & ((1u << lane) - 1u));
+      }
+      s.vbin[i] = bin;
+      s.vslot[i] = slot | (lp << 26);
+    }
+  }
+  if (do_bucket && last_block(s.tickets + 0)) {
+    extern __shared__ int s_scan[];
+    const int nb = in.nbx * in.nby;
+    // scan in shared-memory pieces of 4096 bins, carrying the running total
+    int carry = 0;
+    for (int base = 0; base < nb; base += 4096) {
+      const int n = min(4096, nb - base);
+      for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        s_scan[k] = __ldcg(s.bin_count + base + k);
+        s.bin_count[base + k] = 0;
+      }
+      __syncthreads();
+      const int tot = block_exclusive_scan(s_scan, n);
+      for (int k = threadIdx.x; k < n; k += blockDim.x) s.bin_off[base + k] = s_scan[k] + carry;
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) s.bin_off[nb] = carry;
+  }
+}
+
+// K3c scatter into bin order (association.cpp:57-66, unordered within a bin:
+// the winner rule is a lexicographic (d^2, index) minimum, so bucket order
+// never changes a result).
+__global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevState s) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m.V) return;
+  const unsigned bin = s.vbin[i];
+  if (bin == kNoBin) return;
+  const unsigned sl = s.vslot[i];
+  const double4 v = s.pv[i];
+  const unsigned tag = (static_cast<unsigned>(i) << 6) | (sl >> 26);
+  s.items[s.bin_off[bin] + (sl & 0x03FFFFFFu)] =
+      make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(tag)));
+}
+
+// ---------------------------------------------------------------------------
+// K4 + K5: windowed nearest-vertex search (associate_winners,
+// association.cpp:69-109) and the scatter-average accumulation
+// (association.cpp:124-131) in one pass. One CTA per 16x16 pixel tile: the
+// bucketed vertices of the bins overlapping the tile's (16+2w)^2 halo are
+// staged in shared memory and re-bucketed per halo pixel, so each window row
+// is one contiguous span exactly as in the reference.
+
+// Relative band within which fp32 anchor-relative distances cannot order two
+// candidates reliably (their d^2 error is ~1e-6 relative); such pixels are
+// re-decided in fp64.
+constexpr float kTieEps = 1e-4f;
+constexpr float kTieAbs = 1e-12f;
+
+__device__ __forceinline__ double exact_d2(double4 v, double px, double py, double pz) {
+  const double dx = __dsub_rn(v.x, px), dy = __dsub_rn(v.y, py), dz = __dsub_rn(v.z, pz);
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+struct SearchArgs {
+  int W, H, nbx;
+  int ntx;
+  int window;
+  float cut2;
+  double cut2_hi;  // cutoff^2 in fp64, the reference's test (association.cpp:98)
+  int write_winners;
+  int* winners;
+};
+
+__global__ void __launch_bounds__(kSearchThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float4* sorted = reinterpret_cast<float4*>(smem);
+  unsigned* keys = reinterpret_cast<unsigned*>(sorted + kSearchCap);
+  int* off = reinterpret_cast<int*>(keys + kSearchCap);
+  __shared__ int bin_pref[64];
+  __shared__ int bin_id[64];
+  __shared__ int s_first;
+
+  const int b = blockIdx.x;
+  if (b >= *f.n_active) return;
+  const int tile = f.active_tiles[b];
+  const int tx = tile % a.ntx, ty = tile / a.ntx;
+  const int tu0 = tx * kTile, tv0 = ty * kTile;
+  const int pu = tu0 + (threadIdx.x & (kTile - 1));
+  const int pv = tv0 + threadIdx.x / kTile;
+  const int w = a.window;
+  const bool inside = pu < a.W && pv < a.H;
+  const int pix = inside ? pv * a.W + pu : 0;
+  const bool valid = inside && f.valid[pix] != 0;
+  // Distances are evaluated in fp32 relative to a per-tile anchor (the first
+  // valid pixel's fp64 point): differences of fp64 positions rounded once,
+  // so d^2 keeps ~1e-6 relative precision instead of fp32 absolute
+  // coordinates' ~1e-4 near ties.
+  if (threadIdx.x == 0) s_first = kSearchThreads;
+  __syncthreads();
+  if (valid) atomicMin(&s_first, static_cast<int>(threadIdx.x));
+  __syncthreads();
+  const int ap = (tv0 + s_first / kTile) * a.W + tu0 + (s_first & (kTile - 1));
+  const double ax = f.pts_hi[3 * ap], ay = f.pts_hi[3 * ap + 1], az = f.pts_hi[3 * ap + 2];
+  float px = 0.f, py = 0.f, pz = 0.f;
+  if (valid) {
+    px = static_cast<float>(f.pts_hi[3 * pix] - ax);
+    py = static_cast<float>(f.pts_hi[3 * pix + 1] - ay);
+    pz = static_cast<float>(f.pts_hi[3 * pix + 2] - az);
+  }
+
+  const int hu0 = max(0, tu0 - w), hv0 = max(0, tv0 - w);
+  const int hu1 = min(a.W - 1, tu0 + kTile - 1 + w), hv1 = min(a.H - 1, tv0 + kTile - 1 + w);
+  const int HU = hu1 - hu0 + 1, HV = hv1 - hv0 + 1;
+  const int bx0 = hu0 / kBin, bx1 = hu1 / kBin, by0 = hv0 / kBin, by1 = hv1 / kBin;
+  const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);  // <= 49 for w <= 16
+  if (threadIdx.x < 32) {
+    // prefix sums of the overlapped bins' item counts
+    int carry = 0;
+    for (int base = 0; base < nb; base += 32) {
+      const int k = base + threadIdx.x;
+      int c = 0, id = 0;
+      if (k < nb) {
+        id = (by0 + k / nbx) * a.nbx + (bx0 + k % nbx);
+        c = s.bin_off[id + 1] - s.bin_off[id];
+      }
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) >= o) x += y;
+      }
+      if (k < nb) {
+        bin_pref[k] = carry + x - c;
+        bin_id[k] = id;
+      }
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (threadIdx.x == 0) bin_pref[nb] = carry;
+  }
+  __syncthreads();
+  const int total = bin_pref[nb];
+
+  // Exact winner across chunks: fp64 d^2 evaluated like the reference,
+  // ((dx*dx + dy*dy) + dz*dz) without FMA contraction.
+  double best_x = INFINITY;
+  int best_i = -1;
+  double phx = 0.0, phy = 0.0, phz = 0.0;
+  if (valid) {
+    phx = f.pts_hi[3 * pix];
+    phy = f.pts_hi[3 * pix + 1];
+    phz = f.pts_hi[3 * pix + 2];
+  }
+  const int ncell = HU * HV;
+  for (int chunk = 0; chunk < total; chunk += kSearchCap) {
+    const int n = min(kSearchCap, total - chunk);
+    for (int k = threadIdx.x; k <= ncell; k += blockDim.x) off[k] = 0;
+    __syncthreads();
+    // pass 1: halo pixel of every staged candidate, per-pixel slot
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      const int g = chunk + c;
+      int lo = 0, hi = nb;  // bin_pref[lo] <= g < bin_pref[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (bin_pref[mid] <= g) lo = mid;
+        else hi = mid;
+      }
+      const int bid = bin_id[lo];
+      const double4 it = s.items[s.bin_off[bid] + (g - bin_pref[lo])];
+      const unsigned tag = static_cast<unsigned>(__double_as_longlong(it.w));
+      const int lp = tag & 63u;
+      const int u = (bid % a.nbx) * kBin + (lp % kBin);
+      const int v = (bid / a.nbx) * kBin + (lp / kBin);
+      unsigned key = 0xFFFFFFFFu;
+      if (u >= hu0 && u <= hu1 && v >= hv0 && v <= hv1) {
+        const int hp = (v - hv0) * HU + (u - hu0);
+        const int slot = atomicAdd(&off[hp], 1);
+        key = static_cast<unsigned>(hp) * kSearchCap + static_cast<unsigned>(slot);
+      }
+      keys[c] = key;
+    }
+    __syncthreads();
+    block_exclusive_scan(off, ncell + 1);
+    __syncthreads();
+    // pass 2: place candidates by halo pixel, anchor-relative (re-read hits L1)
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      const unsigned key = keys[c];
+      if (key == 0xFFFFFFFFu) continue;
+      const int g = chunk + c;
+      int lo = 0, hi = nb;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (bin_pref[mid] <= g) lo = mid;
+        else hi = mid;
+      }
+      const double4 it = s.items[s.bin_off[bin_id[lo]] + (g - bin_pref[lo])];
+      const unsigned tag = static_cast<unsigned>(__double_as_longlong(it.w));
+      sorted[off[key / kSearchCap] + (key % kSearchCap)] =
+          make_float4(static_cast<float>(it.x - ax), static_cast<float>(it.y - ay),
+                      static_cast<float>(it.z - az), __uint_as_float(tag));
+    }
+    __syncthreads();
+    if (valid) {
+      const int r0 = max(pv - w, 0), r1 = min(pv + w, a.H - 1);
+      const int c0 = max(pu - w, 0) - hu0, c1 = min(pu + w, a.W - 1) - hu0;
+      // fp32 scan: best and runner-up within a slightly widened cutoff
+      const float cut_hi = a.cut2 * (1.0f + kTieEps);
+      float bd = INFINITY, d2 = INFINITY;
+      int bi = -1;
+      for (int r = r0; r <= r1; ++r) {
+        const int row = (r - hv0) * HU;
+        const int e0 = off[row + c0], e1 = off[row + c1 + 1];
+        for (int e = e0; e < e1; ++e) {
+          const float4 c = sorted[e];
+          const float dx = c.x - px, dy = c.y - py, dz = c.z - pz;
+          const float d = dx * dx + dy * dy + dz * dz;
+          if (d <= cut_hi) {
+            const int vi = static_cast<int>(__float_as_uint(c.w) >> 6);
+            if (d < bd || (d == bd && vi < bi)) {
+              d2 = bd;
+              bd = d;
+              bi = vi;
+            } else {
+              d2 = fminf(d2, d);
+            }
+          }
+        }
+      }
+      if (bi >= 0) {
+        const float thr = bd * (1.0f + kTieEps) + kTieAbs;
+        if (d2 <= thr || bd >= a.cut2 * (1.0f - kTieEps)) {
+          // ambiguous (near-tie or near the cutoff): exact fp64 re-evaluation
+          for (int r = r0; r <= r1; ++r) {
+            const int row = (r - hv0) * HU;
+            const int e0 = off[row + c0], e1 = off[row + c1 + 1];
+            for (int e = e0; e < e1; ++e) {
+              const float4 c = sorted[e];
+              const float dx = c.x - px, dy = c.y - py, dz = c.z - pz;
+              if (dx * dx + dy * dy + dz * dz <= thr) {
+                const int vi = static_cast<int>(__float_as_uint(c.w) >> 6);
+                const double x = exact_d2(s.pv[vi], phx, phy, phz);
+                if (x <= a.cut2_hi && (x < best_x || (x == best_x && vi < best_i))) {
+                  best_x = x;
+                  best_i = vi;
+                }
+              }
+            }
+          }
+        } else {
+          const double x = exact_d2(s.pv[bi], phx, phy, phz);
+          if (x <= a.cut2_hi && (x < best_x || (x == best_x && bi < best_i))) {
+            best_x = x;
+            best_i = bi;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (valid) {
+    if (a.write_winners) a.winners[pix] = best_i;
+    if (best_i >= 0) {
+      unsigned long long* acc = s.acc + 4 * static_cast<size_t>(best_i);
+      red_add(acc + 0, fix(f.pts_hi[3 * pix], kFixPoint));
+      red_add(acc + 1, fix(f.pts_hi[3 * pix + 1], kFixPoint));
+      red_add(acc + 2, fix(f.pts_hi[3 * pix + 2], kFixPoint));
+      red_add(acc + 3, 1ll);
+    }
+  }
+}
+
+// p~_i = mean of the observations won by vertex i; count in *cnt.
+__device__ __forceinline__ bool observed_mean(const unsigned long long* acc, int i, double* pt,
+                                              long long* cnt) {
+  const ulonglong2 a01 = reinterpret_cast<const ulonglong2*>(acc)[2 * i];
+  const ulonglong2 a23 = reinterpret_cast<const ulonglong2*>(acc)[2 * i + 1];
+  const long long c = static_cast<long long>(a23.y);
+  *cnt = c;
+  if (c <= 0) return false;
+  const double inv = 1.0 / static_cast<double>(c);
+  pt[0] = unfix(a01.x, kFixPoint) * inv;
+  pt[1] = unfix(a01.y, kFixPoint) * inv;
+  pt[2] = unfix(a23.x, kFixPoint) * inv;
+  return true;
+}
+
+
+// ---------------------------------------------------------------------------
+// Dense fp64 Cholesky + solve for the L x L pose system, executed by one CTA
+// (solve_step, kinopt.cpp:121-130). A is row-major in shared memory and is
+// overwritten by its factor. Like Eigen's LLT the factorisation fails at the
+// first pivot that is not strictly positive. Returns ok in *ok (CTA-uniform).
+__device__ void block_cholesky_solve(int L, double* A, const double* b, double* x, int* ok) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  for (int k = 0; k < L; ++k) {
+    if (threadIdx.x == 0) {
+      const double p = A[k * L + k];
+      if (!(p > 0.0)) s_ok = 0;
+      else A[k * L + k] = sqrt(p);
+    }
+    __syncthreads();
+    if (!s_ok) break;
+    const double lkk = A[k * L + k];
+    for (int i = k + 1 + threadIdx.x; i < L; i += blockDim.x) A[i * L + k] /= lkk;
+    __syncthreads();
+    const int m = L - k - 1;
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+      const int i = k + 1 + t / m, j = k + 1 + t % m;
+      if (j <= i) A[i * L + j] -= A[i * L + k] * A[j * L + k];
+    }
+    __syncthreads();
+  }
+  if (s_ok && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    // forward: L y = b
+    for (int i = 0; i < L; ++i) {
+      double s = 0.0;
+      for (int j = lane; j < i; j += 32) s += A[i * L + j] * x[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) x[i] = (b[i] - s) / A[i * L + i];
+      __syncwarp();
+    }
+    // backward: L^T x = y
+    for (int i = L - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int j = i + 1 + lane; j < L; j += 32) s += A[j * L + i] * x[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) x[i] = (x[i] - s) / A[i * L + i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  *ok = s_ok;
+}
+
+// Block-wide sum of a double and an int (result valid in thread 0).
+__device__ __forceinline__ void block_sum2(double& d, long long& n) {
+  __shared__ double sd[32];
+  __shared__ long long sn[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    sd[wid] = d;
+    sn[wid] = n;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    d = 0.0;
+    n = 0;
+    for (int k = 0; k < nw; ++k) {  // fixed order
+      d += sd[k];
+      n += sn[k];
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// K6 + K7 (+K0): pose normal equations (accumulate_normal_system,
+// kinopt.cpp:72-119 with fill_row :29-47) for every associated vertex, then
+// in the last CTA: prior (:113-117), damped Cholesky (solve_step :121-130),
+// theta update (:161-165), iteration stats (:153-169) and FK/dchain for the
+// new theta. JtJ rows of 128 vertices are staged in shared memory (fp64),
+// compacted to the vertices that carry a row, and reduced entry-parallel.
+
+struct PoseArgs {
+  double lambda_k, lambda_s, diag_floor, limit;
+  int clamp;
+  int iteration;
+  int solve;             // 0: only dump JtJ/Jtr (+prior) to s.sys_out (stage hook)
+  int pad;
+  const int* count_in;   // optional association override (stage hook)
+  const double* res_in;
+};
+
+__host__ __device__ inline size_t pose_smem_bytes(int L, int NP) {
+  const int Lp = L | 1;
+  const int NE = L * (L + 1) / 2 + L;
+  return sizeof(double) * (8 * L + 8 * NP + kPoseThreads * Lp + kPoseThreads + NE) +
+         sizeof(int) * (L + 1 + NP + kPoseThreads + 1) + sizeof(unsigned short) * 2 * NE + 16;
+}
+
+__global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevState s,
+                                                              const double4* phi, PoseArgs a) {
+  extern __shared__ __align__(16) double psm[];
+  const int L = m.L;
+  const int Lp = L | 1;
+  const int NT = L * (L + 1) / 2;
+  const int NE = NT + L;  // upper JtJ, then Jtr
+  double* s_off = psm;                        // 8L
+  double* s_dch = s_off + 8 * L;              // 8NP
+  double* rows = s_dch + 8 * m.NP;            // kPoseThreads * Lp (compacted rows)
+  double* rres = rows + kPoseThreads * Lp;    // kPoseThreads
+  double* esum = rres + kPoseThreads;         // NE running sums
+  int* s_poff = reinterpret_cast<int*>(esum + NE);  // L+1
+  int* s_pth = s_poff + (L + 1);                     // NP
+  int* flag = s_pth + m.NP;                          // kPoseThreads + 1
+  unsigned short* ea = reinterpret_cast<unsigned short*>(flag + kPoseThreads + 1);
+  unsigned short* eb = ea + NE;
+
+  for (int k = threadIdx.x; k < 8 * L; k += blockDim.x) s_off[k] = s.offsets[k];
+  for (int k = threadIdx.x; k < 8 * m.NP; k += blockDim.x) s_dch[k] = s.dchain[k];
+  for (int k = threadIdx.x; k <= L; k += blockDim.x) s_poff[k] = m.pair_off[k];
+  for (int k = threadIdx.x; k < m.NP; k += blockDim.x) s_pth[k] = m.pair_theta[k];
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    esum[e] = 0.0;
+    if (e < NT) {  // row-major upper triangle
+      int r = 0, rem = e;
+      while (rem >= L - r) {
+        rem -= L - r;
+        ++r;
+      }
+      ea[e] = static_cast<unsigned short>(r);
+      eb[e] = static_cast<unsigned short>(r + rem);
+    } else {
+      ea[e] = static_cast<unsigned short>(e - NT);
+      eb[e] = 0xFFFF;  // pairs with the residual
+    }
+  }
+  double rsum = 0.0;
+  long long nassoc = 0;
+  __syncthreads();
+
+  for (int base = blockIdx.x * blockDim.x; base < m.V; base += gridDim.x * blockDim.x) {
+    const int i = base + threadIdx.x;
+    double r = 0.0;
+    bool has_row = false;
+    DQ raw;
+    double sign[4];
+    double r8[8];
+    double4 wv = make_double4(0, 0, 0, 0);
+    uchar4 lk = make_uchar4(0xFF, 0xFF, 0xFF, 0xFF);
+    if (i < m.V) {
+      long long cnt = 0;
+      bool have = false;
+      const double4 v = s.pv[i];
+      const float4 n = s.pn[i];
+      if (a.count_in) {
+        cnt = a.count_in[i];
+        have = cnt > 0;
+        r = have ? a.res_in[i] : 0.0;
+      } else {
+        double pt[3];
+        have = observed_mean(s.acc, i, pt, &cnt);
+        if (have)
+          r = static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
+              static_cast<double>(n.z) * (pt[2] - v.z);
+      }
+      if (have) {
+        rsum += r * r;
+        ++nassoc;
+        wv = m.wgt[i];
+        lk = m.wlink[i];
+        if (n.w != 0.0f && blend_vertex(s_off, wv, lk, raw, sign)) {
+          const double4 a0 = m.v0[i];
+          const double4 f = phi[i];
+          const double rest[3] = {a0.x + f.x, a0.y + f.y, a0.z + f.z};
+          const double nn[3] = {n.x, n.y, n.z};
+          dq_point_plane_row(raw, rest, nn, r8);
+          has_row = true;
+        }
+      }
+    }
+    // compact the rows of this chunk in vertex order (deterministic)
+    flag[threadIdx.x] = has_row ? 1 : 0;
+    __syncthreads();
+    const int nrows = block_exclusive_scan(flag, kPoseThreads);
+    if (has_row) {
+      const int slot = flag[threadIdx.x];
+      double* row = rows + slot * Lp;
+      for (int k = 0; k < L; ++k) row[k] = 0.0;
+      const unsigned char li[4] = {lk.x, lk.y, lk.z, lk.w};
+      const double wi[4] = {wv.x, wv.y, wv.z, wv.w};
+      for (int e = 0; e < 4; ++e) {
+        if (li[e] == 0xFF) break;
+        const double coeff = wi[e] * sign[e];
+        for (int p = s_poff[li[e]]; p < s_poff[li[e] + 1]; ++p) {
+          const double* d8 = s_dch + 8 * p;
+          double dot = 0.0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) dot += r8[c] * d8[c];
+          row[s_pth[p]] += coeff * dot;
+        }
+      }
+      rres[slot] = r;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+      const int ca = ea[e], cb = eb[e];
+      double acc = 0.0;
+      if (cb == 0xFFFF) {
+        for (int t = 0; t < nrows; ++t) acc += rows[t * Lp + ca] * rres[t];
+      } else {
+        for (int t = 0; t < nrows; ++t) acc += rows[t * Lp + ca] * rows[t * Lp + cb];
+      }
+      esum[e] += acc;
+    }
+    __syncthreads();
+  }
+  block_sum2(rsum, nassoc);
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) red_add(s.red + e, fix(esum[e], kFixSys));
+  if (threadIdx.x == 0) {
+    red_add(s.red + NE, fix(rsum, kFixRes));
+    red_add(s.red + NE + 1, nassoc);
+  }
+  if (!last_block(s.tickets + 1)) return;
+
+  // ---- last CTA: assemble, prior, solve, update, stats, FK ---------------
+  double* A = rows;                 // L*L (fits: kPoseThreads*Lp >= L*L for L <= 128)
+  double* jtr = rres;               // L (kPoseThreads >= L)
+  double* jtj_d = esum;             // reuse: diag of JtJ (L)
+  __shared__ double s_theta[64];
+  __shared__ double s_x[64];
+  __shared__ double s_rsum;
+  __shared__ long long s_nassoc;
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    const double val = unfix(__ldcg(s.red + e), kFixSys);
+    s.red[e] = 0ull;
+    const int ca = ea[e], cb = eb[e];
+    if (cb == 0xFFFF) {
+      jtr[ca] = val;
+    } else {
+      A[ca * L + cb] = val;
+      A[cb * L + ca] = val;
+    }
+  }
+  if (threadIdx.x == 0) {
+    s_rsum = unfix(__ldcg(s.red + NE), kFixRes);
+    s_nassoc = static_cast<long long>(__ldcg(s.red + NE + 1));
+    s.red[NE] = 0ull;
+    s.red[NE + 1] = 0ull;
+  }
+  for (int k = threadIdx.x; k < L; k += blockDim.x) s_theta[k] = s.theta[k];
+  __syncthreads();
+  // default-pose prior (lambda_s S)^2 on the diagonal (kinopt.cpp:113-117)
+  for (int k = threadIdx.x; k < L; k += blockDim.x) {
+    const double p = a.lambda_s * m.s_diag[k];
+    A[k * L + k] += p * p;
+    jtr[k] += p * p * s_theta[k];
+  }
+  __syncthreads();
+  if (!a.solve) {
+    for (int e = threadIdx.x; e < L * L; e += blockDim.x) s.sys_out[e] = A[e];
+    for (int k = threadIdx.x; k < L; k += blockDim.x) s.sys_out[L * L + k] = jtr[k];
+    return;
+  }
+  // A = JtJ + lambda_k diag(JtJ) + floor I
+  __shared__ int s_finite;
+  if (threadIdx.x == 0) s_finite = 1;
+  for (int k = threadIdx.x; k < L; k += blockDim.x) jtj_d[k] = A[k * L + k];
+  __syncthreads();
+  for (int k = threadIdx.x; k < L; k += blockDim.x)
+    A[k * L + k] = A[k * L + k] + a.lambda_k * jtj_d[k] + a.diag_floor;
+  __syncthreads();
+  for (int e = threadIdx.x; e < L * L; e += blockDim.x)
+    if (!isfinite(A[e])) s_finite = 0;
+  for (int k = threadIdx.x; k < L; k += blockDim.x)
+    if (!isfinite(jtr[k])) s_finite = 0;
+  __syncthreads();
+  int ok = 0;
+  if (s_finite) block_cholesky_solve(L, A, jtr, s_x, &ok);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double nrm = 0.0;
+    if (ok) {
+      for (int k = 0; k < L; ++k) {
+        double t = s_theta[k] - s_x[k];
+        if (a.clamp && a.limit > 0.0) t = fmin(fmax(t, -a.limit), a.limit);
+        s_theta[k] = t;
+        nrm += s_x[k] * s_x[k];
+      }
+    }
+    KinStat st;
+    st.residual_sum = s_rsum;
+    st.associated = static_cast<int>(s_nassoc);
+    st.step_norm = ok ? sqrt(nrm) : 0.0;
+    st.skipped = ok ? 0 : 1;
+    s.kin_stats[a.iteration] = st;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < L; k += blockDim.x) s.theta[k] = s_theta[k];
+  __syncthreads();
+  block_fk(m, s, s_theta);
+}
+
+// ---------------------------------------------------------------------------
+// K8: per-vertex regularised 3x3 shape step (optimize_shape body,
+// shapeopt.cpp:78-96, solve_vertex :25-48), Jacobi: reads phi_in, writes
+// phi_out. The last CTA writes the iteration's ShapeIterStats.
+
+// solve_vertex with Eigen LLT semantics on the 3x3 system; returns false
+// (singular) on non-finite input or a non-positive pivot.
+__device__ __forceinline__ bool solve_vertex3(const double g[3], double r, const double phi[3],
+                                              const double nd[3], int ncount, double lphi,
+                                              double lnbr, double lw, double floor_,
+                                              double delta[3]) {
+  double A[3][3];
+  for (int x = 0; x < 3; ++x)
+    for (int y = 0; y < 3; ++y) A[x][y] = g[x] * g[y];
+  const double reg = lphi + lnbr * ncount;
+  for (int d = 0; d < 3; ++d) {
+    A[d][d] += reg;
+    A[d][d] += lw * A[d][d];
+    A[d][d] += floor_;
+  }
+  double b[3];
+  for (int d = 0; d < 3; ++d) b[d] = g[d] * r + lphi * phi[d] + lnbr * nd[d];
+  bool finite = true;
+  for (int x = 0; x < 3; ++x) {
+    finite = finite && isfinite(b[x]);
+    for (int y = 0; y < 3; ++y) finite = finite && isfinite(A[x][y]);
+  }
+  delta[0] = delta[1] = delta[2] = 0.0;
+  if (!finite) return false;
+  // LLT on the lower triangle (Eigen llt_inplace semantics)
+  double l00 = A[0][0];
+  if (!(l00 > 0.0)) return false;
+  l00 = sqrt(l00);
+  const double l10 = A[1][0] / l00, l20 = A[2][0] / l00;
+  double l11 = A[1][1] - l10 * l10;
+  if (!(l11 > 0.0)) return false;
+  l11 = sqrt(l11);
+  const double l21 = (A[2][1] - l20 * l10) / l11;
+  double l22 = A[2][2] - l20 * l20 - l21 * l21;
+  if (!(l22 > 0.0)) return false;
+  l22 = sqrt(l22);
+  const double y0 = b[0] / l00;
+  const double y1 = (b[1] - l10 * y0) / l11;
+  const double y2 = (b[2] - l20 * y0 - l21 * y1) / l22;
+  delta[2] = y2 / l22;
+  delta[1] = (y1 - l21 * delta[2]) / l11;
+  delta[0] = (y0 - l10 * delta[1] - l20 * delta[2]) / l00;
+  return true;
+}
+
+struct ShapeArgs {
+  double lambda_phi, lambda_nbr, lambda_w, diag_floor;
+  int iteration;
+  int pad;
+};
+
+__global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState s, const double4* phi_in,
+                                                     double4* phi_out, ShapeArgs a) {
+  extern __shared__ double s_off[];
+  load_offsets(m, s, s_off);
+  __syncthreads();
+  double abs_r = 0.0, sum_phi = 0.0, max_phi = 0.0;
+  long long observed = 0, singular = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
+    const double4 f = phi_in[i];
+    const double ph[3] = {f.x, f.y, f.z};
+    double nd[3] = {0.0, 0.0, 0.0};
+    int ncount = 0;
+    for (int k = 0; k < m.K; ++k) {
+      const int j = m.nbr[k * m.V + i];
+      if (j < 0) break;
+      const double4 fj = phi_in[j];
+      nd[0] += ph[0] - fj.x;
+      nd[1] += ph[1] - fj.y;
+      nd[2] += ph[2] - fj.z;
+      ++ncount;
+    }
+    double g[3] = {0.0, 0.0, 0.0};
+    double r = 0.0;
+    double pt[3];
+    long long cnt = 0;
+    if (observed_mean(s.acc, i, pt, &cnt)) {
+      const double4 v = s.pv[i];
+      const float4 n = s.pn[i];
+      const double ro = static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
+                        static_cast<double>(n.z) * (pt[2] - v.z);
+      abs_r += fabs(ro);
+      ++observed;
+      DQ raw;
+      double sign[4];
+      if (n.w != 0.0f && blend_vertex(s_off, m.wgt[i], m.wlink[i], raw, sign)) {
+        // dr/dphi = -(R^T n), R = rotation of the normalised blend
+        double R[9];
+        dq_rotation(dq_normalize(raw), R);
+        g[0] = -(R[0] * n.x + R[3] * n.y + R[6] * n.z);
+        g[1] = -(R[1] * n.x + R[4] * n.y + R[7] * n.z);
+        g[2] = -(R[2] * n.x + R[5] * n.y + R[8] * n.z);
+        r = ro;
+      }
+    }
+    double delta[3];
+    const bool ok = solve_vertex3(g, r, ph, nd, ncount, a.lambda_phi, a.lambda_nbr, a.lambda_w,
+                                  a.diag_floor, delta);
+    singular += ok ? 0 : 1;
+    const double nx = ph[0] - delta[0], ny = ph[1] - delta[1], nz = ph[2] - delta[2];
+    phi_out[i] = make_double4(nx, ny, nz, 0.0);
+    const double len = sqrt(nx * nx + ny * ny + nz * nz);
+    sum_phi += len;
+    max_phi = fmax(max_phi, len);
+  }
+  // block reductions (fixed order) then fixed-point atomics
+  block_sum2(abs_r, observed);
+  double sp = sum_phi;
+  block_sum2(sp, singular);
+  __shared__ double smax[32];
+  double mx = max_phi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < (blockDim.x >> 5); ++k) mx = fmax(mx, smax[k]);
+    red_add(s.red + 0, fix(abs_r, kFixSys));
+    red_add(s.red + 1, observed);
+    red_add(s.red + 2, fix(sp, kFixSys));
+    red_add(s.red + 3, singular);
+    atomicMax(s.red + 4, static_cast<unsigned long long>(__double_as_longlong(mx)));
+  }
+  if (!last_block(s.tickets + 2)) return;
+  if (threadIdx.x == 0) {
+    const double sabs = unfix(__ldcg(s.red + 0), kFixSys);
+    const long long nobs = static_cast<long long>(__ldcg(s.red + 1));
+    const double sphi = unfix(__ldcg(s.red + 2), kFixSys);
+    const long long nsing = static_cast<long long>(__ldcg(s.red + 3));
+    const double mphi = __longlong_as_double(static_cast<long long>(__ldcg(s.red + 4)));
+    for (int k = 0; k < 5; ++k) s.red[k] = 0ull;
+    ShapeStat st;
+    st.mean_phi = m.V > 0 ? sphi / static_cast<double>(m.V) : 0.0;
+    st.max_phi = mphi;
+    st.mean_abs_r_before = nobs > 0 ? sabs / static_cast<double>(nobs) : 0.0;
+    st.mean_abs_r_after = 0.0;
+    st.singular = static_cast<int>(nsing);
+    st.pad = 0;
+    s.shape_stats[a.iteration] = st;
+  }
+}
+
+// Closing measurement pass of optimize_shape (shapeopt.cpp:112-129): mean
+// |r| over observed vertices of a fresh association; fills mean_abs_r_after.
+__global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, DevState s, int n_its) {
+  double abs_r = 0.0;
+  long long observed = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
+    double pt[3];
+    long long cnt = 0;
+    if (observed_mean(s.acc, i, pt, &cnt)) {
+      const double4 v = s.pv[i];
+      const float4 n = s.pn[i];
+      abs_r += fabs(static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
+                    static_cast<double>(n.z) * (pt[2] - v.z));
+      ++observed;
+    }
+  }
+  block_sum2(abs_r, observed);
+  if (threadIdx.x == 0) {
+    red_add(s.red + 0, fix(abs_r, kFixSys));
+    red_add(s.red + 1, observed);
+  }
+  if (!last_block(s.tickets + 3)) return;
+  if (threadIdx.x == 0) {
+    const double sabs = unfix(__ldcg(s.red + 0), kFixSys);
+    const long long nobs = static_cast<long long>(__ldcg(s.red + 1));
+    s.red[0] = 0ull;
+    s.red[1] = 0ull;
+    for (int k = 0; k + 1 < n_its; ++k)
+      s.shape_stats[k].mean_abs_r_after = s.shape_stats[k + 1].mean_abs_r_before;
+    if (n_its > 0) s.shape_stats[n_its - 1].mean_abs_r_after = nobs > 0 ? sabs / nobs : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage-hook kernels.
+
+// solve_step on an explicit system (kinopt.cpp:121-130): out[0..n) = x,
+// out[n] = 1 on success, 0 for NotPositiveDefinite.
+__global__ void k_solve_step(int n, const double* jtj, const double* jtr, double lambda_k,
+                             double diag_floor, double* out) {
+  extern __shared__ double sm[];
+  double* A = sm;
+  double* b = A + n * n;
+  double* x = b + n;
+  __shared__ int fin;
+  if (threadIdx.x == 0) fin = 1;
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) A[e] = jtj[e];
+  for (int k = threadIdx.x; k < n; k += blockDim.x) b[k] = jtr[k];
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += blockDim.x)
+    A[k * n + k] = jtj[k * n + k] + lambda_k * jtj[k * n + k] + diag_floor;
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x)
+    if (!isfinite(A[e])) fin = 0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x)
+    if (!isfinite(b[k])) fin = 0;
+  __syncthreads();
+  int ok = 0;
+  if (fin) block_cholesky_solve(n, A, b, x, &ok);
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += blockDim.x) out[k] = ok ? x[k] : 0.0;
+  if (threadIdx.x == 0) out[n] = ok ? 1.0 : 0.0;
+}
+
+__global__ void k_solve_vertices(int n, const double* dr, const double* r, const double* phi,
+                                 const double* nd, const int* ncount, double lphi, double lnbr,
+                                 double lw, double floor_, double* delta, uint8_t* singular) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double d[3];
+  const bool ok = solve_vertex3(dr + 3 * i, r[i], phi + 3 * i, nd + 3 * i, ncount[i], lphi, lnbr,
+                                lw, floor_, d);
+  delta[3 * i] = d[0];
+  delta[3 * i + 1] = d[1];
+  delta[3 * i + 2] = d[2];
+  singular[i] = ok ? 0 : 1;
+}
+
+}  // namespace wt
