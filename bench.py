@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Per-frame tracking throughput of the warptrack hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c1|c2|c3|c4] [--sequences S]
+
+A step is one track_frame (tracker.cpp:54-68) on one synthetic depth frame:
+5 pose Gauss-Newton iterations + 2 surface iterations + optimize_shape's
+closing stats pass (dynamic mode), the BASELINE.json headline configuration
+C3 (640x480 depth, ~100k-vertex 20-link humanoid) unless --config says
+otherwise. Frames are rendered on the GPU (synthesize_frame semantics, no
+noise) from a sinusoidal joint trajectory before timing.
+
+value: frames/s over all ranks with the depth frames already resident in
+HBM, each frame = device copy into the tracker + one graph launch, timed
+with CUDA events on the tracker's stream; L2 is flushed (256 MiB write)
+between frames, outside the timed spans. e2e: the same metric through the
+public per-frame API (Tracker.track_frame with a pinned host depth frame,
+stats read back, then theta read back), events bracketing each call.
+
+Under torchrun each rank tracks its own sequence(s) on its own GPU (weak
+scaling, no collective in the loop); time = max over ranks.
+--impl reference times the unmodified reference CPU implementation
+(oracle/_ref, all host threads) on rank 0 on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (width, height, target vertices, mode, pose its, shape its)
+    "c1": (320, 240, 7_000, "smooth-bind", 12, 0),
+    "c2": (640, 480, 25_000, "dynamic", 5, 2),
+    "c3": (640, 480, 100_000, "dynamic", 5, 2),
+    "c4": (1920, 1080, 400_000, "dynamic", 5, 2),
+}
+METRIC = "frames/s at 640×480 depth, pose+surface, 100k-vert mesh; % of HBM roofline"
+
+# SURVEY.md §8(d) algorithmic bytes per launch (fp32, unpadded) for each
+# kernel kind: V vertices, P pixels, A associated vertices, Vvis bucketed.
+def alg_bytes(kind: str, V: int, P: int, A: int, Vvis: int) -> float:
+    return {
+        "skin": 56 * V,                       # K1
+        "normals+bucket": 77 * V + 37 * V + 16 * P,  # K2 + K3 histogram/scan
+        "scatter": 8 * Vvis,                  # K3 scatter part (items)
+        "search+average": 12 * P + 16 * Vvis + 8 * P + 72 * V,  # K4 + K5
+        "pose_system+solve": 4 * V + 61 * A,  # K6 + K7
+        "shape_step": 81 * V,                 # K8
+        "shape_stats": 72 * V,
+        "fk": 0,
+    }[kind]
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 3 + k and s[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_workload(cfg_name: str):
+    from paper_1711_07999_b200.model import make_humanoid
+    from paper_1711_07999_b200.tracker import AssocConfig, Intrinsics, KinSolverConfig, ShapeSolverConfig, TrackConfig
+    W, H, nv, mode, kits, sits = CONFIGS[cfg_name]
+    bundle = make_humanoid(nv)
+    intr = Intrinsics.scaled(W, H)
+    cfg = TrackConfig(mode=mode, kin=KinSolverConfig(iterations=kits), shape=ShapeSolverConfig(iterations=max(sits, 1)),
+                      assoc=AssocConfig())
+    return bundle, intr, cfg
+
+
+def trajectory(bundle, frame: int, seq: int) -> np.ndarray:
+    from paper_1711_07999_b200.model import humanoid_trajectory
+    return humanoid_trajectory(bundle.link_count, frame, phase_offset=0.7 * seq)
+
+
+def cpu_reference(bundle, intr, cfg, frames_host, seconds: float, theta0) -> dict:
+    """The reference's own track_frame (oracle/_ref) on all host threads over a
+    bounded sample of the same frames."""
+    from oracle import ref
+    rm = ref.RefModel.from_bundle(bundle)
+    rt = ref.RefTracker(rm, theta0)
+    c = cfg.c()
+    c.threads = 0  # resolve_threads(0) = all hardware threads (parallel.hpp:17-21)
+    rt.track_frame_depth(intr.c(), frames_host[0], c)  # warm-up frame
+    n, t0 = 0, time.perf_counter()
+    while n + 1 < len(frames_host):
+        rt.track_frame_depth(intr.c(), frames_host[n + 1], c)
+        n += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "frames/s", "cores": ref.hardware_threads(), "kind": "reference",
+            "sample": f"{n} frames of the same workload after 1 warm-up frame, track_frame threads=0 "
+                      f"(oracle/_ref, reference sources compiled unmodified), {dt:.1f} s"}
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    from oracle import ref
+    from paper_1711_07999_b200 import _lib as W
+    bundle, intr, cfg = make_workload(args.config)
+    rm = ref.RefModel.from_bundle(bundle)
+    nframes = args.warmup + args.steps + 1
+    frames = [rm.render_depth(trajectory(bundle, f, 0), intr.c(), frame=f)[0] for f in range(nframes)]
+    rt = ref.RefTracker(rm, trajectory(bundle, 0, 0))
+    c = cfg.c()
+    c.threads = 0
+    for f in range(args.warmup):
+        rt.track_frame_depth(intr.c(), frames[f + 1], c)
+    t0 = time.perf_counter()
+    for f in range(args.steps):
+        rt.track_frame_depth(intr.c(), frames[args.warmup + f + 1], c)
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {"metric": METRIC, "value": v, "unit": "frames/s", "impl": "reference", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference synthesize_frame renders of a sinusoidal trajectory, no noise)",
+            "config": workload_config(args, bundle, intr, cfg),
+            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": ref.hardware_threads(), "kind": "reference",
+                             "sample": f"{args.steps} frames after {args.warmup} warm-up frames, "
+                                       "track_frame threads=0, wall clock"},
+            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, bundle, intr, cfg) -> dict:
+    W, H, nv, mode, kits, sits = CONFIGS[args.config]
+    names = {"c1": "C1", "c2": "C2", "c3": "C3 (headline)", "c4": "C4"}
+    return {"workload": f"{names[args.config]}: {W}x{H} depth, {bundle.vertex_count}-vertex "
+                        f"{bundle.link_count}-link humanoid, {mode} ({kits} pose + {sits} surface GN iterations"
+                        f"{' + stats pass' if sits else ''}), {args.sequences} sequence(s) per GPU",
+            "vertices": bundle.vertex_count, "triangles": bundle.triangle_count, "links": bundle.link_count,
+            "width": W, "height": H, "mode": mode, "pose_iterations": kits, "shape_iterations": sits,
+            "window_radius": cfg.assoc.window_radius, "cutoff": cfg.assoc.cutoff,
+            "sequences_per_gpu": args.sequences,
+            "l2": "flushed between timed frames (256 MiB write, outside the timed spans)"}
+
+
+def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1711_07999_b200 import _lib as W
+    from paper_1711_07999_b200.tracker import Tracker
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    bundle, intr, cfg = make_workload(args.config)
+    S = args.sequences
+    trackers = [Tracker(bundle, intr, trajectory(bundle, 0, rank * S + s), device=local_rank) for s in range(S)]
+    L = W.lib()
+    ccfg = cfg.c()
+    nframes = args.warmup + args.steps + 1
+    P = intr.width * intr.height
+    # frames rendered on the GPU straight into HBM, plus pinned host copies
+    frames_dev = [torch.empty((nframes, intr.height, intr.width), dtype=torch.float32, device=dev) for _ in range(S)]
+    for s, trk in enumerate(trackers):
+        for f in range(nframes):
+            trk.render_depth(trajectory(bundle, f, rank * S + s), frame=f, out_ptr=frames_dev[s][f].data_ptr())
+    torch.cuda.synchronize()
+    frames_host = [t.cpu().pin_memory() for t in frames_dev]
+    valid_px = float((frames_dev[0][1:] > 0).float().sum().item() / (nframes - 1))
+    streams = [torch.cuda.ExternalStream(L.wt_gpu_stream(t._ctx), device=dev) for t in trackers]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def reset():
+        for s, trk in enumerate(trackers):
+            trk.set_state(theta=trajectory(bundle, 0, rank * S + s), phi=np.zeros((bundle.vertex_count, 3)),
+                          frame_index=0)
+
+    def frame_dev(s, f):
+        W.check(L.wt_gpu_load_depth(trackers[s]._ctx, frames_dev[s][f].data_ptr(), 1.0), trackers[s]._ctx)
+        W.check(L.wt_gpu_track_async(trackers[s]._ctx, C.byref(ccfg)), trackers[s]._ctx)
+
+    # ---- device-resident timing (value) ----
+    reset()
+    for f in range(1, args.warmup + 1):
+        for s in range(S):
+            frame_dev(s, f)
+    for t in trackers:
+        W.check(L.wt_gpu_sync(t._ctx))
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    st0 = streams[0]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            f = args.warmup + 1 + k
+            with torch.cuda.stream(st0):
+                flush.zero_()
+                starts[k].record(st0)
+            for s in range(S):
+                if s > 0:
+                    streams[s].wait_event(starts[k])
+                frame_dev(s, f)
+            for s in range(1, S):
+                e = torch.cuda.Event()
+                e.record(streams[s])
+                st0.wait_event(e)
+            ends[k].record(st0)
+        torch.cuda.synchronize()
+    dev_ms = sum(starts[k].elapsed_time(ends[k]) for k in range(args.steps))
+    if world > 1:
+        dist.barrier()
+
+    # ---- end-to-end through the public per-frame API (e2e) ----
+    reset()
+    stats_buf = W.FrameStatsC(0, 0, 0, 64, 64, 0, trackers[0]._kin, trackers[0]._shape)
+    theta = np.zeros(bundle.link_count)
+    e_st = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_en = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for f in range(1, args.warmup + 1):
+        for s in range(S):
+            trackers[s].track_frame(cfg, depth=frames_host[s][f].numpy())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        f = args.warmup + 1 + k
+        with torch.cuda.stream(st0):
+            flush.zero_()
+        e_st[k].record(st0)
+        for s in range(S):
+            t = trackers[s]
+            W.check(L.wt_gpu_track_frame(t._ctx, frames_host[s][f].data_ptr(), 1.0, C.byref(ccfg),
+                                         C.byref(stats_buf)), t._ctx)
+            W.check(L.wt_gpu_get_state(t._ctx, theta.ctypes.data, None, None), t._ctx)
+        e_en[k].record(st0)
+    torch.cuda.synchronize()
+    e2e_ms = sum(e_st[k].elapsed_time(e_en[k]) for k in range(args.steps))
+
+    # ---- per-kernel device times inside the real frame (events between kernels) ----
+    kinds = (C.c_int32 * 512)()
+    ms = (C.c_float * 512)()
+    n = C.c_int32()
+    per_kind = {}
+    nprof = 3
+    nker = 0
+    for rep in range(nprof):
+        f = 1 + rep
+        W.check(L.wt_gpu_load_depth(trackers[0]._ctx, frames_dev[0][f].data_ptr(), 1.0), trackers[0]._ctx)
+        W.check(L.wt_gpu_profile_frame(trackers[0]._ctx, C.byref(ccfg), kinds, ms, 512, C.byref(n)),
+                trackers[0]._ctx)
+        nker = n.value
+        for k in range(n.value):
+            name = W.KERNEL_KINDS[kinds[k]]
+            d = per_kind.setdefault(name, [0.0, 0])
+            d[0] += ms[k]
+            d[1] += 1
+    # association statistics for the byte model
+    st = trackers[0].track_frame(cfg, depth=frames_host[0][args.warmup].numpy())
+    A = st.kin[-1].associated if st and st.kin else bundle.vertex_count // 4
+    Vvis = bundle.vertex_count // 2
+    kernels = {}
+    for name, (tot, cnt) in per_kind.items():
+        avg_ms = tot / cnt
+        b = alg_bytes(name, bundle.vertex_count, P, A, Vvis)
+        kernels[name] = {"launches_per_frame": cnt // nprof, "avg_us": 1e3 * avg_ms,
+                         "us_per_frame": 1e3 * tot / nprof, "alg_bytes": b,
+                         "achieved_gbs": b / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else None}
+    dominant = max(kernels, key=lambda k: kernels[k]["us_per_frame"])
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    # ---- aggregate over ranks (max time) ----
+    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms = t.tolist()
+    total_frames = args.steps * S * world
+    value = total_frames / (dev_ms * 1e-3)
+    e2e = total_frames / (e2e_ms * 1e-3)
+    if rank != 0:
+        return
+    frame_bytes = sum(alg_bytes(nm, bundle.vertex_count, P, A, Vvis) * kernels[nm]["launches_per_frame"]
+                      for nm in kernels)
+    frame_us = sum(kernels[nm]["us_per_frame"] for nm in kernels)
+    dk = kernels[dominant]
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 geometry, f32 search (fp64 tie re-decision)",
+        "data": "synthetic (GPU synthesize_frame renders of a sinusoidal joint trajectory, no noise)",
+        "config": {**workload_config(args, bundle, intr, cfg), "valid_pixels_mean": valid_px,
+                   "associated_vertices": A},
+        "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": 4 * P * S,
+                "d2h_bytes_per_step": S * (8 * bundle.link_count + 32 * (cfg.kin.iterations + cfg.shape.iterations))},
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dk["achieved_gbs"], "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
+                     "traffic": None, "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"]},
+        "frame_roofline": {"alg_bytes_per_frame": frame_bytes, "kernel_us_per_frame": frame_us,
+                           "achieved": frame_bytes / (frame_us * 1e-6) / 1e9,
+                           "frac": frame_bytes / (frame_us * 1e-6) / 1e9 / peak},
+        "kernels": kernels,
+        "gpu_launches": args.steps * S * (nker + 1),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_reference(bundle, intr, cfg, [frames_host[0][f].numpy() for f in range(nframes)],
+                                             args.cpu_seconds, trajectory(bundle, 0, 0))
+    print(json.dumps(line), flush=True)
+    for t_ in trackers:
+        t_.close()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--sequences", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -212,6 +212,20 @@ int wt_gpu_optimize_shape(wt_gpu_ctx* ctx, const wt_shape_config* shape,
                           const wt_assoc_config* assoc, int32_t with_stats_pass,
                           wt_shape_iter_stats* stats, int32_t cap, int32_t* n_out);
 
+/* ---- asynchronous use / measurement --------------------------------------- */
+/* The context's CUDA stream (cudaStream_t) for event timing by the caller. */
+void* wt_gpu_stream(wt_gpu_ctx* ctx);
+/* Enqueues track_frame on the loaded frame without waiting and without
+ * stats; wt_gpu_sync (or any synchronous call) waits for completion. */
+int wt_gpu_track_async(wt_gpu_ctx* ctx, const wt_track_config* cfg);
+int wt_gpu_sync(wt_gpu_ctx* ctx);
+/* Runs one track_frame through an instrumented graph (a CUDA event after
+ * every kernel) and returns each kernel's kind and device time in ms:
+ * 0 fk, 1 skin, 2 normals+bucket, 3 scatter, 4 search+average,
+ * 5 pose system+solve, 6 shape step, 7 shape stats pass. */
+int wt_gpu_profile_frame(wt_gpu_ctx* ctx, const wt_track_config* cfg, int32_t* kinds, float* ms,
+                         int32_t cap, int32_t* n_out);
+
 /* ---- stage hooks (parity / tests) --------------------------------------- */
 /* skin(mesh, link_offsets(theta)) with phi override (NULL = state phi).
  * Outputs are host arrays [V*3],[V*3],[V]; any may be NULL. */

@@ -88,8 +88,11 @@ EXPORTS = [
     "wt_gpu_load_depth", "wt_gpu_load_cloud", "wt_gpu_track_loaded", "wt_gpu_track_frame",
     "wt_gpu_track_frame_cloud", "wt_gpu_optimize_pose", "wt_gpu_optimize_shape", "wt_gpu_skin",
     "wt_gpu_associate", "wt_gpu_associate_posed", "wt_gpu_normal_system", "wt_gpu_solve_step",
-    "wt_gpu_solve_vertices", "wt_gpu_render_depth",
+    "wt_gpu_solve_vertices", "wt_gpu_render_depth", "wt_gpu_stream", "wt_gpu_track_async", "wt_gpu_sync",
+    "wt_gpu_profile_frame",
 ]
+KERNEL_KINDS = ["fk", "skin", "normals+bucket", "scatter", "search+average", "pose_system+solve",
+                "shape_step", "shape_stats"]
 
 
 class WarptrackError(RuntimeError):
@@ -156,6 +159,11 @@ def _declare(L: C.CDLL) -> None:
     L.wt_gpu_solve_vertices.argtypes = [C.c_int, C.c_int32, vp, vp, vp, vp, vp, P(ShapeConfig), vp,
                                         vp]
     L.wt_gpu_render_depth.argtypes = [vp, vp, vp, P(Noise), C.c_int32, vp, vp]
+    L.wt_gpu_stream.argtypes = [vp]
+    L.wt_gpu_stream.restype = vp
+    L.wt_gpu_track_async.argtypes = [vp, P(TrackConfigC)]
+    L.wt_gpu_sync.argtypes = [vp]
+    L.wt_gpu_profile_frame.argtypes = [vp, P(TrackConfigC), vp, vp, C.c_int32, P(C.c_int32)]
 
 
 def check(rc: int, ctx=None) -> None:

@@ -96,7 +96,7 @@ struct wt_gpu_ctx {
 
   // host model copies
   std::vector<wt::LinkDesc> links;
-  std::vector<int> pair_off, pair_theta, pair_link;
+  std::vector<int> pair_off, pair_theta, pair_link, pair_owner;
   std::vector<double> s_diag;
   std::vector<int> dominant;
 
@@ -143,10 +143,17 @@ struct wt_gpu_ctx {
   int* hook_cnt = nullptr;
   double* hook_res = nullptr;
 
+  // profiling: when set during capture, an event is recorded after every
+  // kernel so per-kernel device time inside the real frame graph is known
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_events;
+  std::vector<int> prof_kind;
+
   std::map<GraphKey, cudaGraphExec_t> graphs;
 
   ~wt_gpu_ctx() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
     if (h_kin) cudaFreeHost(h_kin);
     if (h_shape) cudaFreeHost(h_shape);
     if (stream) cudaStreamDestroy(stream);
@@ -175,6 +182,20 @@ int guarded(wt_gpu_ctx* ctx, F&& f) {
 void check_launch() {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw CudaError{WT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+// kernel kinds reported by wt_gpu_profile_frame
+enum { K_FK = 0, K_SKIN, K_NORMALS, K_SCATTER, K_SEARCH, K_POSE, K_SHAPE, K_SHAPE_AFTER, K_NKIND };
+
+void mark(wt_gpu_ctx* c, int kind) {
+  check_launch();
+  if (!c->prof_on) return;
+  cudaEvent_t e;
+  WT_CUDA(cudaEventCreate(&e));
+  // External: becomes an event-record node of the captured graph
+  WT_CUDA(cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal));
+  c->prof_events.push_back(e);
+  c->prof_kind.push_back(kind);
 }
 
 int vgrid(int n) { return std::max(1, (n + wt::kVThreads - 1) / wt::kVThreads); }
@@ -287,31 +308,27 @@ void ensure_stats(wt_gpu_ctx* c, int nk, int ns) {
 
 void enq_fk(wt_gpu_ctx* c, const wt::DevState& s) {
   wt::k_fk<<<1, 128, 0, c->stream>>>(c->dm, s);
-  check_launch();
+  mark(c, K_FK);
 }
 
 void enq_skin(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi) {
   wt::k_skin<<<vgrid(c->V), wt::kVThreads, sizeof(double) * 8 * c->L, c->stream>>>(c->dm, s, phi);
-  check_launch();
+  mark(c, K_SKIN);
 }
 
 void enq_normals(wt_gpu_ctx* c, const wt::DevState& s, bool bucket, bool zero_acc,
                  bool compute = true) {
-  wt::k_normals<<<vgrid(c->V), wt::kVThreads, bucket ? 4096 * sizeof(int) : 0, c->stream>>>(
+  wt::k_normals<<<vgrid(c->V), wt::kVThreads, 0, c->stream>>>(
       c->dm, s, c->din, bucket ? 1 : 0, zero_acc ? 1 : 0, compute ? 1 : 0);
-  check_launch();
+  mark(c, K_NORMALS);
 }
 
 void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
-  wt::k_scatter<<<vgrid(c->V), wt::kVThreads, 0, c->stream>>>(c->dm, s);
-  check_launch();
+  const int grid = std::max(1, std::min((c->V + wt::kScatterThreads - 1) / wt::kScatterThreads, 148));
+  wt::k_scatter<<<grid, wt::kScatterThreads, sizeof(int) * (c->NB + 1), c->stream>>>(c->dm, s, c->NB);
+  mark(c, K_SCATTER);
 }
 
-size_t search_smem(int window) {
-  const int halo = wt::kTile + 2 * window;
-  return sizeof(float4) * wt::kSearchCap + sizeof(unsigned) * wt::kSearchCap +
-         sizeof(int) * (halo * halo + 1);
-}
 
 void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, int* winners) {
   wt::DevFrame f{c->d_valid, c->d_pts_hi, c->d_active, c->d_nactive};
@@ -319,14 +336,16 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   sa.W = c->din.W;
   sa.H = c->din.H;
   sa.nbx = c->din.nbx;
+  sa.nbins = c->NB;
   sa.ntx = c->din.ntx;
   sa.window = a->window_radius;
   sa.cut2 = static_cast<float>(a->cutoff * a->cutoff);
   sa.cut2_hi = a->cutoff * a->cutoff;
   sa.write_winners = winners ? 1 : 0;
   sa.winners = winners;
-  wt::k_search<<<c->NTILE, wt::kSearchThreads, search_smem(a->window_radius), c->stream>>>(s, f, sa);
-  check_launch();
+  wt::k_search<<<c->NTILE, wt::kTile * wt::kTile * wt::kSearchTPP, wt::search_smem_bytes(), c->stream>>>(
+      s, f, sa);
+  mark(c, K_SEARCH);
 }
 
 void enq_associate(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, int* winners) {
@@ -336,7 +355,7 @@ void enq_associate(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* 
 }
 
 int pose_grid(const wt_gpu_ctx* c) {
-  return std::max(1, std::min((c->V + wt::kPoseThreads - 1) / wt::kPoseThreads, 2 * 148));
+  return std::max(1, std::min((c->V + wt::kPoseThreads - 1) / wt::kPoseThreads, 148));
 }
 
 void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt_kin_config* k,
@@ -354,7 +373,7 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
   pa.res_in = res_in;
   wt::k_pose_system<<<pose_grid(c), wt::kPoseThreads, wt::pose_smem_bytes(c->L, c->NP), c->stream>>>(
       c->dm, s, phi, pa);
-  check_launch();
+  mark(c, K_POSE);
 }
 
 int shape_grid(const wt_gpu_ctx* c) { return std::max(1, std::min(vgrid(c->V), 4 * 148)); }
@@ -369,7 +388,7 @@ void enq_shape(wt_gpu_ctx* c, const wt_shape_config* sc, int it, const double4* 
   sa.pad = 0;
   wt::k_shape<<<shape_grid(c), wt::kVThreads, sizeof(double) * 8 * c->L, c->stream>>>(c->dm, c->ds,
                                                                                      in, out, sa);
-  check_launch();
+  mark(c, K_SHAPE);
 }
 
 // optimize_pose (kinopt.cpp:132-171) as a static kernel sequence.
@@ -402,7 +421,7 @@ int enq_optimize_shape(wt_gpu_ctx* c, int cur, const wt_shape_config* sc, const 
     enq_skin(c, c->ds, c->phi[cur]);
     enq_associate(c, c->ds, a, nullptr);
     wt::k_shape_after<<<shape_grid(c), wt::kVThreads, 0, c->stream>>>(c->dm, c->ds, sc->iterations);
-    check_launch();
+    mark(c, K_SHAPE_AFTER);
   }
   return cur;
 }
@@ -574,6 +593,7 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
       for (int k : path) {
         c->pair_theta.push_back(k);
         c->pair_link.push_back(theta_to_link[static_cast<size_t>(k)]);
+        c->pair_owner.push_back(j);
       }
       c->pair_off.push_back(static_cast<int>(c->pair_theta.size()));
     }
@@ -656,6 +676,7 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     int* d_poff = c->mem.alloc<int>(L + 1);
     int* d_pth = c->mem.alloc<int>(std::max(1, c->NP));
     int* d_plk = c->mem.alloc<int>(std::max(1, c->NP));
+    int* d_pow = c->mem.alloc<int>(std::max(1, c->NP));
     double* d_s = c->mem.alloc<double>(L);
     upload(d_v0, v0.data(), V, c->stream);
     upload(d_wg, wg.data(), V, c->stream);
@@ -667,9 +688,10 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     upload(d_poff, c->pair_off.data(), L + 1, c->stream);
     upload(d_pth, c->pair_theta.data(), c->NP, c->stream);
     upload(d_plk, c->pair_link.data(), c->NP, c->stream);
+    upload(d_pow, c->pair_owner.data(), c->NP, c->stream);
     upload(d_s, c->s_diag.data(), L, c->stream);
     c->dm = wt::DevModel{V, L, c->NP, K, d_v0, d_wg, d_wl, d_roff, d_ring, d_nbr,
-                         d_links, d_poff, d_pth, d_plk, d_s};
+                         d_links, d_poff, d_pth, d_plk, d_pow, d_s};
 
     alloc_state(c, c->ds, false);
     c->hs = c->ds;  // hooks share the per-vertex buffers, own theta/fk/offsets/dchain
@@ -689,7 +711,10 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     ensure_stats(c, 16, 8);
 
     WT_CUDA(cudaFuncSetAttribute(wt::k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(search_smem(16))));
+                                 static_cast<int>(wt::search_smem_bytes())));
+    if (sizeof(int) * (c->NB + 1) > 227 * 1024) fail(WT_EINVAL, "image too large for the bin histogram");
+    WT_CUDA(cudaFuncSetAttribute(wt::k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(int) * (c->NB + 1))));
     WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(wt::pose_smem_bytes(L, c->NP))));
     WT_CUDA(cudaStreamSynchronize(c->stream));
@@ -819,6 +844,98 @@ int wt_gpu_track_loaded(wt_gpu_ctx* c, const wt_track_config* cfg, wt_frame_stat
       if (stats->shape) put_shape(c, ns, stats->shape, stats->cap_shape);
     }
     ++c->frame_index;
+  });
+}
+
+namespace {
+GraphKey track_key(const wt_gpu_ctx* c, const wt_track_config* cfg, bool shape_now, double tag) {
+  return GraphKey{{tag, static_cast<double>(cfg->kin.iterations), static_cast<double>(cfg->kin.assoc_refresh),
+                   cfg->kin.lambda_k, cfg->kin.lambda_s, cfg->kin.diag_floor,
+                   static_cast<double>(cfg->kin.clamp_limits), cfg->kin.limit,
+                   static_cast<double>(cfg->assoc.window_radius), cfg->assoc.cutoff, shape_now ? 1.0 : 0.0,
+                   static_cast<double>(cfg->shape.iterations), cfg->shape.lambda_phi, cfg->shape.lambda_nbr,
+                   cfg->shape.lambda_w, cfg->shape.diag_floor, static_cast<double>(cfg->shape_stats),
+                   static_cast<double>(c->cur)}};
+}
+
+void enq_track(wt_gpu_ctx* c, const wt_track_config* cfg, bool shape_now) {
+  enq_optimize_pose(c, &cfg->kin, &cfg->assoc);
+  if (shape_now)
+    enq_optimize_shape(c, c->cur, &cfg->shape, &cfg->assoc, cfg->shape_stats != 0, cfg->kin.iterations == 0);
+}
+}  // namespace
+
+void* wt_gpu_stream(wt_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int wt_gpu_sync(wt_gpu_ctx* c) {
+  if (!c) return WT_EINVAL;
+  return guarded(c, [&] { WT_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+
+int wt_gpu_track_async(wt_gpu_ctx* c, const wt_track_config* cfg) {
+  if (!c || !cfg) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    require_frame(c);
+    check_assoc(&cfg->assoc);
+    const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
+                           (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
+    ensure_stats(c, cfg->kin.iterations, cfg->shape.iterations);
+    const int start = c->cur;
+    run_graph(c, track_key(c, cfg, shape_now, 1.0), [&] { enq_track(c, cfg, shape_now); });
+    c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
+    ++c->frame_index;
+  });
+}
+
+int wt_gpu_profile_frame(wt_gpu_ctx* c, const wt_track_config* cfg, int32_t* kinds, float* ms, int32_t cap,
+                         int32_t* n_out) {
+  if (!c || !cfg) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    require_frame(c);
+    check_assoc(&cfg->assoc);
+    const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
+                           (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
+    ensure_stats(c, cfg->kin.iterations, cfg->shape.iterations);
+    for (cudaEvent_t e : c->prof_events) cudaEventDestroy(e);
+    c->prof_events.clear();
+    c->prof_kind.clear();
+    const int start = c->cur;
+    cudaEvent_t e0;
+    WT_CUDA(cudaEventCreate(&e0));
+    cudaGraph_t g;
+    c->prof_on = true;
+    WT_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      WT_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
+      enq_track(c, cfg, shape_now);
+    } catch (...) {
+      c->prof_on = false;
+      cudaStreamEndCapture(c->stream, &g);
+      throw;
+    }
+    c->prof_on = false;
+    WT_CUDA(cudaStreamEndCapture(c->stream, &g));
+    cudaGraphExec_t ex;
+    WT_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    WT_CUDA(cudaGraphLaunch(ex, c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    cudaGraphExecDestroy(ex);
+    c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
+    ++c->frame_index;
+    const int n = static_cast<int>(c->prof_events.size());
+    cudaEvent_t prev = e0;
+    for (int k = 0; k < n && k < cap; ++k) {
+      float t = 0.0f;
+      WT_CUDA(cudaEventElapsedTime(&t, prev, c->prof_events[k]));
+      if (ms) ms[k] = t;
+      if (kinds) kinds[k] = c->prof_kind[k];
+      prev = c->prof_events[k];
+    }
+    cudaEventDestroy(e0);
+    if (n_out) *n_out = n;
   });
 }
 

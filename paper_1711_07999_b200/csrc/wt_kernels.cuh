@@ -39,6 +39,7 @@ struct DevModel {
   const int* pair_off;     // [L+1] dchain pairs of each link
   const int* pair_theta;   // [NP] theta index k of the pair
   const int* pair_link;    // [NP] link driven by theta k
+  const int* pair_owner;   // [NP] link j the pair belongs to
   const double* s_diag;    // [L] influence counts S
 };
 
@@ -196,20 +197,31 @@ __device__ __forceinline__ bool blend_vertex(const double* s_off, double4 w, uch
 // FK / link offsets / dchain for the current theta (skeleton.cpp:56-108),
 // executed by one whole CTA. Also used by the pose-solve tail.
 
-__device__ void block_fk(const DevModel& m, const DevState& s, const double* theta) {
+__device__ void block_fk(const DevModel& m, const DevState& s, const double* theta_in) {
   __shared__ DQ fk[64];
-  if (threadIdx.x == 0) fk_all(m.links, m.L, theta, fk);
+  __shared__ DQ loc[64];
+  __shared__ int par[64];
+  __shared__ double th[64];
+  const int L = m.L;
+  for (int j = threadIdx.x; j < L; j += blockDim.x) th[j] = theta_in[j];
   __syncthreads();
-  for (int j = threadIdx.x; j < m.L; j += blockDim.x) {
+  // joint transforms and local offsets in parallel (one link per thread) ...
+  for (int j = threadIdx.x; j < L; j += blockDim.x) {
+    const LinkDesc& l = m.links[j];
+    par[j] = l.parent;
+    loc[j] = dq_compose(dq_load(l.offset), dq_joint(l.kind, l.axis, th[l.theta_index]));
+  }
+  __syncthreads();
+  // ... then the parent chain from shared memory (topological order)
+  if (threadIdx.x == 0)
+    for (int j = 0; j < L; ++j) fk[j] = par[j] < 0 ? loc[j] : dq_compose(fk[par[j]], loc[j]);
+  __syncthreads();
+  for (int j = threadIdx.x; j < L; j += blockDim.x) {
     dq_store(fk[j], s.fk + 8 * j);
     dq_store(dq_compose(fk[j], dq_load(m.links[j].bind_inv)), s.offsets + 8 * j);
   }
-  for (int p = threadIdx.x; p < m.NP; p += blockDim.x) {
-    // link j owning pair p
-    int j = 0;
-    while (m.pair_off[j + 1] <= p) ++j;
-    dq_store(d_link_offset(m.links, fk, theta, j, m.pair_link[p]), s.dchain + 8 * p);
-  }
+  for (int p = threadIdx.x; p < m.NP; p += blockDim.x)
+    dq_store(d_link_offset(m.links, fk, th, m.pair_owner[p], m.pair_link[p]), s.dchain + 8 * p);
 }
 
 __global__ void k_fk(DevModel m, DevState s) { block_fk(m, s, s.theta); }
@@ -283,7 +295,6 @@ __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, cons
 // ---------------------------------------------------------------------------
 // K2 normals (skinmesh.cpp:125-139) fused with K3a: back-face cull, projection
 // with lround semantics (association.cpp:29-37,49-51) and the bin histogram.
-// The last CTA scans the bin counts into offsets and clears them.
 
 __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, DevIntr in,
                                                        int do_bucket, int zero_acc, int compute) {
@@ -356,55 +367,55 @@ __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, D
       s.vslot[i] = slot | (lp << 26);
     }
   }
-  if (do_bucket && last_block(s.tickets + 0)) {
-    extern __shared__ int s_scan[];
-    const int nb = in.nbx * in.nby;
-    // scan in shared-memory pieces of 4096 bins, carrying the running total
-    int carry = 0;
-    for (int base = 0; base < nb; base += 4096) {
-      const int n = min(4096, nb - base);
-      for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        s_scan[k] = __ldcg(s.bin_count + base + k);
-        s.bin_count[base + k] = 0;
-      }
-      __syncthreads();
-      const int tot = block_exclusive_scan(s_scan, n);
-      for (int k = threadIdx.x; k < n; k += blockDim.x) s.bin_off[base + k] = s_scan[k] + carry;
-      carry += tot;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) s.bin_off[nb] = carry;
-  }
 }
 
 // K3c scatter into bin order (association.cpp:57-66, unordered within a bin:
 // the winner rule is a lexicographic (d^2, index) minimum, so bucket order
-// never changes a result).
-__global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevState s) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m.V) return;
-  const unsigned bin = s.vbin[i];
-  if (bin == kNoBin) return;
-  const unsigned sl = s.vslot[i];
-  const double4 v = s.pv[i];
-  const unsigned tag = (static_cast<unsigned>(i) << 6) | (sl >> 26);
-  s.items[s.bin_off[bin] + (sl & 0x03FFFFFFu)] =
-      make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(tag)));
+// never changes a result). Every CTA scans the (small, L2-resident) bin
+// histogram itself, so no grid-wide dependency or serial tail is needed;
+// CTA 0 publishes the offsets for the search.
+constexpr int kScatterThreads = 1024;
+
+__global__ void __launch_bounds__(kScatterThreads) k_scatter(DevModel m, DevState s, int nb) {
+  extern __shared__ int s_boff[];
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) s_boff[k] = __ldcg(s.bin_count + k);
+  if (threadIdx.x == 0) s_boff[nb] = 0;
+  __syncthreads();
+  block_exclusive_scan(s_boff, nb + 1);
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k <= nb; k += blockDim.x) s.bin_off[k] = s_boff[k];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
+    const unsigned bin = s.vbin[i];
+    if (bin == kNoBin) continue;
+    const unsigned sl = s.vslot[i];
+    const double4 v = s.pv[i];
+    const unsigned tag = (static_cast<unsigned>(i) << 6) | (sl >> 26);
+    s.items[s_boff[bin] + (sl & 0x03FFFFFFu)] =
+        make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(tag)));
+  }
 }
 
 // ---------------------------------------------------------------------------
 // K4 + K5: windowed nearest-vertex search (associate_winners,
 // association.cpp:69-109) and the scatter-average accumulation
-// (association.cpp:124-131) in one pass. One CTA per 16x16 pixel tile: the
-// bucketed vertices of the bins overlapping the tile's (16+2w)^2 halo are
-// staged in shared memory and re-bucketed per halo pixel, so each window row
-// is one contiguous span exactly as in the reference.
+// (association.cpp:124-131) in one pass. One CTA per 16x16 pixel tile with
+// TPP threads per pixel (window rows interleaved across them): the bucketed
+// vertices of the bins overlapping the tile's (16+2w)^2 halo are staged in
+// shared memory and re-bucketed per halo pixel, so every window row is one
+// contiguous span exactly as in the reference.
+//
+// Distances are evaluated in fp32 relative to a per-tile anchor (the first
+// valid pixel's point): fp64 differences rounded once keep ~1e-6 relative
+// precision on d^2. Whenever the runner-up is within kTieEps of the best (or
+// the best is within kTieEps of the cutoff) the pixel is re-decided with the
+// reference's exact fp64 ((dx*dx + dy*dy) + dz*dz), so the winner map equals
+// the reference's whenever the posed vertices do.
 
-// Relative band within which fp32 anchor-relative distances cannot order two
-// candidates reliably (their d^2 error is ~1e-6 relative); such pixels are
-// re-decided in fp64.
 constexpr float kTieEps = 1e-4f;
 constexpr float kTieAbs = 1e-12f;
+constexpr int kSearchTPP = 2;
+constexpr int kHaloMax = kTile + 2 * 16;
 
 __device__ __forceinline__ double exact_d2(double4 v, double px, double py, double pz) {
   const double dx = __dsub_rn(v.x, px), dy = __dsub_rn(v.y, py), dz = __dsub_rn(v.z, pz);
@@ -412,7 +423,7 @@ __device__ __forceinline__ double exact_d2(double4 v, double px, double py, doub
 }
 
 struct SearchArgs {
-  int W, H, nbx;
+  int W, H, nbx, nbins;
   int ntx;
   int window;
   float cut2;
@@ -421,42 +432,55 @@ struct SearchArgs {
   int* winners;
 };
 
-__global__ void __launch_bounds__(kSearchThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
+__host__ __device__ inline size_t search_smem_bytes() {
+  return sizeof(float4) * kSearchCap + sizeof(int) * (2 * (kHaloMax * kHaloMax + 1));
+}
+
+__device__ __forceinline__ bool lex_less(double x, int i, double bx, int bi) {
+  return x < bx || (x == bx && i < bi);
+}
+
+__global__ void __launch_bounds__(kTile * kTile * kSearchTPP) k_search(DevState s, DevFrame f,
+                                                                       SearchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   float4* sorted = reinterpret_cast<float4*>(smem);
-  unsigned* keys = reinterpret_cast<unsigned*>(sorted + kSearchCap);
-  int* off = reinterpret_cast<int*>(keys + kSearchCap);
+  int* off = reinterpret_cast<int*>(sorted + kSearchCap);
+  int* cur = off + (kHaloMax * kHaloMax + 1);
   __shared__ int bin_pref[64];
+  __shared__ int bin_base[64];
   __shared__ int bin_id[64];
   __shared__ int s_first;
+  const int nthr = blockDim.x;
 
+  // clear the bin histogram for the next association (scatter already read it)
+  for (int k = blockIdx.x * nthr + threadIdx.x; k < a.nbins; k += gridDim.x * nthr) s.bin_count[k] = 0;
   const int b = blockIdx.x;
   if (b >= *f.n_active) return;
   const int tile = f.active_tiles[b];
   const int tx = tile % a.ntx, ty = tile / a.ntx;
   const int tu0 = tx * kTile, tv0 = ty * kTile;
-  const int pu = tu0 + (threadIdx.x & (kTile - 1));
-  const int pv = tv0 + threadIdx.x / kTile;
+  const int lp_px = threadIdx.x / kSearchTPP;   // pixel within the tile
+  const int sub = threadIdx.x % kSearchTPP;     // row phase within the window
+  const int pu = tu0 + (lp_px & (kTile - 1));
+  const int pv = tv0 + lp_px / kTile;
   const int w = a.window;
   const bool inside = pu < a.W && pv < a.H;
   const int pix = inside ? pv * a.W + pu : 0;
   const bool valid = inside && f.valid[pix] != 0;
-  // Distances are evaluated in fp32 relative to a per-tile anchor (the first
-  // valid pixel's fp64 point): differences of fp64 positions rounded once,
-  // so d^2 keeps ~1e-6 relative precision instead of fp32 absolute
-  // coordinates' ~1e-4 near ties.
-  if (threadIdx.x == 0) s_first = kSearchThreads;
+  if (threadIdx.x == 0) s_first = kTile * kTile;
   __syncthreads();
-  if (valid) atomicMin(&s_first, static_cast<int>(threadIdx.x));
+  if (valid && sub == 0) atomicMin(&s_first, lp_px);
   __syncthreads();
   const int ap = (tv0 + s_first / kTile) * a.W + tu0 + (s_first & (kTile - 1));
   const double ax = f.pts_hi[3 * ap], ay = f.pts_hi[3 * ap + 1], az = f.pts_hi[3 * ap + 2];
-  float px = 0.f, py = 0.f, pz = 0.f;
+  double phx = 0.0, phy = 0.0, phz = 0.0;
   if (valid) {
-    px = static_cast<float>(f.pts_hi[3 * pix] - ax);
-    py = static_cast<float>(f.pts_hi[3 * pix + 1] - ay);
-    pz = static_cast<float>(f.pts_hi[3 * pix + 2] - az);
+    phx = f.pts_hi[3 * pix];
+    phy = f.pts_hi[3 * pix + 1];
+    phz = f.pts_hi[3 * pix + 2];
   }
+  const float px = static_cast<float>(phx - ax), py = static_cast<float>(phy - ay),
+              pz = static_cast<float>(phz - az);
 
   const int hu0 = max(0, tu0 - w), hv0 = max(0, tv0 - w);
   const int hu1 = min(a.W - 1, tu0 + kTile - 1 + w), hv1 = min(a.H - 1, tv0 + kTile - 1 + w);
@@ -464,14 +488,14 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(DevState s, DevFrame 
   const int bx0 = hu0 / kBin, bx1 = hu1 / kBin, by0 = hv0 / kBin, by1 = hv1 / kBin;
   const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);  // <= 49 for w <= 16
   if (threadIdx.x < 32) {
-    // prefix sums of the overlapped bins' item counts
     int carry = 0;
     for (int base = 0; base < nb; base += 32) {
       const int k = base + threadIdx.x;
-      int c = 0, id = 0;
+      int c = 0, id = 0, o0 = 0;
       if (k < nb) {
         id = (by0 + k / nbx) * a.nbx + (bx0 + k % nbx);
-        c = s.bin_off[id + 1] - s.bin_off[id];
+        o0 = s.bin_off[id];
+        c = s.bin_off[id + 1] - o0;
       }
       int x = c;
 #pragma unroll
@@ -481,6 +505,7 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(DevState s, DevFrame 
       }
       if (k < nb) {
         bin_pref[k] = carry + x - c;
+        bin_base[k] = o0 - (carry + x - c);  // item index = bin_base[k] + stream index
         bin_id[k] = id;
       }
       carry += __shfl_sync(0xffffffffu, x, 31);
@@ -489,74 +514,55 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(DevState s, DevFrame 
   }
   __syncthreads();
   const int total = bin_pref[nb];
-
-  // Exact winner across chunks: fp64 d^2 evaluated like the reference,
-  // ((dx*dx + dy*dy) + dz*dz) without FMA contraction.
-  double best_x = INFINITY;
-  int best_i = -1;
-  double phx = 0.0, phy = 0.0, phz = 0.0;
-  if (valid) {
-    phx = f.pts_hi[3 * pix];
-    phy = f.pts_hi[3 * pix + 1];
-    phz = f.pts_hi[3 * pix + 2];
-  }
   const int ncell = HU * HV;
+  const int r0 = max(pv - w, 0), r1 = min(pv + w, a.H - 1);
+  const int c0 = max(pu - w, 0) - hu0, c1 = min(pu + w, a.W - 1) - hu0;
+  const float cut_hi = a.cut2 * (1.0f + kTieEps);
+
+  double best_x = INFINITY;  // exact winner across chunks
+  int best_i = -1;
   for (int chunk = 0; chunk < total; chunk += kSearchCap) {
-    const int n = min(kSearchCap, total - chunk);
-    for (int k = threadIdx.x; k <= ncell; k += blockDim.x) off[k] = 0;
+    const int cend = min(total, chunk + kSearchCap);
+    for (int k = threadIdx.x; k <= ncell; k += nthr) off[k] = 0;
     __syncthreads();
-    // pass 1: halo pixel of every staged candidate, per-pixel slot
-    for (int c = threadIdx.x; c < n; c += blockDim.x) {
-      const int g = chunk + c;
-      int lo = 0, hi = nb;  // bin_pref[lo] <= g < bin_pref[hi]
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (bin_pref[mid] <= g) lo = mid;
-        else hi = mid;
+    // pass 1: per-halo-pixel counts (coalesced reads of each bin's items)
+    for (int k = 0; k < nb; ++k) {
+      const int lo = max(bin_pref[k], chunk), hi = min(bin_pref[k + 1], cend);
+      const int bid = bin_id[k];
+      const int bu = (bid % a.nbx) * kBin, bv = (bid / a.nbx) * kBin;
+      for (int g = lo + threadIdx.x; g < hi; g += nthr) {
+        const unsigned tag = static_cast<unsigned>(__double_as_longlong(s.items[bin_base[k] + g].w));
+        const int u = bu + (tag & 7u), v = bv + ((tag >> 3) & 7u);
+        if (u >= hu0 && u <= hu1 && v >= hv0 && v <= hv1) atomicAdd(&off[(v - hv0) * HU + (u - hu0)], 1);
       }
-      const int bid = bin_id[lo];
-      const double4 it = s.items[s.bin_off[bid] + (g - bin_pref[lo])];
-      const unsigned tag = static_cast<unsigned>(__double_as_longlong(it.w));
-      const int lp = tag & 63u;
-      const int u = (bid % a.nbx) * kBin + (lp % kBin);
-      const int v = (bid / a.nbx) * kBin + (lp / kBin);
-      unsigned key = 0xFFFFFFFFu;
-      if (u >= hu0 && u <= hu1 && v >= hv0 && v <= hv1) {
-        const int hp = (v - hv0) * HU + (u - hu0);
-        const int slot = atomicAdd(&off[hp], 1);
-        key = static_cast<unsigned>(hp) * kSearchCap + static_cast<unsigned>(slot);
-      }
-      keys[c] = key;
     }
     __syncthreads();
     block_exclusive_scan(off, ncell + 1);
     __syncthreads();
-    // pass 2: place candidates by halo pixel, anchor-relative (re-read hits L1)
-    for (int c = threadIdx.x; c < n; c += blockDim.x) {
-      const unsigned key = keys[c];
-      if (key == 0xFFFFFFFFu) continue;
-      const int g = chunk + c;
-      int lo = 0, hi = nb;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (bin_pref[mid] <= g) lo = mid;
-        else hi = mid;
+    for (int k = threadIdx.x; k < ncell; k += nthr) cur[k] = off[k];
+    __syncthreads();
+    // pass 2: place anchor-relative candidates by halo pixel (re-reads hit L1)
+    for (int k = 0; k < nb; ++k) {
+      const int lo = max(bin_pref[k], chunk), hi = min(bin_pref[k + 1], cend);
+      const int bid = bin_id[k];
+      const int bu = (bid % a.nbx) * kBin, bv = (bid / a.nbx) * kBin;
+      for (int g = lo + threadIdx.x; g < hi; g += nthr) {
+        const double4 it = s.items[bin_base[k] + g];
+        const unsigned tag = static_cast<unsigned>(__double_as_longlong(it.w));
+        const int u = bu + (tag & 7u), v = bv + ((tag >> 3) & 7u);
+        if (u >= hu0 && u <= hu1 && v >= hv0 && v <= hv1) {
+          const int pos = atomicAdd(&cur[(v - hv0) * HU + (u - hu0)], 1);
+          sorted[pos] = make_float4(static_cast<float>(it.x - ax), static_cast<float>(it.y - ay),
+                                    static_cast<float>(it.z - az), __uint_as_float(tag));
+        }
       }
-      const double4 it = s.items[s.bin_off[bin_id[lo]] + (g - bin_pref[lo])];
-      const unsigned tag = static_cast<unsigned>(__double_as_longlong(it.w));
-      sorted[off[key / kSearchCap] + (key % kSearchCap)] =
-          make_float4(static_cast<float>(it.x - ax), static_cast<float>(it.y - ay),
-                      static_cast<float>(it.z - az), __uint_as_float(tag));
     }
     __syncthreads();
+    // fp32 scan of this thread's window rows: best and runner-up
+    float bd = INFINITY, d2 = INFINITY;
+    int bi = -1;
     if (valid) {
-      const int r0 = max(pv - w, 0), r1 = min(pv + w, a.H - 1);
-      const int c0 = max(pu - w, 0) - hu0, c1 = min(pu + w, a.W - 1) - hu0;
-      // fp32 scan: best and runner-up within a slightly widened cutoff
-      const float cut_hi = a.cut2 * (1.0f + kTieEps);
-      float bd = INFINITY, d2 = INFINITY;
-      int bi = -1;
-      for (int r = r0; r <= r1; ++r) {
+      for (int r = r0 + sub; r <= r1; r += kSearchTPP) {
         const int row = (r - hv0) * HU;
         const int e0 = off[row + c0], e1 = off[row + c1 + 1];
         for (int e = e0; e < e1; ++e) {
@@ -575,44 +581,72 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(DevState s, DevFrame 
           }
         }
       }
-      if (bi >= 0) {
-        const float thr = bd * (1.0f + kTieEps) + kTieAbs;
-        if (d2 <= thr || bd >= a.cut2 * (1.0f - kTieEps)) {
-          // ambiguous (near-tie or near the cutoff): exact fp64 re-evaluation
-          for (int r = r0; r <= r1; ++r) {
-            const int row = (r - hv0) * HU;
-            const int e0 = off[row + c0], e1 = off[row + c1 + 1];
-            for (int e = e0; e < e1; ++e) {
-              const float4 c = sorted[e];
-              const float dx = c.x - px, dy = c.y - py, dz = c.z - pz;
-              if (dx * dx + dy * dy + dz * dz <= thr) {
-                const int vi = static_cast<int>(__float_as_uint(c.w) >> 6);
-                const double x = exact_d2(s.pv[vi], phx, phy, phz);
-                if (x <= a.cut2_hi && (x < best_x || (x == best_x && vi < best_i))) {
-                  best_x = x;
-                  best_i = vi;
-                }
+    }
+    // merge across the pixel's TPP lanes (contiguous lanes)
+#pragma unroll
+    for (int o = 1; o < kSearchTPP; o <<= 1) {
+      const float obd = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int obi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const float od2 = __shfl_xor_sync(0xffffffffu, d2, o);
+      const bool theirs = obd < bd || (obd == bd && obi < bi);
+      d2 = fminf(fminf(d2, od2), theirs ? bd : obd);
+      if (theirs) {
+        bd = obd;
+        bi = obi;
+      }
+    }
+    double cx = INFINITY;
+    int ci = -1;
+    if (valid && bi >= 0) {
+      const float thr = bd * (1.0f + kTieEps) + kTieAbs;
+      if (d2 <= thr || bd >= a.cut2 * (1.0f - kTieEps)) {
+        // ambiguous (near-tie or near the cutoff): exact fp64 re-evaluation
+        for (int r = r0 + sub; r <= r1; r += kSearchTPP) {
+          const int row = (r - hv0) * HU;
+          const int e0 = off[row + c0], e1 = off[row + c1 + 1];
+          for (int e = e0; e < e1; ++e) {
+            const float4 c = sorted[e];
+            const float dx = c.x - px, dy = c.y - py, dz = c.z - pz;
+            if (dx * dx + dy * dy + dz * dz <= thr) {
+              const int vi = static_cast<int>(__float_as_uint(c.w) >> 6);
+              const double x = exact_d2(s.pv[vi], phx, phy, phz);
+              if (x <= a.cut2_hi && lex_less(x, vi, cx, ci)) {
+                cx = x;
+                ci = vi;
               }
             }
           }
-        } else {
-          const double x = exact_d2(s.pv[bi], phx, phy, phz);
-          if (x <= a.cut2_hi && (x < best_x || (x == best_x && bi < best_i))) {
-            best_x = x;
-            best_i = bi;
-          }
+        }
+      } else if (sub == 0) {
+        const double x = exact_d2(s.pv[bi], phx, phy, phz);
+        if (x <= a.cut2_hi) {
+          cx = x;
+          ci = bi;
         }
       }
     }
+#pragma unroll
+    for (int o = 1; o < kSearchTPP; o <<= 1) {
+      const double ox = __shfl_xor_sync(0xffffffffu, cx, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
+      if (oi >= 0 && (ci < 0 || lex_less(ox, oi, cx, ci))) {
+        cx = ox;
+        ci = oi;
+      }
+    }
+    if (ci >= 0 && (best_i < 0 || lex_less(cx, ci, best_x, best_i))) {
+      best_x = cx;
+      best_i = ci;
+    }
     __syncthreads();
   }
-  if (valid) {
+  if (valid && sub == 0) {
     if (a.write_winners) a.winners[pix] = best_i;
     if (best_i >= 0) {
       unsigned long long* acc = s.acc + 4 * static_cast<size_t>(best_i);
-      red_add(acc + 0, fix(f.pts_hi[3 * pix], kFixPoint));
-      red_add(acc + 1, fix(f.pts_hi[3 * pix + 1], kFixPoint));
-      red_add(acc + 2, fix(f.pts_hi[3 * pix + 2], kFixPoint));
+      red_add(acc + 0, fix(phx, kFixPoint));
+      red_add(acc + 1, fix(phy, kFixPoint));
+      red_add(acc + 2, fix(phz, kFixPoint));
       red_add(acc + 3, 1ll);
     }
   }
@@ -756,9 +790,12 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevSta
   unsigned short* ea = reinterpret_cast<unsigned short*>(flag + kPoseThreads + 1);
   unsigned short* eb = ea + NE;
 
+#pragma unroll 4
   for (int k = threadIdx.x; k < 8 * L; k += blockDim.x) s_off[k] = s.offsets[k];
+#pragma unroll 8
   for (int k = threadIdx.x; k < 8 * m.NP; k += blockDim.x) s_dch[k] = s.dchain[k];
   for (int k = threadIdx.x; k <= L; k += blockDim.x) s_poff[k] = m.pair_off[k];
+#pragma unroll 4
   for (int k = threadIdx.x; k < m.NP; k += blockDim.x) s_pth[k] = m.pair_theta[k];
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
     esum[e] = 0.0;

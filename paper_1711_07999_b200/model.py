@@ -255,17 +255,21 @@ def _smooth01(t: np.ndarray) -> np.ndarray:
 
 def _capsule(p0, axis, length, r0, r1, h, vbase):
     """Tapered capsule (hemispherical caps r0/r1 joined by a frustum) around
-    the segment p0 -> p0 + axis*length, tessellated at spacing ~h. Returns
-    (positions [n,3], height-along-axis [n], polys)."""
+    the segment p0 -> p0 + axis*length, in the layout of append_capsule
+    (synth.cpp:365-422): a pole, rings, a pole; quads between rings and pole
+    fans. Segments ~ 2 pi r / h (8..24), caps and body rings chosen for
+    near-square quads. Returns (positions [n,3], height-along-axis [n], polys)."""
     a = np.asarray(axis, float)
     a = a / np.linalg.norm(a)
     ref = np.array([1.0, 0, 0]) if abs(a[0]) < 0.9 else np.array([0, 0, 1.0])
     b = np.cross(a, ref)
     b /= np.linalg.norm(b)
     c = np.cross(b, a)
-    seg = max(8, int(round(2 * math.pi * max(r0, r1) / h)))
-    caps = max(2, int(round(0.5 * math.pi * max(r0, r1) / h)))
-    body = max(1, int(round(length / h)))
+    rmax = max(r0, r1)
+    seg = int(min(24, max(8, round(2 * math.pi * rmax / h))))
+    step = 2 * math.pi * rmax / seg
+    caps = max(2, int(round(seg / 4)))
+    body = max(1, int(round(length / step)))
     rings = []
     for i in range(1, caps + 1):
         ang = -math.pi / 2 + (math.pi / 2) * i / caps
@@ -336,7 +340,7 @@ def _humanoid_at(h: float, depth: float) -> ModelBundle:
             off = tuple(pd / np.linalg.norm(pd) * pb[6])
         off = np.asarray(off, float)
         if par < 0:
-            off = off + np.array([0.0, 0.0, depth])
+            off = off + np.array([0.03, 0.0, depth])
             origins.append(off)
         else:
             origins.append(origins[par] + off)
@@ -383,25 +387,31 @@ def _humanoid_at(h: float, depth: float) -> ModelBundle:
         polys=polys, link_names=[b[0] for b in _HUMANOID], name="humanoid20")
 
 
-def make_humanoid(target_vertices: int = 100_000, depth: float = 2.2, neighbors: int = 4) -> ModelBundle:
-    """20-link humanoid (one prismatic root, hinges on x/y/z axes) over tapered
-    capsules with near-uniform vertex spacing solved to hit target_vertices
-    (within ~2%). Placed `depth` metres in front of the camera, head up in
-    the image. Finalized, with k-NN neighbour sets."""
-    lo, hi = 1e-3, 0.2
-    for _ in range(40):
+def make_humanoid(target_vertices: int = 100_000, depth: float = 2.2, neighbors: int = 4,
+                  levels: int | None = None) -> ModelBundle:
+    """20-link humanoid (one prismatic root, hinges about x/y/z axes): a coarse
+    capsule rig refined by `levels` Catmull-Clark subdivisions (the reference
+    tracks subdivided templates, acceptance.cpp:543-548), with the coarse
+    spacing solved so the result has ~target_vertices (within ~3%). Placed
+    `depth` metres in front of the camera, head up in the image, 3 cm off the
+    optical axis. Finalized, with k-NN neighbour sets."""
+    if levels is None:
+        levels = 1 if target_vertices < 20_000 else (2 if target_vertices <= 200_000 else 3)
+    base_target = target_vertices / (4.0 ** levels)
+    lo, hi = 1e-3, 0.5
+    best = None
+    for _ in range(60):
         mid = math.sqrt(lo * hi)
         n = _humanoid_at(mid, depth).vertex_count
-        if n > target_vertices:
+        if best is None or abs(n - base_target) < abs(best[1] - base_target):
+            best = (mid, n)
+        if n > base_target:
             lo = mid
         else:
             hi = mid
-        if abs(n - target_vertices) <= 0.01 * target_vertices:
-            break
-    b = _humanoid_at(mid, depth)
+    b = _humanoid_at(best[0], depth)
     b.finalize()
-    b.with_neighbors(neighbors)
-    return b
+    return subdivide(b, levels, neighbors) if levels > 0 else b.with_neighbors(neighbors)
 
 
 def humanoid_trajectory(L: int, frame: int, fps: float = 30.0, phase_offset: float = 0.0) -> np.ndarray:
@@ -416,3 +426,190 @@ def humanoid_trajectory(L: int, frame: int, fps: float = 30.0, phase_offset: flo
     theta = amp * np.sin(2 * math.pi * freq * t + ph)
     theta[0] = 0.02 * math.sin(2 * math.pi * 0.3 * t + phase_offset)
     return theta
+
+
+# ---------------------------------------------------------------------------
+# Catmull-Clark subdivision (subdivide, skinmesh.cpp:249-511): positions, phi
+# and skin weights follow the position scheme; weights are then truncated to
+# the four largest entries (ties to the lower link) and renormalised. Sums are
+# accumulated in the reference's order so results agree to the last bit.
+
+def _cc_once(pos, phi, W, faces):
+    nv = pos.shape[0]
+    nf = len(faces)
+    # edges in order of first appearance (face order, side order)
+    edge_index = {}
+    ea, eb, ef0, ef1, nfe = [], [], [], [], []
+    face_edges = []
+    for f, poly in enumerate(faces):
+        fe = []
+        n = len(poly)
+        for s in range(n):
+            a, b = poly[s], poly[(s + 1) % n]
+            key = (a, b) if a < b else (b, a)
+            e = edge_index.get(key)
+            if e is None:
+                e = len(ea)
+                edge_index[key] = e
+                ea.append(key[0])
+                eb.append(key[1])
+                ef0.append(f)
+                ef1.append(-1)
+                nfe.append(1)
+            else:
+                if nfe[e] >= 2:
+                    raise ValueError(f"edge ({key[0]}, {key[1]}) has more than two incident faces")
+                ef1[e] = f
+                nfe[e] += 1
+            fe.append(e)
+        face_edges.append(fe)
+    ne = len(ea)
+    ea, eb, ef0, ef1, nfe = map(np.asarray, (ea, eb, ef0, ef1, nfe))
+    sizes = np.fromiter((len(p) for p in faces), dtype=np.int64, count=nf)
+    maxn = int(sizes.max()) if nf else 0
+    pad = np.zeros((nf, maxn), dtype=np.int64)
+    for f, p in enumerate(faces):
+        pad[f, :len(p)] = p
+    face_base, edge_base = nv + ne, nv
+
+    # face points: sum of pos * (1/n) in vertex order
+    c = 1.0 / sizes.astype(np.float64)
+    fp = np.zeros((nf, 3))
+    fph = np.zeros((nf, 3))
+    fw = np.zeros((nf, W.shape[1]))
+    for k in range(maxn):
+        m = k < sizes
+        idx = pad[m, k]
+        fp[m] += pos[idx] * c[m, None]
+        fph[m] += phi[idx] * c[m, None]
+        fw[m] += W[idx] * c[m, None]
+
+    # edge points
+    two = nfe == 2
+    epos = np.empty((ne, 3))
+    ephi = np.empty((ne, 3))
+    ew = np.empty((ne, W.shape[1]))
+    f0, f1 = ef0, np.where(two, ef1, 0)
+    epos[two] = (((pos[ea[two]] + pos[eb[two]]) + fp[f0[two]]) + fp[f1[two]]) * 0.25
+    ephi[two] = (((phi[ea[two]] + phi[eb[two]]) + fph[f0[two]]) + fph[f1[two]]) * 0.25
+    ew[two] = (((0.25 * W[ea[two]] + 0.25 * W[eb[two]]) + 0.25 * fw[f0[two]]) + 0.25 * fw[f1[two]])
+    bd = ~two
+    epos[bd] = (pos[ea[bd]] + pos[eb[bd]]) * 0.5
+    ephi[bd] = (phi[ea[bd]] + phi[eb[bd]]) * 0.5
+    ew[bd] = 0.5 * W[ea[bd]] + 0.5 * W[eb[bd]]
+
+    # vertex points
+    vdeg = np.bincount(np.concatenate([ea, eb]), minlength=nv)
+    # (vertex, edge) pairs in edge order, (vertex, face) pairs in face order
+    pv_e = np.empty(2 * ne, dtype=np.int64)
+    pv_e[0::2], pv_e[1::2] = ea, eb
+    pe = np.repeat(np.arange(ne), 2)
+    order = np.argsort(pv_e, kind="stable")  # per vertex: ascending edge index
+    ve_v, ve_e = pv_e[order], pe[order]
+    fl = pad[sizes[:, None] > np.arange(maxn)[None, :]]
+    ff = np.repeat(np.arange(nf), sizes)
+    order = np.argsort(fl, kind="stable")
+    vf_v, vf_f = fl[order], ff[order]
+    vnf = np.bincount(vf_v, minlength=nv)
+    boundary = np.zeros(nv, bool)
+    boundary[ve_v[nfe[ve_e] < 2]] = True
+    npos, nphi, nw = pos.copy(), phi.copy(), W.copy()
+    inter = (vdeg > 0) & ~boundary
+    # interior rule (F + 2R + (n-3)P)/n
+    favg = np.zeros((nv, 3))
+    fphi = np.zeros((nv, 3))
+    np.add.at(favg, vf_v, fp[vf_f])
+    np.add.at(fphi, vf_v, fph[vf_f])
+    fwv = np.zeros_like(W)
+    cf = 1.0 / np.maximum(vnf, 1).astype(np.float64)
+    np.add.at(fwv, vf_v, fw[vf_f] * cf[vf_v][:, None])
+    favg /= np.maximum(vnf, 1)[:, None]
+    fphi /= np.maximum(vnf, 1)[:, None]
+    rsum = np.zeros((nv, 3))
+    rphi = np.zeros((nv, 3))
+    np.add.at(rsum, ve_v, (pos[ea[ve_e]] + pos[eb[ve_e]]) * 0.5)
+    np.add.at(rphi, ve_v, (phi[ea[ve_e]] + phi[eb[ve_e]]) * 0.5)
+    nn = np.maximum(vdeg, 1).astype(np.float64)
+    rsum /= nn[:, None]
+    rphi /= nn[:, None]
+    rw = np.zeros_like(W)
+    seq_v = np.repeat(ve_v, 2)
+    seq_src = np.empty(2 * len(ve_e), dtype=np.int64)
+    seq_src[0::2], seq_src[1::2] = ea[ve_e], eb[ve_e]
+    np.add.at(rw, seq_v, W[seq_src] * (0.5 / nn[seq_v])[:, None])
+    i = np.where(inter)[0]
+    n_i = nn[i][:, None]
+    npos[i] = (favg[i] + 2.0 * rsum[i] + (n_i - 3.0) * pos[i]) / n_i
+    nphi[i] = (fphi[i] + 2.0 * rphi[i] + (n_i - 3.0) * phi[i]) / n_i
+    nw[i] = ((fwv[i] * (1.0 / n_i)) + rw[i] * (2.0 / n_i)) + W[i] * ((n_i - 3.0) / n_i)
+    # boundary (crease) rule (m1 + 6P + m2)/8, rarely used by our rigs
+    for v in np.where(boundary)[0]:
+        p = np.zeros(3)
+        ph = np.zeros(3)
+        wm = np.zeros(W.shape[1])
+        for e in ve_e[ve_v == v]:
+            if nfe[e] < 2:
+                other = eb[e] if ea[e] == v else ea[e]
+                p += (pos[v] + pos[other]) * 0.5
+                ph += (phi[v] + phi[other]) * 0.5
+                wm += (0.5 / 8.0) * W[v]
+                wm += (0.5 / 8.0) * W[other]
+        npos[v] = p / 8.0 + pos[v] * (6.0 / 8.0)
+        nphi[v] = ph / 8.0 + phi[v] * (6.0 / 8.0)
+        nw[v] = wm + (6.0 / 8.0) * W[v]
+
+    out_pos = np.concatenate([npos, epos, fp])
+    out_phi = np.concatenate([nphi, ephi, fph])
+    out_w = np.concatenate([nw, ew, fw])
+    new_faces = []
+    for f, poly in enumerate(faces):
+        n = len(poly)
+        fe = face_edges[f]
+        for s in range(n):
+            new_faces.append([poly[s], edge_base + fe[s], face_base + f, edge_base + fe[(s + n - 1) % n]])
+    return out_pos, out_phi, out_w, new_faces
+
+
+def _truncate_weights(W: np.ndarray):
+    """truncate_weights (skinmesh.cpp:274-289): four largest (ties to the lower
+    link), summed in that order, re-sorted by link, zeros dropped, renormalised."""
+    nv, L = W.shape
+    order = np.argsort(-W, axis=1, kind="stable")[:, :4]
+    top = np.take_along_axis(W, order, axis=1)
+    s = np.zeros(nv)
+    for k in range(min(4, L)):
+        s = s + top[:, k]
+    by_link = np.sort(order, axis=1)
+    wl = np.take_along_axis(W, by_link, axis=1)
+    keep = wl > 0.0
+    cnt = keep.sum(axis=1).astype(np.int32)
+    links = np.full((nv, 4), -1, np.int32)
+    wts = np.zeros((nv, 4))
+    rank = np.cumsum(keep, axis=1) - 1
+    rows = np.repeat(np.arange(nv), keep.sum(axis=1))
+    links[rows, rank[keep]] = by_link[keep]
+    wts[rows, rank[keep]] = (wl / s[:, None])[keep]
+    if L < 4:
+        links, wts = links[:, :4], wts[:, :4]
+    return cnt, links, wts
+
+
+def subdivide(b: ModelBundle, iterations: int, neighbors: int = 4) -> ModelBundle:
+    """subdivide (skinmesh.cpp:490-511) + build_neighbors(v0, 4), as the
+    reference's Python binding subdivide_model does (bindings.cpp:154-161)."""
+    L = b.link_count
+    W = np.zeros((b.vertex_count, L))
+    for s in range(4):
+        m = s < b.weight_count
+        np.add.at(W, (np.where(m)[0], b.weight_link[m, s]), b.weight[m, s] * 1.0)
+    pos = b.v0.copy()
+    phi = b.phi.copy() if b.phi is not None and b.phi.shape == b.v0.shape else np.zeros_like(b.v0)
+    faces = [list(p) for p in b.polys]
+    for _ in range(iterations):
+        pos, phi, W, faces = _cc_once(pos, phi, W, faces)
+    cnt, links, wts = _truncate_weights(W)
+    out = replace(b, v0=pos, phi=phi, weight_count=cnt, weight_link=links, weight=wts, polys=faces,
+                  triangles=None, vtri_offsets=None, vtri_items=None, nbr_offsets=None, nbr_items=None)
+    out.finalize()
+    out.with_neighbors(neighbors)
+    return out

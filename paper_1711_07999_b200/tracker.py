@@ -282,15 +282,17 @@ class Tracker:
         return jtj, jtr
 
     def render_depth(self, theta, phi=None, sigma=0.0, dropout=0.0, quantization=0.0, seed=0,
-                     frame: int = 0, out: np.ndarray | None = None):
-        """synthesize_frame (synth.cpp:229-270) on the GPU: (depth [H,W] f32, joint_visible [L])."""
+                     frame: int = 0, out_ptr: int | None = None):
+        """synthesize_frame (synth.cpp:229-270) on the GPU: (depth [H,W] f32, joint_visible [L]).
+        With out_ptr (a device or host address of H*W floats) the depth is
+        written there and None is returned in its place."""
         th = _f64(theta, (self.bundle.link_count,))
         ph = None if phi is None else _f64(phi, (self.bundle.vertex_count, 3))
-        depth = out if out is not None else np.zeros((self.intr.height, self.intr.width), np.float32)
+        depth = None if out_ptr is not None else np.zeros((self.intr.height, self.intr.width), np.float32)
         vis = np.zeros(self.bundle.link_count, np.uint8)
         nz = _lib.Noise(sigma, dropout, quantization, seed)
-        check(lib().wt_gpu_render_depth(self._ctx, ptr(th), ptr(ph), C.byref(nz), frame, ptr(depth), ptr(vis)),
-              self._ctx)
+        check(lib().wt_gpu_render_depth(self._ctx, ptr(th), ptr(ph), C.byref(nz), frame,
+                                        out_ptr if out_ptr is not None else ptr(depth), ptr(vis)), self._ctx)
         return depth, vis
 
 
