@@ -301,8 +301,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     per_kind = {}
     nprof = 3
     nker = 0
+    # profile frames that follow the tracker's state (steady tracking)
+    trackers[0].set_state(theta=trajectory(bundle, args.warmup, rank * S), phi=np.zeros((bundle.vertex_count, 3)),
+                          frame_index=1)
     for rep in range(nprof):
-        f = 1 + rep
+        f = args.warmup + 1 + rep
         W.check(L.wt_gpu_load_depth(trackers[0]._ctx, frames_dev[0][f].data_ptr(), 1.0), trackers[0]._ctx)
         W.check(L.wt_gpu_profile_frame(trackers[0]._ctx, C.byref(ccfg), kinds, ms, 512, C.byref(n)),
                 trackers[0]._ctx)
@@ -313,7 +316,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             d[0] += ms[k]
             d[1] += 1
     # association statistics for the byte model
-    st = trackers[0].track_frame(cfg, depth=frames_host[0][args.warmup].numpy())
+    st = trackers[0].track_frame(cfg, depth=frames_host[0][args.warmup + nprof + 1].numpy())
     A = st.kin[-1].associated if st and st.kin else bundle.vertex_count // 4
     Vvis = bundle.vertex_count // 2
     kernels = {}

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -92,7 +93,7 @@ struct wt_gpu_ctx {
   int V = 0, L = 0, NP = 0, K = 0, T = 0;
   wt_intrinsics intr{};
   wt::DevIntr din{};
-  int P = 0, NB = 0, NTILE = 0;
+  int P = 0;
 
   // host model copies
   std::vector<wt::LinkDesc> links;
@@ -113,10 +114,11 @@ struct wt_gpu_ctx {
   float* d_depth = nullptr;
   uint8_t* d_valid = nullptr;
   double* d_pts_hi = nullptr;
-  int* d_active = nullptr;
-  int* d_nactive = nullptr;
+  int* d_vlist = nullptr;
+  int* d_nvalid = nullptr;
   int* d_winners = nullptr;
   bool frame_loaded = false;
+  bool frame_on_rays = false;  // depth frame: every point on its pixel's centre ray
 
   // stats
   int cap_kin = 0, cap_shape = 0;
@@ -268,17 +270,19 @@ void alloc_state(wt_gpu_ctx* c, wt::DevState& s, bool hook) {
   if (!hook) {
     s.pv = c->mem.alloc<double4>(c->V);
     s.pn = c->mem.alloc<float4>(c->V);
-    s.vbin = c->mem.alloc<unsigned>(c->V);
-    s.vslot = c->mem.alloc<unsigned>(c->V);
-    s.bin_count = c->mem.alloc<int>(c->NB);
-    s.bin_off = c->mem.alloc<int>(c->NB + 1);
+    s.vpix = c->mem.alloc<int>(c->V);
+    s.vslot = c->mem.alloc<int>(c->V);
+    s.pix_cnt = c->mem.alloc<int>(c->P);
+    s.row_cnt = c->mem.alloc<int>(c->din.H);
+    s.poff = c->mem.alloc<int>(c->P + 1);
     s.items = c->mem.alloc<double4>(c->V);
     s.acc = c->mem.alloc<unsigned long long>(4 * static_cast<size_t>(std::max(1, c->V)));
     const int NE = c->L * (c->L + 1) / 2 + c->L + 8;
     s.red = c->mem.alloc<unsigned long long>(NE);
     s.tickets = c->mem.alloc<unsigned>(8);
     s.sys_out = c->mem.alloc<double>(c->L * c->L + c->L);
-    WT_CUDA(cudaMemsetAsync(s.bin_count, 0, sizeof(int) * c->NB, c->stream));
+    WT_CUDA(cudaMemsetAsync(s.pix_cnt, 0, sizeof(int) * c->P, c->stream));
+    WT_CUDA(cudaMemsetAsync(s.row_cnt, 0, sizeof(int) * c->din.H, c->stream));
     WT_CUDA(cudaMemsetAsync(s.acc, 0, sizeof(unsigned long long) * 4 * std::max(1, c->V), c->stream));
     WT_CUDA(cudaMemsetAsync(s.red, 0, sizeof(unsigned long long) * NE, c->stream));
     WT_CUDA(cudaMemsetAsync(s.tickets, 0, sizeof(unsigned) * 8, c->stream));
@@ -324,27 +328,28 @@ void enq_normals(wt_gpu_ctx* c, const wt::DevState& s, bool bucket, bool zero_ac
 }
 
 void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
-  const int grid = std::max(1, std::min((c->V + wt::kScatterThreads - 1) / wt::kScatterThreads, 148));
-  wt::k_scatter<<<grid, wt::kScatterThreads, sizeof(int) * (c->NB + 1), c->stream>>>(c->dm, s, c->NB);
+  wt::k_pixoff<<<c->din.H, wt::kVThreads, sizeof(int) * c->din.W, c->stream>>>(s, c->din.W, c->din.H);
+  mark(c, K_SCATTER);
+  wt::k_scatter<<<vgrid(std::max(c->V, c->din.H)), wt::kVThreads, 0, c->stream>>>(c->dm, s, c->din.H);
   mark(c, K_SCATTER);
 }
 
-
 void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, int* winners) {
-  wt::DevFrame f{c->d_valid, c->d_pts_hi, c->d_active, c->d_nactive};
+  wt::DevFrame f{c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid};
   wt::SearchArgs sa;
+  sa.fx = c->din.fx;
+  sa.fy = c->din.fy;
+  sa.cx = c->din.cx;
+  sa.cy = c->din.cy;
+  sa.prune = c->frame_on_rays ? 1 : 0;
   sa.W = c->din.W;
   sa.H = c->din.H;
-  sa.nbx = c->din.nbx;
-  sa.nbins = c->NB;
-  sa.ntx = c->din.ntx;
   sa.window = a->window_radius;
-  sa.cut2 = static_cast<float>(a->cutoff * a->cutoff);
-  sa.cut2_hi = a->cutoff * a->cutoff;
+  sa.cut2 = a->cutoff * a->cutoff;
   sa.write_winners = winners ? 1 : 0;
   sa.winners = winners;
-  wt::k_search<<<c->NTILE, wt::kTile * wt::kTile * wt::kSearchTPP, wt::search_smem_bytes(), c->stream>>>(
-      s, f, sa);
+  const int grid = std::max(1, std::min(vgrid(c->P), 4 * 148));
+  wt::k_search<<<grid, wt::kVThreads, 0, c->stream>>>(s, f, sa);
   mark(c, K_SEARCH);
 }
 
@@ -557,13 +562,7 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     c->din.cy = intr->cy;
     c->din.W = intr->width;
     c->din.H = intr->height;
-    c->din.nbx = (intr->width + wt::kBin - 1) / wt::kBin;
-    c->din.nby = (intr->height + wt::kBin - 1) / wt::kBin;
-    c->din.ntx = (intr->width + wt::kTile - 1) / wt::kTile;
-    c->din.nty = (intr->height + wt::kTile - 1) / wt::kTile;
     c->P = intr->width * intr->height;
-    c->NB = c->din.nbx * c->din.nby;
-    c->NTILE = c->din.ntx * c->din.nty;
     const int L = c->L, V = c->V;
 
     // skeleton: bind pose = FK(0), ancestors, dchain pairs (skeleton.cpp:7-50)
@@ -705,16 +704,12 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     c->d_depth = c->mem.alloc<float>(c->P);
     c->d_valid = c->mem.alloc<uint8_t>(c->P);
     c->d_pts_hi = c->mem.alloc<double>(3 * static_cast<size_t>(c->P));
-    c->d_active = c->mem.alloc<int>(c->NTILE);
-    c->d_nactive = c->mem.alloc<int>(1);
+    c->d_vlist = c->mem.alloc<int>(c->P);
+    c->d_nvalid = c->mem.alloc<int>(1);
     c->d_winners = c->mem.alloc<int>(c->P);
     ensure_stats(c, 16, 8);
-
-    WT_CUDA(cudaFuncSetAttribute(wt::k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(wt::search_smem_bytes())));
-    if (sizeof(int) * (c->NB + 1) > 227 * 1024) fail(WT_EINVAL, "image too large for the bin histogram");
-    WT_CUDA(cudaFuncSetAttribute(wt::k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sizeof(int) * (c->NB + 1))));
+    WT_CUDA(cudaFuncSetAttribute(wt::k_pixoff, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(int) * intr->width)));
     WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(wt::pose_smem_bytes(L, c->NP))));
     WT_CUDA(cudaStreamSynchronize(c->stream));
@@ -774,11 +769,9 @@ int wt_gpu_get_state(wt_gpu_ctx* c, double* theta, double* phi, int32_t* frame_i
 
 static void ingest(wt_gpu_ctx* c, const float* depth_dev, double scale, const double* cloud_dev,
                    const uint8_t* valid_dev) {
-  WT_CUDA(cudaMemsetAsync(c->d_nactive, 0, sizeof(int), c->stream));
-  const dim3 grid(c->din.ntx, c->din.nty);
-  wt::k_ingest<<<grid, wt::kSearchThreads, 0, c->stream>>>(c->din, depth_dev, scale, cloud_dev,
-                                                           valid_dev, c->d_valid, c->d_pts_hi,
-                                                           c->d_active, c->d_nactive);
+  WT_CUDA(cudaMemsetAsync(c->d_nvalid, 0, sizeof(int), c->stream));
+  wt::k_ingest<<<vgrid(c->P), wt::kVThreads, 0, c->stream>>>(c->din, depth_dev, scale, cloud_dev, valid_dev,
+                                                              c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid);
   check_launch();
 }
 
@@ -789,6 +782,7 @@ int wt_gpu_load_depth(wt_gpu_ctx* c, const float* depth, double depth_scale) {
     WT_CUDA(cudaMemcpyAsync(c->d_depth, depth, sizeof(float) * c->P, cudaMemcpyDefault, c->stream));
     ingest(c, c->d_depth, depth_scale, nullptr, nullptr);
     c->frame_loaded = true;
+    c->frame_on_rays = true;
   });
 }
 
@@ -800,6 +794,7 @@ int wt_gpu_load_cloud(wt_gpu_ctx* c, const double* points, const uint8_t* valid)
     WT_CUDA(cudaMemcpyAsync(c->d_valid, valid, c->P, cudaMemcpyDefault, c->stream));
     ingest(c, nullptr, 1.0, c->d_pts_hi, c->d_valid);
     c->frame_loaded = true;
+    c->frame_on_rays = false;
   });
 }
 

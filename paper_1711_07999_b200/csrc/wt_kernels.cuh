@@ -16,16 +16,11 @@
 
 namespace wt {
 
-constexpr int kBin = 8;         // vertex-bucket bin edge in pixels (8x8 bins)
-constexpr int kTile = 16;       // search tile edge: one CTA per 16x16 pixels
-constexpr int kSearchThreads = kTile * kTile;
-constexpr int kSearchCap = 2048;  // candidates staged in shared memory per pass
-constexpr int kVThreads = 256;    // per-vertex kernels
+constexpr int kVThreads = 256;    // per-vertex / per-pixel kernels
 constexpr int kPoseThreads = 128; // rows per CTA in the normal-equation kernel
 constexpr double kFixPoint = 4294967296.0;        // 2^32: observation sums
 constexpr double kFixSys = 1099511627776.0;       // 2^40: JtJ / Jtr / shape sums
 constexpr double kFixRes = 17592186044416.0;      // 2^44: residual sum of squares
-constexpr unsigned kNoBin = 0xFFFFFFFFu;
 
 struct DevModel {
   int V, L, NP, K;
@@ -46,8 +41,6 @@ struct DevModel {
 struct DevIntr {
   double fx, fy, cx, cy;
   int W, H;
-  int nbx, nby;   // bins
-  int ntx, nty;   // search tiles
 };
 
 struct KinStat {      // per pose iteration (device)
@@ -70,11 +63,12 @@ struct DevState {
   double* dchain;     // [NP*8]
   double4* pv;        // posed vertices (x,y,z, blend ok), fp64
   float4* pn;         // normals (x,y,z, valid)
-  unsigned* vbin;     // bin id or kNoBin
-  unsigned* vslot;    // slot in bin | local pixel << 26
-  int* bin_count;     // [NB] (self-cleaning)
-  int* bin_off;       // [NB+1]
-  double4* items;     // bucketed vertices (x,y,z, bits: vi<<6 | local pixel)
+  int* vpix;          // bucket pixel (row-major) or -1
+  int* vslot;         // slot within the pixel's bucket
+  int* pix_cnt;       // [P] bucket sizes (self-cleaning: cleared by k_pixoff)
+  int* row_cnt;       // [H] bucketed vertices per image row (cleared by k_scatter)
+  int* poff;          // [P+1] row-major pixel offsets: the VertexBuckets CSR
+  double4* items;     // bucketed vertices in pixel order (x,y,z, bits: vertex index)
   unsigned long long* acc;   // [V*4] fixed-point sum x,y,z + count
   unsigned long long* red;   // reduction slots (self-cleaning)
   unsigned* tickets;         // last-CTA tickets (self-cleaning)
@@ -86,8 +80,8 @@ struct DevState {
 struct DevFrame {
   const uint8_t* valid;  // per pixel
   const double* pts_hi;  // per pixel fp64 point (valid pixels only)
-  const int* active_tiles;
-  const int* n_active;
+  const int* vlist;      // valid pixel indices
+  const int* n_valid;
 };
 
 // ---------------------------------------------------------------------------
@@ -159,6 +153,33 @@ __device__ int block_exclusive_scan(int* a, int n) {
   return carry;
 }
 
+// Block-wide sum of a double and an int (result valid in thread 0).
+__device__ __forceinline__ void block_sum2(double& d, long long& n) {
+  __shared__ double sd[32];
+  __shared__ long long sn[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    sd[wid] = d;
+    sn[wid] = n;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    d = 0.0;
+    n = 0;
+    for (int k = 0; k < nw; ++k) {  // fixed order
+      d += sd[k];
+      n += sn[k];
+    }
+  }
+  __syncthreads();
+}
+
 // Loads link offsets (and optionally the dchain) into shared memory.
 __device__ __forceinline__ void load_offsets(const DevModel& m, const DevState& s, double* s_off) {
   for (int i = threadIdx.x; i < m.L * 8; i += blockDim.x) s_off[i] = s.offsets[i];
@@ -227,18 +248,17 @@ __device__ void block_fk(const DevModel& m, const DevState& s, const double* the
 __global__ void k_fk(DevModel m, DevState s) { block_fk(m, s, s.theta); }
 
 // ---------------------------------------------------------------------------
-// frame ingest: depth_to_cloud (seqio.cpp:419-437) and the active-tile list.
+// frame ingest: depth_to_cloud (seqio.cpp:419-437) in fp64 and the list of
+// valid pixels (warp-aggregated append keeps row neighbours adjacent).
 
-__global__ void __launch_bounds__(kSearchThreads) k_ingest(DevIntr in, const float* depth,
-                                                           double scale, const double* cloud,
-                                                           const uint8_t* cloud_valid, uint8_t* pvalid,
-                                                           double* pts_hi, int* active_tiles,
-                                                           int* n_active) {
-  const int u = blockIdx.x * kTile + (threadIdx.x & (kTile - 1));
-  const int v = blockIdx.y * kTile + (threadIdx.x / kTile);
+__global__ void __launch_bounds__(kVThreads) k_ingest(DevIntr in, const float* depth, double scale,
+                                                      const double* cloud, const uint8_t* cloud_valid,
+                                                      uint8_t* pvalid, double* pts_hi, int* vlist,
+                                                      int* n_valid) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   int valid = 0;
-  if (u < in.W && v < in.H) {
-    const int i = v * in.W + u;
+  if (i < in.W * in.H) {
+    const int u = i % in.W, v = i / in.W;
     double x = 0, y = 0, z = 0;
     if (depth) {
       const float d = depth[i];
@@ -263,8 +283,11 @@ __global__ void __launch_bounds__(kSearchThreads) k_ingest(DevIntr in, const flo
       pts_hi[3 * i + 2] = z;
     }
   }
-  if (__syncthreads_or(valid) && threadIdx.x == 0)
-    active_tiles[atomicAdd(n_active, 1)] = blockIdx.y * in.ntx + blockIdx.x;
+  const unsigned m = __ballot_sync(0xffffffffu, valid);
+  int base = 0;
+  if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(n_valid, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (valid) vlist[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = i;
 }
 
 // ---------------------------------------------------------------------------
@@ -340,82 +363,87 @@ __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, D
       reinterpret_cast<ulonglong2*>(s.acc)[2 * i + 1] = make_ulonglong2(0ull, 0ull);
     }
     if (do_bucket) {
-      unsigned bin = kNoBin;
-      unsigned lp = 0;
+      // bucket_occupancy (association.cpp:39-56): per-pixel slot and per-row
+      // count, both warp-aggregated
+      int pix = -1, row = -1;
       if (valid && !(nx * vx + ny * vy + nz * vz > 0.0) && vz > 0.0) {
         const double pu = in.fx * vx / vz + in.cx;
         const double pvv = in.fy * vy / vz + in.cy;
         const double ru = round(pu), rv = round(pvv);  // half away from zero, like lround
         if (ru >= 0.0 && rv >= 0.0 && ru < in.W && rv < in.H) {
-          const int iu = static_cast<int>(ru), iv = static_cast<int>(rv);
-          bin = static_cast<unsigned>((iv / kBin) * in.nbx + (iu / kBin));
-          lp = static_cast<unsigned>((iv % kBin) * kBin + (iu % kBin));
+          row = static_cast<int>(rv);
+          pix = row * in.W + static_cast<int>(ru);
         }
       }
-      // warp-aggregated histogram update: one atomic per distinct bin
-      const unsigned peers = __match_any_sync(__activemask(), bin);
-      unsigned slot = 0;
-      if (bin != kNoBin) {
+      const unsigned act = __activemask();
+      const int lane = threadIdx.x & 31;
+      unsigned peers = __match_any_sync(act, pix);
+      int slot = 0;
+      if (pix >= 0) {
         const int leader = __ffs(peers) - 1;
-        const int lane = threadIdx.x & 31;
-        unsigned base = 0;
-        if (lane == leader) base = atomicAdd(&s.bin_count[bin], __popc(peers));
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&s.pix_cnt[pix], __popc(peers));
         base = __shfl_sync(peers, base, leader);
         slot = base + __popc(peers & ((1u << lane) - 1u));
       }
-      s.vbin[i] = bin;
-      s.vslot[i] = slot | (lp << 26);
+      peers = __match_any_sync(act, row);
+      if (row >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s.row_cnt[row], __popc(peers));
+      s.vpix[i] = pix;
+      s.vslot[i] = slot;
     }
   }
 }
 
-// K3c scatter into bin order (association.cpp:57-66, unordered within a bin:
-// the winner rule is a lexicographic (d^2, index) minimum, so bucket order
-// never changes a result). Every CTA scans the (small, L2-resident) bin
-// histogram itself, so no grid-wide dependency or serial tail is needed;
-// CTA 0 publishes the offsets for the search.
-constexpr int kScatterThreads = 1024;
-
-__global__ void __launch_bounds__(kScatterThreads) k_scatter(DevModel m, DevState s, int nb) {
-  extern __shared__ int s_boff[];
-  for (int k = threadIdx.x; k < nb; k += blockDim.x) s_boff[k] = __ldcg(s.bin_count + k);
-  if (threadIdx.x == 0) s_boff[nb] = 0;
-  __syncthreads();
-  block_exclusive_scan(s_boff, nb + 1);
-  __syncthreads();
-  if (blockIdx.x == 0)
-    for (int k = threadIdx.x; k <= nb; k += blockDim.x) s.bin_off[k] = s_boff[k];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
-    const unsigned bin = s.vbin[i];
-    if (bin == kNoBin) continue;
-    const unsigned sl = s.vslot[i];
-    const double4 v = s.pv[i];
-    const unsigned tag = (static_cast<unsigned>(i) << 6) | (sl >> 26);
-    s.items[s_boff[bin] + (sl & 0x03FFFFFFu)] =
-        make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(tag)));
+// K3b: row-major pixel offsets of the bucket CSR (association.cpp:58-59),
+// one CTA per image row: its base is the sum of the preceding rows' counts,
+// then a shared-memory scan of the row. Clears the per-pixel counts.
+__global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, int H) {
+  extern __shared__ int s_row[];
+  const int row = blockIdx.x;
+  long long part = 0;
+  for (int k = threadIdx.x; k < row; k += blockDim.x) part += __ldcg(s.row_cnt + k);
+  double dummy = 0.0;
+  block_sum2(dummy, part);
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = static_cast<int>(part);
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    s_row[c] = __ldcg(s.pix_cnt + row * W + c);
+    s.pix_cnt[row * W + c] = 0;
   }
+  __syncthreads();
+  const int total = block_exclusive_scan(s_row, W);
+  const int base = s_base;
+  for (int c = threadIdx.x; c < W; c += blockDim.x) s.poff[row * W + c] = base + s_row[c];
+  if (row == H - 1 && threadIdx.x == 0) s.poff[W * H] = base + total;
+}
+
+// K3c: scatter into pixel order (association.cpp:60-66; unordered within a
+// pixel -- the winner rule is a lexicographic (d^2, index) minimum, so bucket
+// order never changes a result). Clears the row counts for the next pass.
+__global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevState s, int H) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < H) s.row_cnt[i] = 0;
+  if (i >= m.V) return;
+  const int pix = s.vpix[i];
+  if (pix < 0) return;
+  const double4 v = s.pv[i];
+  s.items[s.poff[pix] + s.vslot[i]] = make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(i)));
 }
 
 // ---------------------------------------------------------------------------
 // K4 + K5: windowed nearest-vertex search (associate_winners,
 // association.cpp:69-109) and the scatter-average accumulation
-// (association.cpp:124-131) in one pass. One CTA per 16x16 pixel tile with
-// TPP threads per pixel (window rows interleaved across them): the bucketed
-// vertices of the bins overlapping the tile's (16+2w)^2 halo are staged in
-// shared memory and re-bucketed per halo pixel, so every window row is one
-// contiguous span exactly as in the reference.
+// (association.cpp:124-131), one thread per valid pixel. Window rows are
+// contiguous spans of the bucket CSR as in the reference, and every distance
+// is the reference's exact fp64 ((dx*dx + dy*dy) + dz*dz) (no FMA), so the
+// winner map equals the reference's whenever the posed vertices do.
 //
-// Distances are evaluated in fp32 relative to a per-tile anchor (the first
-// valid pixel's point): fp64 differences rounded once keep ~1e-6 relative
-// precision on d^2. Whenever the runner-up is within kTieEps of the best (or
-// the best is within kTieEps of the cutoff) the pixel is re-decided with the
-// reference's exact fp64 ((dx*dx + dy*dy) + dz*dz), so the winner map equals
-// the reference's whenever the posed vertices do.
-
-constexpr float kTieEps = 1e-4f;
-constexpr float kTieAbs = 1e-12f;
-constexpr int kSearchTPP = 2;
-constexpr int kHaloMax = kTile + 2 * 16;
+// Rings: for depth frames every point lies on its pixel's centre ray, so a
+// vertex bucketed in Chebyshev ring k is at least lb(k) away (lround buckets
+// put it (k - 1/2)/f off the ray in normalised coordinates on one axis; the
+// half-space {x/z >= t + d} is d z / sqrt(1 + (t + d)^2) from the point).
+// Scanning rings outward and stopping once lb(k)^2 exceeds the best (or the
+// cutoff) yields the full-window answer from a few rings.
 
 __device__ __forceinline__ double exact_d2(double4 v, double px, double py, double pz) {
   const double dx = __dsub_rn(v.x, px), dy = __dsub_rn(v.y, py), dz = __dsub_rn(v.z, pz);
@@ -423,230 +451,76 @@ __device__ __forceinline__ double exact_d2(double4 v, double px, double py, doub
 }
 
 struct SearchArgs {
-  int W, H, nbx, nbins;
-  int ntx;
+  double fx, fy, cx, cy;
+  int prune;  // points lie on their pixel's centre ray (depth frames)
+  int W, H;
   int window;
-  float cut2;
-  double cut2_hi;  // cutoff^2 in fp64, the reference's test (association.cpp:98)
+  double cut2;  // cutoff^2 (association.cpp:75,98)
   int write_winners;
   int* winners;
 };
 
-__host__ __device__ inline size_t search_smem_bytes() {
-  return sizeof(float4) * kSearchCap + sizeof(int) * (2 * (kHaloMax * kHaloMax + 1));
+__device__ __forceinline__ double ring_lb2(int k, double atx, double aty, double z, const SearchArgs& a) {
+  const double dx = (k - 0.5) / a.fx, dy = (k - 0.5) / a.fy;
+  const double tx = atx + dx, ty = aty + dy;
+  const double b = fmin(dx / sqrt(1.0 + tx * tx), dy / sqrt(1.0 + ty * ty)) * z;
+  return b * b * (1.0 - 1e-9);
 }
 
-__device__ __forceinline__ bool lex_less(double x, int i, double bx, int bi) {
-  return x < bx || (x == bx && i < bi);
+__device__ __forceinline__ void scan_span(const DevState& s, int e0, int e1, double px, double py, double pz,
+                                          double cut2, double& best_x, int& best_i) {
+  for (int e = e0; e < e1; ++e) {
+    const double2* q = reinterpret_cast<const double2*>(s.items + e);
+    const double2 a01 = __ldg(q), a23 = __ldg(q + 1);
+    const double x = exact_d2(make_double4(a01.x, a01.y, a23.x, 0.0), px, py, pz);
+    const int vi = static_cast<int>(__double_as_longlong(a23.y));
+    if (x <= cut2 && (x < best_x || (x == best_x && vi < best_i))) {
+      best_x = x;
+      best_i = vi;
+    }
+  }
 }
 
-__global__ void __launch_bounds__(kTile * kTile * kSearchTPP) k_search(DevState s, DevFrame f,
-                                                                       SearchArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  float4* sorted = reinterpret_cast<float4*>(smem);
-  int* off = reinterpret_cast<int*>(sorted + kSearchCap);
-  int* cur = off + (kHaloMax * kHaloMax + 1);
-  __shared__ int bin_pref[64];
-  __shared__ int bin_base[64];
-  __shared__ int bin_id[64];
-  __shared__ int s_first;
-  const int nthr = blockDim.x;
-
-  // clear the bin histogram for the next association (scatter already read it)
-  for (int k = blockIdx.x * nthr + threadIdx.x; k < a.nbins; k += gridDim.x * nthr) s.bin_count[k] = 0;
-  const int b = blockIdx.x;
-  if (b >= *f.n_active) return;
-  const int tile = f.active_tiles[b];
-  const int tx = tile % a.ntx, ty = tile / a.ntx;
-  const int tu0 = tx * kTile, tv0 = ty * kTile;
-  const int lp_px = threadIdx.x / kSearchTPP;   // pixel within the tile
-  const int sub = threadIdx.x % kSearchTPP;     // row phase within the window
-  const int pu = tu0 + (lp_px & (kTile - 1));
-  const int pv = tv0 + lp_px / kTile;
+__global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
+  const int nv = *f.n_valid;
   const int w = a.window;
-  const bool inside = pu < a.W && pv < a.H;
-  const int pix = inside ? pv * a.W + pu : 0;
-  const bool valid = inside && f.valid[pix] != 0;
-  if (threadIdx.x == 0) s_first = kTile * kTile;
-  __syncthreads();
-  if (valid && sub == 0) atomicMin(&s_first, lp_px);
-  __syncthreads();
-  const int ap = (tv0 + s_first / kTile) * a.W + tu0 + (s_first & (kTile - 1));
-  const double ax = f.pts_hi[3 * ap], ay = f.pts_hi[3 * ap + 1], az = f.pts_hi[3 * ap + 2];
-  double phx = 0.0, phy = 0.0, phz = 0.0;
-  if (valid) {
-    phx = f.pts_hi[3 * pix];
-    phy = f.pts_hi[3 * pix + 1];
-    phz = f.pts_hi[3 * pix + 2];
-  }
-  const float px = static_cast<float>(phx - ax), py = static_cast<float>(phy - ay),
-              pz = static_cast<float>(phz - az);
-
-  const int hu0 = max(0, tu0 - w), hv0 = max(0, tv0 - w);
-  const int hu1 = min(a.W - 1, tu0 + kTile - 1 + w), hv1 = min(a.H - 1, tv0 + kTile - 1 + w);
-  const int HU = hu1 - hu0 + 1, HV = hv1 - hv0 + 1;
-  const int bx0 = hu0 / kBin, bx1 = hu1 / kBin, by0 = hv0 / kBin, by1 = hv1 / kBin;
-  const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);  // <= 49 for w <= 16
-  if (threadIdx.x < 32) {
-    int carry = 0;
-    for (int base = 0; base < nb; base += 32) {
-      const int k = base + threadIdx.x;
-      int c = 0, id = 0, o0 = 0;
-      if (k < nb) {
-        id = (by0 + k / nbx) * a.nbx + (bx0 + k % nbx);
-        o0 = s.bin_off[id];
-        c = s.bin_off[id + 1] - o0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += gridDim.x * blockDim.x) {
+    const int pix = f.vlist[j];
+    const int pu = pix % a.W, pv = pix / a.W;
+    const double px = f.pts_hi[3 * pix], py = f.pts_hi[3 * pix + 1], pz = f.pts_hi[3 * pix + 2];
+    const double atx = fabs((pu - a.cx) / a.fx), aty = fabs((pv - a.cy) / a.fy);
+    double best_x = INFINITY;
+    int best_i = -1;
+    for (int k = 0; k <= w; ++k) {
+      if (k > 0 && a.prune) {
+        const double lb = ring_lb2(k, atx, aty, pz, a);
+        if (lb > a.cut2 || lb > best_x) break;  // no vertex of ring >= k can win or tie
       }
-      int x = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if ((threadIdx.x & 31) >= o) x += y;
+      // ring k: top and bottom rows as spans, then the side columns
+      const int c0 = max(pu - k, 0), c1 = min(pu + k, a.W - 1);
+      if (pv - k >= 0) {
+        const int r = (pv - k) * a.W;
+        scan_span(s, s.poff[r + c0], s.poff[r + c1 + 1], px, py, pz, a.cut2, best_x, best_i);
       }
-      if (k < nb) {
-        bin_pref[k] = carry + x - c;
-        bin_base[k] = o0 - (carry + x - c);  // item index = bin_base[k] + stream index
-        bin_id[k] = id;
+      if (k > 0 && pv + k < a.H) {
+        const int r = (pv + k) * a.W;
+        scan_span(s, s.poff[r + c0], s.poff[r + c1 + 1], px, py, pz, a.cut2, best_x, best_i);
       }
-      carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    if (threadIdx.x == 0) bin_pref[nb] = carry;
-  }
-  __syncthreads();
-  const int total = bin_pref[nb];
-  const int ncell = HU * HV;
-  const int r0 = max(pv - w, 0), r1 = min(pv + w, a.H - 1);
-  const int c0 = max(pu - w, 0) - hu0, c1 = min(pu + w, a.W - 1) - hu0;
-  const float cut_hi = a.cut2 * (1.0f + kTieEps);
-
-  double best_x = INFINITY;  // exact winner across chunks
-  int best_i = -1;
-  for (int chunk = 0; chunk < total; chunk += kSearchCap) {
-    const int cend = min(total, chunk + kSearchCap);
-    for (int k = threadIdx.x; k <= ncell; k += nthr) off[k] = 0;
-    __syncthreads();
-    // pass 1: per-halo-pixel counts (coalesced reads of each bin's items)
-    for (int k = 0; k < nb; ++k) {
-      const int lo = max(bin_pref[k], chunk), hi = min(bin_pref[k + 1], cend);
-      const int bid = bin_id[k];
-      const int bu = (bid % a.nbx) * kBin, bv = (bid / a.nbx) * kBin;
-      for (int g = lo + threadIdx.x; g < hi; g += nthr) {
-        const unsigned tag = static_cast<unsigned>(__double_as_longlong(s.items[bin_base[k] + g].w));
-        const int u = bu + (tag & 7u), v = bv + ((tag >> 3) & 7u);
-        if (u >= hu0 && u <= hu1 && v >= hv0 && v <= hv1) atomicAdd(&off[(v - hv0) * HU + (u - hu0)], 1);
-      }
-    }
-    __syncthreads();
-    block_exclusive_scan(off, ncell + 1);
-    __syncthreads();
-    for (int k = threadIdx.x; k < ncell; k += nthr) cur[k] = off[k];
-    __syncthreads();
-    // pass 2: place anchor-relative candidates by halo pixel (re-reads hit L1)
-    for (int k = 0; k < nb; ++k) {
-      const int lo = max(bin_pref[k], chunk), hi = min(bin_pref[k + 1], cend);
-      const int bid = bin_id[k];
-      const int bu = (bid % a.nbx) * kBin, bv = (bid / a.nbx) * kBin;
-      for (int g = lo + threadIdx.x; g < hi; g += nthr) {
-        const double4 it = s.items[bin_base[k] + g];
-        const unsigned tag = static_cast<unsigned>(__double_as_longlong(it.w));
-        const int u = bu + (tag & 7u), v = bv + ((tag >> 3) & 7u);
-        if (u >= hu0 && u <= hu1 && v >= hv0 && v <= hv1) {
-          const int pos = atomicAdd(&cur[(v - hv0) * HU + (u - hu0)], 1);
-          sorted[pos] = make_float4(static_cast<float>(it.x - ax), static_cast<float>(it.y - ay),
-                                    static_cast<float>(it.z - az), __uint_as_float(tag));
+      if (k > 0) {
+        const int r0 = max(pv - k + 1, 0), r1 = min(pv + k - 1, a.H - 1);
+        for (int rr = r0; rr <= r1; ++rr) {
+          const int r = rr * a.W;
+          if (pu - k >= 0) scan_span(s, s.poff[r + pu - k], s.poff[r + pu - k + 1], px, py, pz, a.cut2, best_x, best_i);
+          if (pu + k < a.W) scan_span(s, s.poff[r + pu + k], s.poff[r + pu + k + 1], px, py, pz, a.cut2, best_x, best_i);
         }
       }
     }
-    __syncthreads();
-    // fp32 scan of this thread's window rows: best and runner-up
-    float bd = INFINITY, d2 = INFINITY;
-    int bi = -1;
-    if (valid) {
-      for (int r = r0 + sub; r <= r1; r += kSearchTPP) {
-        const int row = (r - hv0) * HU;
-        const int e0 = off[row + c0], e1 = off[row + c1 + 1];
-        for (int e = e0; e < e1; ++e) {
-          const float4 c = sorted[e];
-          const float dx = c.x - px, dy = c.y - py, dz = c.z - pz;
-          const float d = dx * dx + dy * dy + dz * dz;
-          if (d <= cut_hi) {
-            const int vi = static_cast<int>(__float_as_uint(c.w) >> 6);
-            if (d < bd || (d == bd && vi < bi)) {
-              d2 = bd;
-              bd = d;
-              bi = vi;
-            } else {
-              d2 = fminf(d2, d);
-            }
-          }
-        }
-      }
-    }
-    // merge across the pixel's TPP lanes (contiguous lanes)
-#pragma unroll
-    for (int o = 1; o < kSearchTPP; o <<= 1) {
-      const float obd = __shfl_xor_sync(0xffffffffu, bd, o);
-      const int obi = __shfl_xor_sync(0xffffffffu, bi, o);
-      const float od2 = __shfl_xor_sync(0xffffffffu, d2, o);
-      const bool theirs = obd < bd || (obd == bd && obi < bi);
-      d2 = fminf(fminf(d2, od2), theirs ? bd : obd);
-      if (theirs) {
-        bd = obd;
-        bi = obi;
-      }
-    }
-    double cx = INFINITY;
-    int ci = -1;
-    if (valid && bi >= 0) {
-      const float thr = bd * (1.0f + kTieEps) + kTieAbs;
-      if (d2 <= thr || bd >= a.cut2 * (1.0f - kTieEps)) {
-        // ambiguous (near-tie or near the cutoff): exact fp64 re-evaluation
-        for (int r = r0 + sub; r <= r1; r += kSearchTPP) {
-          const int row = (r - hv0) * HU;
-          const int e0 = off[row + c0], e1 = off[row + c1 + 1];
-          for (int e = e0; e < e1; ++e) {
-            const float4 c = sorted[e];
-            const float dx = c.x - px, dy = c.y - py, dz = c.z - pz;
-            if (dx * dx + dy * dy + dz * dz <= thr) {
-              const int vi = static_cast<int>(__float_as_uint(c.w) >> 6);
-              const double x = exact_d2(s.pv[vi], phx, phy, phz);
-              if (x <= a.cut2_hi && lex_less(x, vi, cx, ci)) {
-                cx = x;
-                ci = vi;
-              }
-            }
-          }
-        }
-      } else if (sub == 0) {
-        const double x = exact_d2(s.pv[bi], phx, phy, phz);
-        if (x <= a.cut2_hi) {
-          cx = x;
-          ci = bi;
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 1; o < kSearchTPP; o <<= 1) {
-      const double ox = __shfl_xor_sync(0xffffffffu, cx, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
-      if (oi >= 0 && (ci < 0 || lex_less(ox, oi, cx, ci))) {
-        cx = ox;
-        ci = oi;
-      }
-    }
-    if (ci >= 0 && (best_i < 0 || lex_less(cx, ci, best_x, best_i))) {
-      best_x = cx;
-      best_i = ci;
-    }
-    __syncthreads();
-  }
-  if (valid && sub == 0) {
     if (a.write_winners) a.winners[pix] = best_i;
     if (best_i >= 0) {
       unsigned long long* acc = s.acc + 4 * static_cast<size_t>(best_i);
-      red_add(acc + 0, fix(phx, kFixPoint));
-      red_add(acc + 1, fix(phy, kFixPoint));
-      red_add(acc + 2, fix(phz, kFixPoint));
+      red_add(acc + 0, fix(px, kFixPoint));
+      red_add(acc + 1, fix(py, kFixPoint));
+      red_add(acc + 2, fix(pz, kFixPoint));
       red_add(acc + 3, 1ll);
     }
   }
@@ -718,33 +592,6 @@ __device__ void block_cholesky_solve(int L, double* A, const double* b, double* 
   }
   __syncthreads();
   *ok = s_ok;
-}
-
-// Block-wide sum of a double and an int (result valid in thread 0).
-__device__ __forceinline__ void block_sum2(double& d, long long& n) {
-  __shared__ double sd[32];
-  __shared__ long long sn[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    d += __shfl_xor_sync(0xffffffffu, d, o);
-    n += __shfl_xor_sync(0xffffffffu, n, o);
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (lane == 0) {
-    sd[wid] = d;
-    sn[wid] = n;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    d = 0.0;
-    n = 0;
-    for (int k = 0; k < nw; ++k) {  // fixed order
-      d += sd[k];
-      n += sn[k];
-    }
-  }
-  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
