@@ -121,6 +121,39 @@ WT_HD DQ dq_djoint(int kind, const double* axis, double theta) {
   return h;
 }
 
+// Joint transform / derivative from the precomputed half-angle cos/sin
+// (c, s) = (cos(theta/2), sin(theta/2)); theta itself for prismatic joints.
+WT_HD DQ dq_joint_cs(int kind, const double* axis, double theta, double c, double s) {
+  DQ h = dq_identity();
+  if (kind == 0) {
+    h.r[0] = c;
+    h.r[1] = axis[0] * s;
+    h.r[2] = axis[1] * s;
+    h.r[3] = axis[2] * s;
+  } else {
+    h.d[1] = axis[0] * theta * 0.5;
+    h.d[2] = axis[1] * theta * 0.5;
+    h.d[3] = axis[2] * theta * 0.5;
+  }
+  return h;
+}
+
+WT_HD DQ dq_djoint_cs(int kind, const double* axis, double c, double s) {
+  DQ h;
+  for (int k = 0; k < 4; ++k) h.r[k] = h.d[k] = 0.0;
+  if (kind == 0) {
+    h.r[0] = -0.5 * s;
+    h.r[1] = axis[0] * (0.5 * c);
+    h.r[2] = axis[1] * (0.5 * c);
+    h.r[3] = axis[2] * (0.5 * c);
+  } else {
+    h.d[1] = axis[0] * 0.5;
+    h.d[2] = axis[1] * 0.5;
+    h.d[3] = axis[2] * 0.5;
+  }
+  return h;
+}
+
 // Rigid action of a unit DQ on a point (dualquat.cpp:88-96).
 WT_HD void dq_transform_point(const DQ& h, const double* p, double* out) {
   const double ux = h.r[1], uy = h.r[2], uz = h.r[3], w = h.r[0];

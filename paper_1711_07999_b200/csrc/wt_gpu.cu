@@ -144,6 +144,7 @@ struct wt_gpu_ctx {
 
   int* hook_cnt = nullptr;
   double* hook_res = nullptr;
+  long long* pose_dbg = nullptr;  // WT_DEBUG_POSE: last-CTA timing of the pose kernel
 
   // profiling: when set during capture, an event is recorded after every
   // kernel so per-kernel device time inside the real frame graph is known
@@ -359,8 +360,29 @@ void enq_associate(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* 
   enq_search(c, s, a, winners);
 }
 
+int pose_threads(const wt_gpu_ctx* c) { return c->L <= 40 ? 256 : 128; }
+
 int pose_grid(const wt_gpu_ctx* c) {
-  return std::max(1, std::min((c->V + wt::kPoseThreads - 1) / wt::kPoseThreads, 148));
+  const int warps = pose_threads(c) / 32;
+  return std::max(1, std::min((c->V + 32 * warps - 1) / (32 * warps), 2 * 148));
+}
+
+// JtJ entries per lane (upper triangle + Jtr) held in registers
+int pose_q(int L) {
+  const int ne = L * (L + 1) / 2 + L;
+  return ne <= 32 * 8 ? 8 : ne <= 32 * 16 ? 16 : ne <= 32 * 32 ? 32 : 68;
+}
+
+template <int Q>
+void launch_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt::PoseArgs& pa) {
+  wt::k_pose_system<Q><<<pose_grid(c), pose_threads(c), wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32),
+                         c->stream>>>(c->dm, s, phi, pa);
+}
+
+template <int Q>
+void pose_attr(wt_gpu_ctx* c) {
+  WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32))));
 }
 
 void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt_kin_config* k,
@@ -376,8 +398,13 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
   pa.pad = 0;
   pa.count_in = count_in;
   pa.res_in = res_in;
-  wt::k_pose_system<<<pose_grid(c), wt::kPoseThreads, wt::pose_smem_bytes(c->L, c->NP), c->stream>>>(
-      c->dm, s, phi, pa);
+  pa.dbg = c->pose_dbg;
+  switch (pose_q(c->L)) {
+    case 8: launch_pose<8>(c, s, phi, pa); break;
+    case 16: launch_pose<16>(c, s, phi, pa); break;
+    case 32: launch_pose<32>(c, s, phi, pa); break;
+    default: launch_pose<68>(c, s, phi, pa); break;
+  }
   mark(c, K_POSE);
 }
 
@@ -676,6 +703,14 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     int* d_pth = c->mem.alloc<int>(std::max(1, c->NP));
     int* d_plk = c->mem.alloc<int>(std::max(1, c->NP));
     int* d_pow = c->mem.alloc<int>(std::max(1, c->NP));
+    std::vector<int> depth(static_cast<size_t>(L), 0);
+    int max_depth = 0;
+    for (int j = 0; j < L; ++j) {
+      depth[j] = d->parent[j] < 0 ? 0 : depth[d->parent[j]] + 1;
+      max_depth = std::max(max_depth, depth[j]);
+    }
+    int* d_depth = c->mem.alloc<int>(L);
+    upload(d_depth, depth.data(), L, c->stream);
     double* d_s = c->mem.alloc<double>(L);
     upload(d_v0, v0.data(), V, c->stream);
     upload(d_wg, wg.data(), V, c->stream);
@@ -690,7 +725,7 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     upload(d_pow, c->pair_owner.data(), c->NP, c->stream);
     upload(d_s, c->s_diag.data(), L, c->stream);
     c->dm = wt::DevModel{V, L, c->NP, K, d_v0, d_wg, d_wl, d_roff, d_ring, d_nbr,
-                         d_links, d_poff, d_pth, d_plk, d_pow, d_s};
+                         d_links, d_poff, d_pth, d_plk, d_pow, d_s, d_depth, max_depth};
 
     alloc_state(c, c->ds, false);
     c->hs = c->ds;  // hooks share the per-vertex buffers, own theta/fk/offsets/dchain
@@ -708,10 +743,17 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     c->d_nvalid = c->mem.alloc<int>(1);
     c->d_winners = c->mem.alloc<int>(c->P);
     ensure_stats(c, 16, 8);
+    if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8);
     WT_CUDA(cudaFuncSetAttribute(wt::k_pixoff, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(sizeof(int) * intr->width)));
-    WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(wt::pose_smem_bytes(L, c->NP))));
+    if (wt::pose_smem_bytes(L, c->NP, pose_threads(c) / 32) > 227 * 1024)
+      fail(WT_EINVAL, "skeleton too large for the pose kernel's shared memory");
+    switch (pose_q(L)) {
+      case 8: pose_attr<8>(c); break;
+      case 16: pose_attr<16>(c); break;
+      case 32: pose_attr<32>(c); break;
+      default: pose_attr<68>(c); break;
+    }
     WT_CUDA(cudaStreamSynchronize(c->stream));
   });
   if (rc != WT_OK) {
@@ -861,6 +903,13 @@ void enq_track(wt_gpu_ctx* c, const wt_track_config* cfg, bool shape_now) {
 }  // namespace
 
 void* wt_gpu_stream(wt_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+// Debug: last pose kernel's last-CTA timing (needs WT_DEBUG_POSE at create).
+int wt_gpu_debug_pose(wt_gpu_ctx* c, long long* out) {
+  if (!c || !c->pose_dbg) return 0;
+  cudaMemcpy(out, c->pose_dbg, sizeof(long long) * 5, cudaMemcpyDeviceToHost);
+  return 5;
+}
 
 int wt_gpu_sync(wt_gpu_ctx* c) {
   if (!c) return WT_EINVAL;
@@ -1191,7 +1240,7 @@ int wt_gpu_solve_step(int device, int32_t n, const double* jtj, const double* jt
     cudaError_t e = cudaMemcpy(d, jtj, sizeof(double) * n * n, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d + n * n, jtr, sizeof(double) * n, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) {
-      wt::k_solve_step<<<1, 128, sizeof(double) * (n * n + 2 * n)>>>(n, d, d + n * n, lambda_k, diag_floor,
+      wt::k_solve_step<<<1, 256, sizeof(double) * (n * n + 2 * n) + sizeof(unsigned short) * n * (n + 1) + 16>>>(n, d, d + n * n, lambda_k, diag_floor,
                                                                      d + n * n + n);
       e = cudaGetLastError();
     }

@@ -17,7 +17,6 @@
 namespace wt {
 
 constexpr int kVThreads = 256;    // per-vertex / per-pixel kernels
-constexpr int kPoseThreads = 128; // rows per CTA in the normal-equation kernel
 constexpr double kFixPoint = 4294967296.0;        // 2^32: observation sums
 constexpr double kFixSys = 1099511627776.0;       // 2^40: JtJ / Jtr / shape sums
 constexpr double kFixRes = 17592186044416.0;      // 2^44: residual sum of squares
@@ -36,6 +35,8 @@ struct DevModel {
   const int* pair_link;    // [NP] link driven by theta k
   const int* pair_owner;   // [NP] link j the pair belongs to
   const double* s_diag;    // [L] influence counts S
+  const int* link_depth;   // [L] depth in the tree (root 0)
+  int max_depth;
 };
 
 struct DevIntr {
@@ -221,28 +222,52 @@ __device__ __forceinline__ bool blend_vertex(const double* s_off, double4 w, uch
 __device__ void block_fk(const DevModel& m, const DevState& s, const double* theta_in) {
   __shared__ DQ fk[64];
   __shared__ DQ loc[64];
+  __shared__ double cs[64][2];
   __shared__ int par[64];
-  __shared__ double th[64];
+  __shared__ int dep[64];
+  __shared__ LinkDesc sl[64];
   const int L = m.L;
-  for (int j = threadIdx.x; j < L; j += blockDim.x) th[j] = theta_in[j];
-  __syncthreads();
-  // joint transforms and local offsets in parallel (one link per thread) ...
-  for (int j = threadIdx.x; j < L; j += blockDim.x) {
-    const LinkDesc& l = m.links[j];
-    par[j] = l.parent;
-    loc[j] = dq_compose(dq_load(l.offset), dq_joint(l.kind, l.axis, th[l.theta_index]));
+  {
+    const int n4 = L * static_cast<int>(sizeof(LinkDesc) / sizeof(double));
+    const double* src = reinterpret_cast<const double*>(m.links);
+    double* dst = reinterpret_cast<double*>(sl);
+    for (int k = threadIdx.x; k < n4; k += blockDim.x) dst[k] = src[k];
   }
   __syncthreads();
-  // ... then the parent chain from shared memory (topological order)
-  if (threadIdx.x == 0)
-    for (int j = 0; j < L; ++j) fk[j] = par[j] < 0 ? loc[j] : dq_compose(fk[par[j]], loc[j]);
+  // joint transforms and local offsets in parallel (one link per thread);
+  // each joint's half-angle sincos is evaluated once ...
+  for (int j = threadIdx.x; j < L; j += blockDim.x) {
+    const LinkDesc& l = sl[j];
+    const double th = theta_in[l.theta_index];
+    double sn, cn;
+    sincos(th * 0.5, &sn, &cn);
+    cs[j][0] = cn;
+    cs[j][1] = sn;
+    par[j] = l.parent;
+    dep[j] = m.link_depth[j];
+    loc[j] = dq_compose(dq_load(l.offset), dq_joint_cs(l.kind, l.axis, th, cn, sn));
+  }
   __syncthreads();
+  // ... the parent chain one tree level at a time ...
+  for (int d = 0; d <= m.max_depth; ++d) {
+    for (int j = threadIdx.x; j < L; j += blockDim.x)
+      if (dep[j] == d) fk[j] = par[j] < 0 ? loc[j] : dq_compose(fk[par[j]], loc[j]);
+    __syncthreads();
+  }
+  // ... then offsets and the dchain blocks in parallel (skeleton.cpp:71-108)
   for (int j = threadIdx.x; j < L; j += blockDim.x) {
     dq_store(fk[j], s.fk + 8 * j);
-    dq_store(dq_compose(fk[j], dq_load(m.links[j].bind_inv)), s.offsets + 8 * j);
+    dq_store(dq_compose(fk[j], dq_load(sl[j].bind_inv)), s.offsets + 8 * j);
   }
-  for (int p = threadIdx.x; p < m.NP; p += blockDim.x)
-    dq_store(d_link_offset(m.links, fk, th, m.pair_owner[p], m.pair_link[p]), s.dchain + 8 * p);
+  for (int p = threadIdx.x; p < m.NP; p += blockDim.x) {
+    const int j = m.pair_owner[p], kl = m.pair_link[p];
+    const LinkDesc& lk = sl[kl];
+    const DQ off = dq_load(lk.offset);
+    const DQ pre = lk.parent < 0 ? off : dq_compose(fk[lk.parent], off);
+    const DQ dj = dq_djoint_cs(lk.kind, lk.axis, cs[kl][0], cs[kl][1]);
+    const DQ k_to_j = dq_compose(dq_inverse(fk[kl]), fk[j]);
+    dq_store(dq_compose(dq_compose(pre, dj), dq_compose(k_to_j, dq_load(sl[j].bind_inv))), s.dchain + 8 * p);
+  }
 }
 
 __global__ void k_fk(DevModel m, DevState s) { block_fk(m, s, s.theta); }
@@ -543,55 +568,56 @@ __device__ __forceinline__ bool observed_mean(const unsigned long long* acc, int
 
 
 // ---------------------------------------------------------------------------
-// Dense fp64 Cholesky + solve for the L x L pose system, executed by one CTA
-// (solve_step, kinopt.cpp:121-130). A is row-major in shared memory and is
-// overwritten by its factor. Like Eigen's LLT the factorisation fails at the
-// first pivot that is not strictly positive. Returns ok in *ok (CTA-uniform).
-__device__ void block_cholesky_solve(int L, double* A, const double* b, double* x, int* ok) {
+// Dense fp64 solve of the damped L x L pose system by one CTA (solve_step,
+// kinopt.cpp:121-130) as an LDL^T factorisation: A = L D L^T with unit L.
+// D_k is exactly the pivot Eigen's LLT takes the square root of, so the
+// factorisation fails (returns 0) under the same condition -- the first pivot
+// that is not strictly positive. No square roots; one barrier per pivot: every
+// thread updates trailing entries (i,j) listed in the (ea, eb) upper-triangle
+// table. A is row-major (lower triangle used, overwritten); b is overwritten;
+// x receives the solution. Must be called by all threads of the CTA.
+__device__ int block_ldlt_solve(int L, double* A, double* b, double* x, const unsigned short* ea,
+                                const unsigned short* eb, int NT) {
   __shared__ int s_ok;
+  __shared__ double inv_d[64];
   if (threadIdx.x == 0) s_ok = 1;
   __syncthreads();
   for (int k = 0; k < L; ++k) {
-    if (threadIdx.x == 0) {
-      const double p = A[k * L + k];
-      if (!(p > 0.0)) s_ok = 0;
-      else A[k * L + k] = sqrt(p);
+    const double dk = A[k * L + k];
+    if (!(dk > 0.0)) {  // uniform: every thread read the same pivot
+      if (threadIdx.x == 0) s_ok = 0;
+      break;
     }
-    __syncthreads();
-    if (!s_ok) break;
-    const double lkk = A[k * L + k];
-    for (int i = k + 1 + threadIdx.x; i < L; i += blockDim.x) A[i * L + k] /= lkk;
-    __syncthreads();
-    const int m = L - k - 1;
-    for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
-      const int i = k + 1 + t / m, j = k + 1 + t % m;
-      if (j <= i) A[i * L + j] -= A[i * L + k] * A[j * L + k];
+    const double inv = 1.0 / dk;
+    for (int e = threadIdx.x; e < NT; e += blockDim.x) {
+      const int r = ea[e], c = eb[e];  // r <= c: update lower entry (c, r)
+      if (r > k) A[c * L + r] -= A[c * L + k] * A[r * L + k] * inv;
     }
+    if (threadIdx.x == 0) inv_d[k] = inv;
     __syncthreads();
   }
-  if (s_ok && threadIdx.x < 32) {
+  __syncthreads();
+  const int ok = s_ok;
+  if (ok && threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    // forward: L y = b
-    for (int i = 0; i < L; ++i) {
-      double s = 0.0;
-      for (int j = lane; j < i; j += 32) s += A[i * L + j] * x[j];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) x[i] = (b[i] - s) / A[i * L + i];
+    for (int k = 0; k < L; ++k) {  // forward: (unit) L z = b
+      const double zk = b[k];
+      __syncwarp();
+      for (int i = k + 1 + lane; i < L; i += 32) b[i] -= A[i * L + k] * inv_d[k] * zk;
       __syncwarp();
     }
-    // backward: L^T x = y
-    for (int i = L - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int j = i + 1 + lane; j < L; j += 32) s += A[j * L + i] * x[j];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) x[i] = (x[i] - s) / A[i * L + i];
+    for (int k = lane; k < L; k += 32) b[k] *= inv_d[k];  // D y = z
+    __syncwarp();
+    for (int k = L - 1; k >= 0; --k) {  // backward: L^T x = y
+      const double xk = b[k];
+      __syncwarp();
+      for (int i = lane; i < k; i += 32) b[i] -= A[k * L + i] * inv_d[i] * xk;
+      if (lane == 0) x[k] = xk;
       __syncwarp();
     }
   }
   __syncthreads();
-  *ok = s_ok;
+  return ok;
 }
 
 // ---------------------------------------------------------------------------
@@ -610,33 +636,38 @@ struct PoseArgs {
   int pad;
   const int* count_in;   // optional association override (stage hook)
   const double* res_in;
+  long long* dbg;        // optional timing record of the last CTA (WT_DEBUG_POSE)
 };
 
-__host__ __device__ inline size_t pose_smem_bytes(int L, int NP) {
+// Shared-memory layout of k_pose_system for L links, NP dchain pairs and
+// W warps: offsets, dchain, per-warp row tiles [W][32][L|1], per-warp
+// residuals, per-warp entry partials [W][NE], pair tables, entry table.
+__host__ __device__ inline size_t pose_smem_bytes(int L, int NP, int warps) {
   const int Lp = L | 1;
   const int NE = L * (L + 1) / 2 + L;
-  return sizeof(double) * (8 * L + 8 * NP + kPoseThreads * Lp + kPoseThreads + NE) +
-         sizeof(int) * (L + 1 + NP + kPoseThreads + 1) + sizeof(unsigned short) * 2 * NE + 16;
+  return sizeof(double) * (8 * L + 8 * NP + warps * 32 * Lp + warps * 32 + warps * NE) +
+         sizeof(int) * (L + 1 + NP) + sizeof(unsigned short) * 2 * NE + 64;
 }
 
-__global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevState s,
-                                                              const double4* phi, PoseArgs a) {
+template <int Q>
+__global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
   extern __shared__ __align__(16) double psm[];
   const int L = m.L;
   const int Lp = L | 1;
   const int NT = L * (L + 1) / 2;
   const int NE = NT + L;  // upper JtJ, then Jtr
-  double* s_off = psm;                        // 8L
-  double* s_dch = s_off + 8 * L;              // 8NP
-  double* rows = s_dch + 8 * m.NP;            // kPoseThreads * Lp (compacted rows)
-  double* rres = rows + kPoseThreads * Lp;    // kPoseThreads
-  double* esum = rres + kPoseThreads;         // NE running sums
-  int* s_poff = reinterpret_cast<int*>(esum + NE);  // L+1
-  int* s_pth = s_poff + (L + 1);                     // NP
-  int* flag = s_pth + m.NP;                          // kPoseThreads + 1
-  unsigned short* ea = reinterpret_cast<unsigned short*>(flag + kPoseThreads + 1);
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* s_off = psm;                       // 8L
+  double* s_dch = s_off + 8 * L;             // 8NP
+  double* rows = s_dch + 8 * m.NP;           // nw * 32 * Lp
+  double* rres = rows + nw * 32 * Lp;        // nw * 32
+  double* part = rres + nw * 32;             // nw * NE (lane-owned entries)
+  int* s_poff = reinterpret_cast<int*>(part + nw * NE);  // L+1
+  int* s_pth = s_poff + (L + 1);                          // NP
+  unsigned short* ea = reinterpret_cast<unsigned short*>(s_pth + m.NP);
   unsigned short* eb = ea + NE;
 
+  const long long t0 = clock64();
 #pragma unroll 4
   for (int k = threadIdx.x; k < 8 * L; k += blockDim.x) s_off[k] = s.offsets[k];
 #pragma unroll 8
@@ -645,7 +676,6 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevSta
 #pragma unroll 4
   for (int k = threadIdx.x; k < m.NP; k += blockDim.x) s_pth[k] = m.pair_theta[k];
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
-    esum[e] = 0.0;
     if (e < NT) {  // row-major upper triangle
       int r = 0, rem = e;
       while (rem >= L - r) {
@@ -659,19 +689,22 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevSta
       eb[e] = 0xFFFF;  // pairs with the residual
     }
   }
-  double rsum = 0.0;
-  long long nassoc = 0;
+  for (int e = threadIdx.x; e < nw * NE; e += blockDim.x) part[e] = 0.0;
   __syncthreads();
 
-  for (int base = blockIdx.x * blockDim.x; base < m.V; base += gridDim.x * blockDim.x) {
-    const int i = base + threadIdx.x;
+  // Warp-level accumulation: each warp takes 32 consecutive vertices, builds
+  // the rows of its associated ones (fill_row) in its own shared tile and
+  // adds their outer products to lane-owned entries -- no block barriers.
+  double rsum = 0.0;
+  long long nassoc = 0;
+  double* wrows = rows + warp * 32 * Lp;
+  double* wres = rres + warp * 32;
+  double* wpart = part + warp * NE;
+  const int gw = blockIdx.x * nw + warp, tw = gridDim.x * nw;
+  for (int base = gw * 32; base < m.V; base += tw * 32) {
+    const int i = base + lane;
     double r = 0.0;
     bool has_row = false;
-    DQ raw;
-    double sign[4];
-    double r8[8];
-    double4 wv = make_double4(0, 0, 0, 0);
-    uchar4 lk = make_uchar4(0xFF, 0xFF, 0xFF, 0xFF);
     if (i < m.V) {
       long long cnt = 0;
       bool have = false;
@@ -691,70 +724,91 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevSta
       if (have) {
         rsum += r * r;
         ++nassoc;
-        wv = m.wgt[i];
-        lk = m.wlink[i];
+        DQ raw;
+        double sign[4];
+        const double4 wv = m.wgt[i];
+        const uchar4 lk = m.wlink[i];
         if (n.w != 0.0f && blend_vertex(s_off, wv, lk, raw, sign)) {
           const double4 a0 = m.v0[i];
           const double4 f = phi[i];
           const double rest[3] = {a0.x + f.x, a0.y + f.y, a0.z + f.z};
           const double nn[3] = {n.x, n.y, n.z};
+          double r8[8];
           dq_point_plane_row(raw, rest, nn, r8);
+          double* row = wrows + lane * Lp;
+          for (int k = 0; k < L; ++k) row[k] = 0.0;
+          const unsigned char li[4] = {lk.x, lk.y, lk.z, lk.w};
+          const double wi[4] = {wv.x, wv.y, wv.z, wv.w};
+          for (int e = 0; e < 4; ++e) {
+            if (li[e] == 0xFF) break;
+            const double coeff = wi[e] * sign[e];
+            for (int p = s_poff[li[e]]; p < s_poff[li[e] + 1]; ++p) {
+              const double* d8 = s_dch + 8 * p;
+              double dot = 0.0;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) dot += r8[c] * d8[c];
+              row[s_pth[p]] += coeff * dot;
+            }
+          }
+          wres[lane] = r;
           has_row = true;
         }
       }
     }
-    // compact the rows of this chunk in vertex order (deterministic)
-    flag[threadIdx.x] = has_row ? 1 : 0;
-    __syncthreads();
-    const int nrows = block_exclusive_scan(flag, kPoseThreads);
-    if (has_row) {
-      const int slot = flag[threadIdx.x];
-      double* row = rows + slot * Lp;
-      for (int k = 0; k < L; ++k) row[k] = 0.0;
-      const unsigned char li[4] = {lk.x, lk.y, lk.z, lk.w};
-      const double wi[4] = {wv.x, wv.y, wv.z, wv.w};
-      for (int e = 0; e < 4; ++e) {
-        if (li[e] == 0xFF) break;
-        const double coeff = wi[e] * sign[e];
-        for (int p = s_poff[li[e]]; p < s_poff[li[e] + 1]; ++p) {
-          const double* d8 = s_dch + 8 * p;
-          double dot = 0.0;
+    unsigned mask = __ballot_sync(0xffffffffu, has_row);
+    __syncwarp();
+    if (mask) {
+      // lane-owned entries e = lane + 32 q accumulate in registers over the
+      // batch's rows (ascending vertex order: deterministic)
+      double acc[Q];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) dot += r8[c] * d8[c];
-          row[s_pth[p]] += coeff * dot;
+      for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+      while (mask) {
+        const int t = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const double* row = wrows + t * Lp;
+        const double rt = wres[t];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int e = lane + 32 * q;
+          if (e < NE) {
+            const int ca = ea[e], cb = eb[e];
+            acc[q] += row[ca] * (cb == 0xFFFF ? rt : row[cb]);
+          }
         }
       }
-      rres[slot] = r;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < NE; e += blockDim.x) {
-      const int ca = ea[e], cb = eb[e];
-      double acc = 0.0;
-      if (cb == 0xFFFF) {
-        for (int t = 0; t < nrows; ++t) acc += rows[t * Lp + ca] * rres[t];
-      } else {
-        for (int t = 0; t < nrows; ++t) acc += rows[t * Lp + ca] * rows[t * Lp + cb];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int e = lane + 32 * q;
+        if (e < NE) wpart[e] += acc[q];
       }
-      esum[e] += acc;
     }
-    __syncthreads();
+    __syncwarp();
   }
+  const long long t1 = clock64();
   block_sum2(rsum, nassoc);
-  for (int e = threadIdx.x; e < NE; e += blockDim.x) red_add(s.red + e, fix(esum[e], kFixSys));
+  __syncthreads();
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    double acc = 0.0;
+    for (int w = 0; w < nw; ++w) acc += part[w * NE + e];  // fixed order
+    red_add(s.red + e, fix(acc, kFixSys));
+  }
   if (threadIdx.x == 0) {
     red_add(s.red + NE, fix(rsum, kFixRes));
     red_add(s.red + NE + 1, nassoc);
   }
   if (!last_block(s.tickets + 1)) return;
+  const long long t2 = clock64();
 
   // ---- last CTA: assemble, prior, solve, update, stats, FK ---------------
-  double* A = rows;                 // L*L (fits: kPoseThreads*Lp >= L*L for L <= 128)
-  double* jtr = rres;               // L (kPoseThreads >= L)
-  double* jtj_d = esum;             // reuse: diag of JtJ (L)
+  double* A = rows;                  // L*L (nw*32*Lp >= L*L for L <= 64 with 4+ warps)
+  double* jtr = rres;                // L <= nw*32
+  double* jtj_d = part;              // diag of JtJ (L)
   __shared__ double s_theta[64];
   __shared__ double s_x[64];
   __shared__ double s_rsum;
   __shared__ long long s_nassoc;
+  __shared__ int s_finite, s_ok;
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
     const double val = unfix(__ldcg(s.red + e), kFixSys);
     s.red[e] = 0ull;
@@ -771,6 +825,8 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevSta
     s_nassoc = static_cast<long long>(__ldcg(s.red + NE + 1));
     s.red[NE] = 0ull;
     s.red[NE + 1] = 0ull;
+    s_finite = 1;
+    s_ok = 0;
   }
   for (int k = threadIdx.x; k < L; k += blockDim.x) s_theta[k] = s.theta[k];
   __syncthreads();
@@ -787,8 +843,6 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevSta
     return;
   }
   // A = JtJ + lambda_k diag(JtJ) + floor I
-  __shared__ int s_finite;
-  if (threadIdx.x == 0) s_finite = 1;
   for (int k = threadIdx.x; k < L; k += blockDim.x) jtj_d[k] = A[k * L + k];
   __syncthreads();
   for (int k = threadIdx.x; k < L; k += blockDim.x)
@@ -799,10 +853,15 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevSta
   for (int k = threadIdx.x; k < L; k += blockDim.x)
     if (!isfinite(jtr[k])) s_finite = 0;
   __syncthreads();
-  int ok = 0;
-  if (s_finite) block_cholesky_solve(L, A, jtr, s_x, &ok);
+  const long long t3 = clock64();
+  {
+    const int ok = s_finite ? block_ldlt_solve(L, A, jtr, s_x, ea, eb, NT) : 0;
+    if (threadIdx.x == 0) s_ok = ok;
+  }
   __syncthreads();
+  const long long t4 = clock64();
   if (threadIdx.x == 0) {
+    const int ok = s_ok;
     double nrm = 0.0;
     if (ok) {
       for (int k = 0; k < L; ++k) {
@@ -821,8 +880,14 @@ __global__ void __launch_bounds__(kPoseThreads) k_pose_system(DevModel m, DevSta
   }
   __syncthreads();
   for (int k = threadIdx.x; k < L; k += blockDim.x) s.theta[k] = s_theta[k];
-  __syncthreads();
   block_fk(m, s, s_theta);
+  if (a.dbg && threadIdx.x == 0) {
+    a.dbg[0] = t1 - t0;
+    a.dbg[1] = t2 - t1;
+    a.dbg[2] = t3 - t2;
+    a.dbg[3] = t4 - t3;
+    a.dbg[4] = clock64() - t4;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1016,9 +1081,20 @@ __global__ void k_solve_step(int n, const double* jtj, const double* jtr, double
   double* A = sm;
   double* b = A + n * n;
   double* x = b + n;
+  unsigned short* ea = reinterpret_cast<unsigned short*>(x + n);
+  const int NT = n * (n + 1) / 2;
+  unsigned short* eb = ea + NT;
   __shared__ int fin;
   if (threadIdx.x == 0) fin = 1;
-  __syncthreads();
+  for (int e = threadIdx.x; e < NT; e += blockDim.x) {
+    int r = 0, rem = e;
+    while (rem >= n - r) {
+      rem -= n - r;
+      ++r;
+    }
+    ea[e] = static_cast<unsigned short>(r);
+    eb[e] = static_cast<unsigned short>(r + rem);
+  }
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) A[e] = jtj[e];
   for (int k = threadIdx.x; k < n; k += blockDim.x) b[k] = jtr[k];
   __syncthreads();
@@ -1030,9 +1106,7 @@ __global__ void k_solve_step(int n, const double* jtj, const double* jtr, double
   for (int k = threadIdx.x; k < n; k += blockDim.x)
     if (!isfinite(b[k])) fin = 0;
   __syncthreads();
-  int ok = 0;
-  if (fin) block_cholesky_solve(n, A, b, x, &ok);
-  __syncthreads();
+  const int ok = fin ? block_ldlt_solve(n, A, b, x, ea, eb, NT) : 0;
   for (int k = threadIdx.x; k < n; k += blockDim.x) out[k] = ok ? x[k] : 0.0;
   if (threadIdx.x == 0) out[n] = ok ? 1.0 : 0.0;
 }
