@@ -278,7 +278,7 @@ void alloc_state(wt_gpu_ctx* c, wt::DevState& s, bool hook) {
     s.poff = c->mem.alloc<int>(c->P + 1);
     s.items = c->mem.alloc<double4>(c->V);
     s.acc = c->mem.alloc<unsigned long long>(4 * static_cast<size_t>(std::max(1, c->V)));
-    const int NE = c->L * (c->L + 1) / 2 + c->L + 8;
+    const int NE = wt::kRedCopies * (c->L * (c->L + 1) / 2 + c->L + 2) + 8;
     s.red = c->mem.alloc<unsigned long long>(NE);
     s.tickets = c->mem.alloc<unsigned>(8);
     s.sys_out = c->mem.alloc<double>(c->L * c->L + c->L);
@@ -329,7 +329,7 @@ void enq_normals(wt_gpu_ctx* c, const wt::DevState& s, bool bucket, bool zero_ac
 }
 
 void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
-  wt::k_pixoff<<<c->din.H, wt::kVThreads, sizeof(int) * c->din.W, c->stream>>>(s, c->din.W, c->din.H);
+  wt::k_pixoff<<<(c->din.H + 7) / 8, wt::kVThreads, 0, c->stream>>>(s, c->din.W, c->din.H);
   mark(c, K_SCATTER);
   wt::k_scatter<<<vgrid(std::max(c->V, c->din.H)), wt::kVThreads, 0, c->stream>>>(c->dm, s, c->din.H);
   mark(c, K_SCATTER);
@@ -570,6 +570,7 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
   const int rc = guarded(nullptr, [&] {
     validate_model(d);
     if (!intr || intr->width <= 0 || intr->height <= 0) fail(WT_EINVAL, "bad intrinsics");
+    if (intr->width > 32 * wt::kRowChunks) fail(WT_EINVAL, "image rows wider than 2048 pixels are not supported");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
       cudaGetLastError();
@@ -743,9 +744,7 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     c->d_nvalid = c->mem.alloc<int>(1);
     c->d_winners = c->mem.alloc<int>(c->P);
     ensure_stats(c, 16, 8);
-    if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8);
-    WT_CUDA(cudaFuncSetAttribute(wt::k_pixoff, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sizeof(int) * intr->width)));
+    if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8 + 4 * 296 + 8);
     if (wt::pose_smem_bytes(L, c->NP, pose_threads(c) / 32) > 227 * 1024)
       fail(WT_EINVAL, "skeleton too large for the pose kernel's shared memory");
     switch (pose_q(L)) {
@@ -907,7 +906,7 @@ void* wt_gpu_stream(wt_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : 
 // Debug: last pose kernel's last-CTA timing (needs WT_DEBUG_POSE at create).
 int wt_gpu_debug_pose(wt_gpu_ctx* c, long long* out) {
   if (!c || !c->pose_dbg) return 0;
-  cudaMemcpy(out, c->pose_dbg, sizeof(long long) * 5, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out, c->pose_dbg, sizeof(long long) * (8 + 4 * 296), cudaMemcpyDeviceToHost);
   return 5;
 }
 

@@ -20,6 +20,7 @@ constexpr int kVThreads = 256;    // per-vertex / per-pixel kernels
 constexpr double kFixPoint = 4294967296.0;        // 2^32: observation sums
 constexpr double kFixSys = 1099511627776.0;       // 2^40: JtJ / Jtr / shape sums
 constexpr double kFixRes = 17592186044416.0;      // 2^44: residual sum of squares
+constexpr int kRedCopies = 8;  // CTAs spread their fixed-point atomics over this many slot copies
 
 struct DevModel {
   int V, L, NP, K;
@@ -355,15 +356,27 @@ __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, D
     if (compute) {
       double ax = 0, ay = 0, az = 0;
       const int r0 = m.ring_off[i], r1 = m.ring_off[i + 1];
-      for (int r = r0; r < r1; ++r) {
-        const int2 bc = m.ring[r];
-        const double4 b = s.pv[bc.x];
-        const double4 c = s.pv[bc.y];
-        const double ex = b.x - vx, ey = b.y - vy, ez = b.z - vz;
-        const double fx = c.x - vx, fy = c.y - vy, fz = c.z - vz;
-        ax += ey * fz - ez * fy;
-        ay += ez * fx - ex * fz;
-        az += ex * fy - ey * fx;
+      for (int r = r0; r < r1; r += 4) {
+        // four incident triangles per step: index loads, then all eight
+        // position gathers in flight, then the cross products in CSR order
+        int2 bc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(i, i);
+        double4 pb[4], pc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          pb[q] = s.pv[bc[q].x];
+          pc[q] = s.pv[bc[q].y];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (r + q >= r1) break;
+          const double ex = pb[q].x - vx, ey = pb[q].y - vy, ez = pb[q].z - vz;
+          const double fx = pc[q].x - vx, fy = pc[q].y - vy, fz = pc[q].z - vz;
+          ax += ey * fz - ez * fy;
+          ay += ez * fx - ex * fz;
+          az += ex * fy - ey * fx;
+        }
       }
       const double len = sqrt(ax * ax + ay * ay + az * az);
       valid = v.w != 0.0;
@@ -420,26 +433,47 @@ __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, D
 }
 
 // K3b: row-major pixel offsets of the bucket CSR (association.cpp:58-59),
-// one CTA per image row: its base is the sum of the preceding rows' counts,
-// then a shared-memory scan of the row. Clears the per-pixel counts.
+// one warp per image row, no block barriers: the row's base is the sum of
+// the preceding rows' counts (warp reduction); the row is read in coalesced
+// 32-pixel chunks, all loads first, then scanned chunk by chunk with
+// shuffles. Clears the per-pixel counts for the next association.
+constexpr int kRowChunks = 64;  // rows up to 2048 pixels
+
 __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, int H) {
-  extern __shared__ int s_row[];
-  const int row = blockIdx.x;
-  long long part = 0;
-  for (int k = threadIdx.x; k < row; k += blockDim.x) part += __ldcg(s.row_cnt + k);
-  double dummy = 0.0;
-  block_sum2(dummy, part);
-  __shared__ int s_base;
-  if (threadIdx.x == 0) s_base = static_cast<int>(part);
-  for (int c = threadIdx.x; c < W; c += blockDim.x) {
-    s_row[c] = __ldcg(s.pix_cnt + row * W + c);
-    s.pix_cnt[row * W + c] = 0;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= H) return;
+  int base = 0;
+  for (int k = lane; k < row; k += 32) base += __ldcg(s.row_cnt + k);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+  int* cnt = s.pix_cnt + row * W;
+  int* off = s.poff + row * W;
+  const int nch = (W + 31) / 32;
+  int v[kRowChunks];
+#pragma unroll
+  for (int t = 0; t < kRowChunks; ++t) {
+    const int c = t * 32 + lane;
+    v[t] = (t < nch && c < W) ? __ldcg(cnt + c) : 0;
   }
-  __syncthreads();
-  const int total = block_exclusive_scan(s_row, W);
-  const int base = s_base;
-  for (int c = threadIdx.x; c < W; c += blockDim.x) s.poff[row * W + c] = base + s_row[c];
-  if (row == H - 1 && threadIdx.x == 0) s.poff[W * H] = base + total;
+  int run = base;
+#pragma unroll
+  for (int t = 0; t < kRowChunks; ++t) {
+    if (t >= nch) break;
+    int incl = v[t];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int c = t * 32 + lane;
+    if (c < W) {
+      off[c] = run + incl - v[t];
+      cnt[c] = 0;
+    }
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (row == H - 1 && lane == 0) s.poff[W * H] = run;
 }
 
 // K3c: scatter into pixel order (association.cpp:60-66; unordered within a
@@ -485,10 +519,10 @@ struct SearchArgs {
   int* winners;
 };
 
-__device__ __forceinline__ double ring_lb2(int k, double atx, double aty, double z, const SearchArgs& a) {
-  const double dx = (k - 0.5) / a.fx, dy = (k - 0.5) / a.fy;
+__device__ __forceinline__ double ring_lb2(int k, double atx, double aty, double ifx, double ify, double z) {
+  const double dx = (k - 0.5) * ifx, dy = (k - 0.5) * ify;
   const double tx = atx + dx, ty = aty + dy;
-  const double b = fmin(dx / sqrt(1.0 + tx * tx), dy / sqrt(1.0 + ty * ty)) * z;
+  const double b = fmin(dx * rsqrt(1.0 + tx * tx), dy * rsqrt(1.0 + ty * ty)) * z;
   return b * b * (1.0 - 1e-9);
 }
 
@@ -513,12 +547,13 @@ __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, Se
     const int pix = f.vlist[j];
     const int pu = pix % a.W, pv = pix / a.W;
     const double px = f.pts_hi[3 * pix], py = f.pts_hi[3 * pix + 1], pz = f.pts_hi[3 * pix + 2];
-    const double atx = fabs((pu - a.cx) / a.fx), aty = fabs((pv - a.cy) / a.fy);
+    const double ifx = 1.0 / a.fx, ify = 1.0 / a.fy;
+    const double atx = fabs((pu - a.cx) * ifx), aty = fabs((pv - a.cy) * ify);
     double best_x = INFINITY;
     int best_i = -1;
     for (int k = 0; k <= w; ++k) {
       if (k > 0 && a.prune) {
-        const double lb = ring_lb2(k, atx, aty, pz, a);
+        const double lb = ring_lb2(k, atx, aty, ifx, ify, pz);
         if (lb > a.cut2 || lb > best_x) break;  // no vertex of ring >= k can win or tie
       }
       // ring k: top and bottom rows as spans, then the side columns
@@ -588,7 +623,7 @@ __device__ int block_ldlt_solve(int L, double* A, double* b, double* x, const un
       if (threadIdx.x == 0) s_ok = 0;
       break;
     }
-    const double inv = 1.0 / dk;
+    const double inv = __drcp_rn(dk);
     for (int e = threadIdx.x; e < NT; e += blockDim.x) {
       const int r = ea[e], c = eb[e];  // r <= c: update lower entry (c, r)
       if (r > k) A[c * L + r] -= A[c * L + k] * A[r * L + k] * inv;
@@ -668,6 +703,11 @@ __global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, 
   unsigned short* eb = ea + NE;
 
   const long long t0 = clock64();
+  if (a.dbg && threadIdx.x == 0) {
+    unsigned long long g0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+    a.dbg[8 + 3 * 296 + blockIdx.x] = static_cast<long long>(g0);
+  }
 #pragma unroll 4
   for (int k = threadIdx.x; k < 8 * L; k += blockDim.x) s_off[k] = s.offsets[k];
 #pragma unroll 8
@@ -744,9 +784,8 @@ __global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, 
             const double coeff = wi[e] * sign[e];
             for (int p = s_poff[li[e]]; p < s_poff[li[e] + 1]; ++p) {
               const double* d8 = s_dch + 8 * p;
-              double dot = 0.0;
-#pragma unroll
-              for (int c = 0; c < 8; ++c) dot += r8[c] * d8[c];
+              const double dot = ((r8[0] * d8[0] + r8[1] * d8[1]) + (r8[2] * d8[2] + r8[3] * d8[3])) +
+                                 ((r8[4] * d8[4] + r8[5] * d8[5]) + (r8[6] * d8[6] + r8[7] * d8[7]));
               row[s_pth[p]] += coeff * dot;
             }
           }
@@ -786,16 +825,30 @@ __global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, 
     __syncwarp();
   }
   const long long t1 = clock64();
+  unsigned long long g_main = 0, g_start = 0;
+  if (a.dbg) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_main));
+  }
   block_sum2(rsum, nassoc);
   __syncthreads();
+  // fixed-point atomics (associative, so the result is order independent),
+  // spread over kRedCopies slot copies to avoid same-address serialisation
+  unsigned long long* red = s.red + (blockIdx.x % kRedCopies) * (NE + 2);
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
     double acc = 0.0;
     for (int w = 0; w < nw; ++w) acc += part[w * NE + e];  // fixed order
-    red_add(s.red + e, fix(acc, kFixSys));
+    red_add(red + e, fix(acc, kFixSys));
   }
   if (threadIdx.x == 0) {
-    red_add(s.red + NE, fix(rsum, kFixRes));
-    red_add(s.red + NE + 1, nassoc);
+    red_add(red + NE, fix(rsum, kFixRes));
+    red_add(red + NE + 1, nassoc);
+  }
+  if (a.dbg && threadIdx.x == 0) {
+    unsigned long long g_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+    a.dbg[8 + 3 * blockIdx.x] = static_cast<long long>(g_main);
+    a.dbg[8 + 3 * blockIdx.x + 1] = static_cast<long long>(g_end);
+    a.dbg[8 + 3 * blockIdx.x + 2] = t1 - t0;
   }
   if (!last_block(s.tickets + 1)) return;
   const long long t2 = clock64();
@@ -810,8 +863,13 @@ __global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, 
   __shared__ long long s_nassoc;
   __shared__ int s_finite, s_ok;
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
-    const double val = unfix(__ldcg(s.red + e), kFixSys);
-    s.red[e] = 0ull;
+    unsigned long long sum = 0ull;
+#pragma unroll
+    for (int c = 0; c < kRedCopies; ++c) {
+      sum += __ldcg(s.red + c * (NE + 2) + e);
+      s.red[c * (NE + 2) + e] = 0ull;
+    }
+    const double val = unfix(sum, kFixSys);
     const int ca = ea[e], cb = eb[e];
     if (cb == 0xFFFF) {
       jtr[ca] = val;
@@ -821,10 +879,15 @@ __global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, 
     }
   }
   if (threadIdx.x == 0) {
-    s_rsum = unfix(__ldcg(s.red + NE), kFixRes);
-    s_nassoc = static_cast<long long>(__ldcg(s.red + NE + 1));
-    s.red[NE] = 0ull;
-    s.red[NE + 1] = 0ull;
+    unsigned long long rs = 0ull, na = 0ull;
+    for (int c = 0; c < kRedCopies; ++c) {
+      rs += __ldcg(s.red + c * (NE + 2) + NE);
+      na += __ldcg(s.red + c * (NE + 2) + NE + 1);
+      s.red[c * (NE + 2) + NE] = 0ull;
+      s.red[c * (NE + 2) + NE + 1] = 0ull;
+    }
+    s_rsum = unfix(rs, kFixRes);
+    s_nassoc = static_cast<long long>(na);
     s_finite = 1;
     s_ok = 0;
   }
