@@ -39,3 +39,23 @@ def cfg(mode="dynamic", kin_its=5, shape_its=2, **kw) -> TrackConfig:
 def cmp_winners(a: np.ndarray, b: np.ndarray) -> float:
     """Fraction of pixels whose winning vertex agrees."""
     return float(np.mean(a == b))
+
+
+GOLDEN = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+_MODEL_KEYS = ["parent", "parent_offset", "joint_kind", "joint_axis", "theta_index", "v0", "phi", "weight_count",
+               "weight_link", "weight", "triangles", "vtri_offsets", "vtri_items", "nbr_offsets", "nbr_items"]
+
+
+def load_golden(name: str):
+    """(fixture dict, ModelBundle, wt_intrinsics) of tests/golden/<name>.npz."""
+    from paper_1711_07999_b200.model import ModelBundle
+    z = dict(np.load(GOLDEN / f"{name}.npz"))
+    kw = {k: z[f"model_{k}"] for k in _MODEL_KEYS}
+    b = ModelBundle(polys=[], **kw)
+    fx, fy, cx, cy, w, h = z["intr"]
+    return z, b, W.Intrinsics(fx, fy, cx, cy, int(w), int(h))
+
+
+def track_cfg_c(mode: int, kin: int, shape: int) -> W.TrackConfigC:
+    return W.TrackConfigC(mode, 1, W.KinConfig(kin, 1, 1e-2, 1e-4, 1e-9, 0, 0, 0.0),
+                          W.ShapeConfig(shape, 0, 0.05, 0.5, 1e-2, 1e-9), W.AssocConfig(5, 0, 0.10), 1, 0)
