@@ -204,6 +204,17 @@ int wt_gpu_track_frame(wt_gpu_ctx* ctx, const float* depth, double depth_scale,
 /* load_cloud + track_loaded. */
 int wt_gpu_track_frame_cloud(wt_gpu_ctx* ctx, const double* points, const uint8_t* valid,
                              const wt_track_config* cfg, wt_frame_stats* stats);
+/* run_tracking (tracker.cpp:70-100) over n_frames depth images laid out
+ * back to back ([n_frames][H*W] float, host or device memory): track_frame on
+ * each in order, recording theta [n_frames*L] and the link origins
+ * transform_point(FK(theta)[j], 0) [n_frames*L*3] (either may be NULL).
+ * Host frames are staged through pinned double buffers on a copy stream so
+ * frame f+1's upload overlaps frame f's solve. frame_index advances by
+ * n_frames; the final Phi stays in the context (wt_gpu_get_state). */
+int wt_gpu_track_sequence(wt_gpu_ctx* ctx, const float* frames, int32_t n_frames, double depth_scale,
+                          const wt_track_config* cfg, double* theta_out, double* joints_out);
+/* Link origins at the current theta, [L*3] (tracker.cpp:84-86). */
+int wt_gpu_joint_positions(wt_gpu_ctx* ctx, double* joints_out);
 /* optimize_pose (kinopt.cpp:132-171) / optimize_shape (shapeopt.cpp:50-130)
  * on the loaded frame; stats arrays may be NULL. */
 int wt_gpu_optimize_pose(wt_gpu_ctx* ctx, const wt_kin_config* kin, const wt_assoc_config* assoc,

@@ -314,3 +314,29 @@ class RefTracker:
 
 def hardware_threads() -> int:
     return lib().wtref_hardware_threads()
+
+
+def write_sequence(path, intr: W.Intrinsics, frames, depth_scale: float = 1.0) -> None:
+    """SequenceWriter (seqio.cpp:493-535)."""
+    fr = np.ascontiguousarray(frames, np.float32)
+    _check(lib().wtref_write_sequence(str(path).encode(), C.byref(intr), C.c_double(depth_scale), _p(fr),
+                                      fr.shape[0]))
+
+
+def read_depth(path, frame: int):
+    """SequenceReader::read_depth (seqio.cpp:476-487) -> (intr, scale, count, depth)."""
+    intr, scale, n = W.Intrinsics(), C.c_double(), C.c_int()
+    _check(lib().wtref_read_depth(str(path).encode(), frame, C.byref(intr), C.byref(scale), C.byref(n), None))
+    d = np.zeros((intr.height, intr.width), np.float32)
+    _check(lib().wtref_read_depth(str(path).encode(), frame, None, None, None, _p(d)))
+    return intr, scale.value, n.value, d
+
+
+def run_tracking(model: RefModel, path, cfg: W.TrackConfigC, init_theta=None):
+    """run_tracking (tracker.cpp:70-100) over a .wts: {theta, joints, final_phi}."""
+    L, V = model.sizes()[:2]
+    F = read_depth(path, 0)[2]
+    th, jt, ph = np.zeros((F, L)), np.zeros((F, L, 3)), np.zeros((V, 3))
+    init = None if init_theta is None else np.ascontiguousarray(init_theta, float)
+    _check(lib().wtref_run_tracking(model.h, str(path).encode(), C.byref(cfg), _p(init), _p(th), _p(jt), _p(ph)))
+    return dict(theta=th, joints=jt, final_phi=ph)

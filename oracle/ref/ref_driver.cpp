@@ -679,4 +679,69 @@ int wtref_rasterize(const wtref_model* m, const double* theta, const double* phi
   });
 }
 
+// ---- sequence files and the sequence driver ------------------------------------------
+
+// SequenceWriter (seqio.cpp:493-535): n frames of H*W float depth.
+int wtref_write_sequence(const char* path, const wt_intrinsics* intr, double depth_scale,
+                         const float* frames, int n) {
+  return guarded([&] {
+    SequenceHeader h;
+    h.width = static_cast<std::uint32_t>(intr->width);
+    h.height = static_cast<std::uint32_t>(intr->height);
+    h.fx = intr->fx;
+    h.fy = intr->fy;
+    h.cx = intr->cx;
+    h.cy = intr->cy;
+    h.frame_count = static_cast<std::uint32_t>(n);
+    h.depth_scale = depth_scale;
+    SequenceWriter w(path, h);
+    const std::size_t px = static_cast<std::size_t>(intr->width) * intr->height;
+    for (int f = 0; f < n; ++f)
+      w.write_depth(std::vector<float>(frames + f * px, frames + (f + 1) * px));
+    w.close();
+  });
+}
+
+// SequenceReader::read_depth (seqio.cpp:476-487) of frame f; header out.
+int wtref_read_depth(const char* path, int f, wt_intrinsics* intr, double* depth_scale, int* frame_count,
+                     float* depth) {
+  return guarded([&] {
+    SequenceReader r(path);
+    const SequenceHeader& h = r.header();
+    if (intr) *intr = wt_intrinsics{h.fx, h.fy, h.cx, h.cy, static_cast<int>(h.width), static_cast<int>(h.height)};
+    if (depth_scale) *depth_scale = h.depth_scale;
+    if (frame_count) *frame_count = r.frame_count();
+    if (depth) {
+      const std::vector<float> d = r.read_depth(f);
+      std::copy(d.begin(), d.end(), depth);
+    }
+  });
+}
+
+// run_tracking (tracker.cpp:70-100) over a .wts file: per-frame theta [F*L],
+// joint origins [F*L*3], final phi [V*3].
+int wtref_run_tracking(const wtref_model* m, const char* path, const wt_track_config* cfg,
+                       const double* init_theta, double* theta_out, double* joints_out, double* phi_out) {
+  return guarded([&] {
+    const Skeleton& sk = m->bundle.skeleton;
+    const TrackConfig tc = to_track(cfg);
+    const ModelBundle tracked = tc.mode == TrackMode::rigid ? rigidify(m->bundle) : m->bundle;
+    SequenceReader reader(path);
+    const Pose init = init_theta ? to_pose(init_theta, sk.joint_count()) : sk.zero_pose();
+    const TrackOutputs out = run_tracking(tracked, reader, tc, init);
+    const int L = sk.link_count(), J = sk.joint_count();
+    for (int f = 0; f < out.estimate.frame_count(); ++f) {
+      for (int k = 0; k < J; ++k) theta_out[f * J + k] = out.estimate.theta[static_cast<std::size_t>(f)][k];
+      for (int j = 0; j < L; ++j)
+        for (int c = 0; c < 3; ++c)
+          joints_out[(f * L + j) * 3 + c] =
+              out.estimate.joints[static_cast<std::size_t>(f)][static_cast<std::size_t>(j)][c];
+    }
+    if (phi_out)
+      for (std::size_t i = 0; i < out.final_phi.size(); ++i)
+        for (int c = 0; c < 3; ++c) phi_out[i * 3 + c] = out.final_phi[i][c];
+  });
+}
+
 }  // extern "C"
+

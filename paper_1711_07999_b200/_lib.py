@@ -13,6 +13,7 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libwt_gpu.so"
 
+ABI_VERSION = 1  # WT_ABI_VERSION, include/wt_gpu.h
 WT_OK, WT_EINVAL, WT_ELENGTH, WT_ECUDA, WT_ENOMEM, WT_ENOTPD, WT_ENODEV = range(7)
 MODE_DYNAMIC, MODE_SHAPE_MATCH, MODE_SMOOTH_BIND, MODE_RIGID = range(4)
 JOINT_HINGE, JOINT_PRISMATIC = 0, 1
@@ -89,7 +90,7 @@ EXPORTS = [
     "wt_gpu_track_frame_cloud", "wt_gpu_optimize_pose", "wt_gpu_optimize_shape", "wt_gpu_skin",
     "wt_gpu_associate", "wt_gpu_associate_posed", "wt_gpu_normal_system", "wt_gpu_solve_step",
     "wt_gpu_solve_vertices", "wt_gpu_render_depth", "wt_gpu_stream", "wt_gpu_track_async", "wt_gpu_sync",
-    "wt_gpu_profile_frame",
+    "wt_gpu_profile_frame", "wt_gpu_track_sequence", "wt_gpu_joint_positions",
 ]
 KERNEL_KINDS = ["fk", "skin", "normals+bucket", "scatter", "search+average", "pose_system+solve",
                 "shape_step", "shape_stats"]
@@ -163,6 +164,8 @@ def _declare(L: C.CDLL) -> None:
     L.wt_gpu_stream.restype = vp
     L.wt_gpu_track_async.argtypes = [vp, P(TrackConfigC)]
     L.wt_gpu_sync.argtypes = [vp]
+    L.wt_gpu_track_sequence.argtypes = [vp, vp, C.c_int32, C.c_double, P(TrackConfigC), vp, vp]
+    L.wt_gpu_joint_positions.argtypes = [vp, vp]
     L.wt_gpu_profile_frame.argtypes = [vp, P(TrackConfigC), vp, vp, C.c_int32, P(C.c_int32)]
 
 

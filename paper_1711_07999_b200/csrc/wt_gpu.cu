@@ -154,7 +154,22 @@ struct wt_gpu_ctx {
 
   std::map<GraphKey, cudaGraphExec_t> graphs;
 
+  // sequence driver: pinned staging + device double buffer + copy stream
+  cudaStream_t copy_stream = nullptr;
+  float* seq_pinned[2] = {nullptr, nullptr};
+  float* seq_depth[2] = {nullptr, nullptr};
+  cudaEvent_t seq_h2d[2] = {nullptr, nullptr};     // upload from slot b finished
+  cudaEvent_t seq_ingest[2] = {nullptr, nullptr};  // ingest of slot b finished
+  double* rec_buf = nullptr;                       // [cap_rec * L * 4] theta + joints
+  int cap_rec = 0;
+
   ~wt_gpu_ctx() {
+    for (int b = 0; b < 2; ++b) {
+      if (seq_pinned[b]) cudaFreeHost(seq_pinned[b]);
+      if (seq_h2d[b]) cudaEventDestroy(seq_h2d[b]);
+      if (seq_ingest[b]) cudaEventDestroy(seq_ingest[b]);
+    }
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
     if (h_kin) cudaFreeHost(h_kin);
@@ -979,6 +994,101 @@ int wt_gpu_profile_frame(wt_gpu_ctx* c, const wt_track_config* cfg, int32_t* kin
     }
     cudaEventDestroy(e0);
     if (n_out) *n_out = n;
+  });
+}
+
+namespace {
+void ensure_seq(wt_gpu_ctx* c, int frames) {
+  if (!c->copy_stream) {
+    WT_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      WT_CUDA(cudaMallocHost(&c->seq_pinned[b], sizeof(float) * c->P));
+      c->seq_depth[b] = c->mem.alloc<float>(c->P);
+      WT_CUDA(cudaEventCreateWithFlags(&c->seq_h2d[b], cudaEventDisableTiming));
+      WT_CUDA(cudaEventCreateWithFlags(&c->seq_ingest[b], cudaEventDisableTiming));
+    }
+  }
+  if (frames > c->cap_rec) {
+    c->cap_rec = std::max(frames, 64);
+    c->rec_buf = c->mem.alloc<double>(static_cast<size_t>(c->cap_rec) * c->L * 4);
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+}  // namespace
+
+int wt_gpu_track_sequence(wt_gpu_ctx* c, const float* frames, int32_t n_frames, double depth_scale,
+                          const wt_track_config* cfg, double* theta_out, double* joints_out) {
+  if (!c || !cfg || (n_frames > 0 && !frames) || n_frames < 0) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    check_assoc(&cfg->assoc);
+    if (cfg->kin.iterations < 0 || cfg->shape.iterations < 0) fail(WT_EINVAL, "negative iteration count");
+    if (n_frames == 0) return;
+    ensure_stats(c, cfg->kin.iterations, cfg->shape.iterations);
+    ensure_seq(c, n_frames);
+    const bool on_device = is_device_ptr(frames);
+    const size_t P = static_cast<size_t>(c->P);
+    const int L = c->L;
+    double* rec_theta = c->rec_buf;
+    double* rec_joints = c->rec_buf + static_cast<size_t>(c->cap_rec) * L;
+    for (int f = 0; f < n_frames; ++f) {
+      const float* src = frames + static_cast<size_t>(f) * P;
+      const float* dev_depth = src;
+      const int b = f & 1;
+      if (!on_device) {
+        // the pinned slot is free once its previous upload (frame f-2) landed
+        WT_CUDA(cudaEventSynchronize(c->seq_h2d[b]));
+        std::memcpy(c->seq_pinned[b], src, sizeof(float) * P);
+        // the device slot is free once frame f-2's ingest has read it
+        WT_CUDA(cudaStreamWaitEvent(c->copy_stream, c->seq_ingest[b], 0));
+        WT_CUDA(cudaMemcpyAsync(c->seq_depth[b], c->seq_pinned[b], sizeof(float) * P, cudaMemcpyHostToDevice,
+                                c->copy_stream));
+        WT_CUDA(cudaEventRecord(c->seq_h2d[b], c->copy_stream));
+        WT_CUDA(cudaStreamWaitEvent(c->stream, c->seq_h2d[b], 0));
+        dev_depth = c->seq_depth[b];
+      }
+      ingest(c, dev_depth, depth_scale, nullptr, nullptr);
+      if (!on_device) WT_CUDA(cudaEventRecord(c->seq_ingest[b], c->stream));
+      c->frame_loaded = true;
+      c->frame_on_rays = true;
+      const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
+                             (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
+      const int start = c->cur;
+      run_graph(c, track_key(c, cfg, shape_now, 1.0), [&] { enq_track(c, cfg, shape_now); });
+      c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
+      ++c->frame_index;
+      wt::k_record<<<1, 32, 0, c->stream>>>(c->dm, c->ds.theta, rec_theta + static_cast<size_t>(f) * L,
+                                            rec_joints + static_cast<size_t>(f) * L * 3);
+      check_launch();
+    }
+    if (theta_out)
+      WT_CUDA(cudaMemcpyAsync(theta_out, rec_theta, sizeof(double) * n_frames * L, cudaMemcpyDeviceToHost,
+                              c->stream));
+    if (joints_out)
+      WT_CUDA(cudaMemcpyAsync(joints_out, rec_joints, sizeof(double) * n_frames * L * 3,
+                              cudaMemcpyDeviceToHost, c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int wt_gpu_joint_positions(wt_gpu_ctx* c, double* joints_out) {
+  if (!c || !joints_out) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    ensure_seq(c, 1);
+    wt::k_record<<<1, 32, 0, c->stream>>>(c->dm, c->ds.theta, nullptr, c->rec_buf);
+    check_launch();
+    WT_CUDA(cudaMemcpyAsync(joints_out, c->rec_buf, sizeof(double) * c->L * 3, cudaMemcpyDeviceToHost,
+                            c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

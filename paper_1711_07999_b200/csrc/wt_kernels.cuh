@@ -1188,4 +1188,18 @@ __global__ void k_solve_vertices(int n, const double* dr, const double* r, const
   singular[i] = ok ? 0 : 1;
 }
 
+// run_tracking's per-frame record (tracker.cpp:84-90): theta and the world
+// origin of every link, transform_point(forward_kinematics(theta)[j], 0).
+// One thread: L <= 64 links, off the per-iteration path.
+__global__ void k_record(DevModel m, const double* theta, double* theta_out, double* joints_out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  DQ fk[64];
+  fk_all(m.links, m.L, theta, fk);
+  const double zero[3] = {0.0, 0.0, 0.0};
+  for (int j = 0; j < m.L; ++j) {
+    if (theta_out) theta_out[j] = theta[j];
+    if (joints_out) dq_transform_point(fk[j], zero, joints_out + 3 * j);
+  }
+}
+
 }  // namespace wt

@@ -69,6 +69,10 @@ class SequenceReader:
             raise ValidationError(WT_EINVAL, f"sequence {self.path}: frame {frame} out of range")
         return np.array(self._mm[frame], dtype=np.float32)
 
+    def frames(self) -> np.ndarray:
+        """All frames [F,H,W] float32 (one read; the GPU driver stages them)."""
+        return np.array(self._mm, dtype=np.float32)
+
 
 class SequenceWriter:
     """SequenceWriter (seqio.cpp:493-535)."""

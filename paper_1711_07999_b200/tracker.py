@@ -235,6 +235,30 @@ class Tracker:
             return None
         return FrameStats(st.frame, _kin_list(self._kin, st.n_kin), _shape_list(self._shape, st.n_shape))
 
+    def track_sequence(self, frames, cfg: TrackConfig, depth_scale: float = 1.0):
+        """run_tracking (tracker.cpp:70-100) over depth frames [F,H,W] (host
+        array, or a device address with n_frames given as frames=(ptr, F)):
+        returns (theta [F,L], joints [F,L,3]). Uploads overlap the solves."""
+        if isinstance(frames, tuple):
+            addr, F = frames
+        else:
+            arr = np.ascontiguousarray(frames, dtype=np.float32)
+            F = arr.shape[0] if arr.size else 0
+            if arr.size and arr[0].size != self.intr.width * self.intr.height:
+                raise _lib.LengthMismatch(_lib.WT_ELENGTH, "depth image size differs from intrinsics grid")
+            addr = ptr(arr)
+        L = self.bundle.link_count
+        th, jt = np.zeros((F, L)), np.zeros((F, L, 3))
+        check(lib().wt_gpu_track_sequence(self._ctx, addr, F, depth_scale, C.byref(cfg.c()), ptr(th), ptr(jt)),
+              self._ctx)
+        return th, jt
+
+    def joint_positions(self) -> np.ndarray:
+        """Link origins at the current theta (tracker.cpp:84-86), [L,3]."""
+        out = np.zeros((self.bundle.link_count, 3))
+        check(lib().wt_gpu_joint_positions(self._ctx, ptr(out)), self._ctx)
+        return out
+
     def optimize_pose(self, kin: KinSolverConfig, assoc: AssocConfig = AssocConfig()) -> list:
         n = C.c_int32()
         check(lib().wt_gpu_optimize_pose(self._ctx, C.byref(kin.c()), C.byref(assoc.c()), self._kin, 64,

@@ -20,6 +20,7 @@ sys.path.insert(0, str(ROOT))
 from oracle import ref  # noqa: E402
 from paper_1711_07999_b200 import _lib as W  # noqa: E402
 from paper_1711_07999_b200.model import ModelBundle, humanoid_trajectory, make_humanoid  # noqa: E402
+from tests import rigs  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 MODEL_KEYS = ["parent", "parent_offset", "joint_kind", "joint_axis", "theta_index", "v0", "phi", "weight_count",
@@ -145,7 +146,62 @@ def association_scenes() -> None:
     np.savez_compressed(OUT / "association_scenes.npz", n=6, **rec)
 
 
+def bundle_arrays(prefix: str, b: ModelBundle) -> dict:
+    out = {f"{prefix}_{k}": getattr(b, k) for k in MODEL_KEYS}
+    out[f"{prefix}_poly_offsets"] = np.concatenate([[0], np.cumsum([len(p) for p in b.polys])]).astype(np.int32)
+    out[f"{prefix}_poly_items"] = np.concatenate([np.asarray(p, np.int32) for p in b.polys]).astype(np.int32)
+    return out
+
+
+def kat_fixture() -> None:
+    """The reference's own arm and sphere rigs (synth.cpp:425-494) with the
+    frames its closed-loop unit tests render (test_kinopt.cpp:320-446,
+    test_shapeopt.cpp:141-288), and the reference's answers on them."""
+    intr = rigs.kinect()
+    ic = intr.c()
+    arm = ref.RefModel.rig("arm")
+    sphere = ref.RefModel.rig("sphere")
+    ab, sb = arm.to_bundle(), sphere.to_bundle()
+    plate = rigs.camera_plate()
+    rp = ref.RefModel.from_bundle(plate)
+    out = {**bundle_arrays("arm", ab), **bundle_arrays("sphere", sb),
+           **bundle_arrays("sphere_sub1", sphere.subdivide(1).to_bundle()),
+           **bundle_arrays("arm_rigid", arm.rigidify().to_bundle())}
+    truth = np.zeros(3)
+    truth[1] = 0.1
+    out["arm_hinge_depth"] = arm.render_depth(truth, ic)[0]
+    out["plate_depth"] = rp.render_depth(np.zeros(1), ic)[0]
+    out["arm_traj_depth"] = np.array([arm.render_depth(rigs.arm_curves(3, f), ic, frame=f)[0] for f in range(10)])
+    bump = (sb.v0 - np.array([0.0, 0.0, 1.2]))
+    bump = bump / np.linalg.norm(bump, axis=1, keepdims=True) * 0.01
+    out["sphere_bump_phi"] = bump
+    out["sphere_bump_depth"] = sphere.render_depth(np.zeros(1), ic, phi=bump)[0]
+    out["sphere_depth"] = sphere.render_depth(np.zeros(1), ic)[0]
+    dent = rigs.dent_phi(sb.v0)
+    out["sphere_dent_phi"] = dent
+    out["sphere_dent_depth"] = sphere.render_depth(np.zeros(1), ic, phi=dent)[0]
+    # reference answers (threads = 1)
+    kin = W.KinConfig(12, 1, 1e-2, 1e-4, 1e-9, 0, 0, 0.0)
+    ac = W.AssocConfig(5, 0, 0.10)
+    pts, val = ref.depth_to_cloud(ic, out["arm_hinge_depth"])
+    for refresh in (1, 3):
+        kin.assoc_refresh = refresh
+        rt = ref.RefTracker(arm, np.zeros(3))
+        st = rt.optimize_pose(ic, pts, val, kin, ac)
+        out[f"arm_hinge_theta_r{refresh}"] = rt.get_state()[0]
+        out[f"arm_hinge_stats_r{refresh}"] = np.array([[s.associated, s.residual_sum, s.step_norm,
+                                                         s.solver_skipped] for s in st])
+    rt = ref.RefTracker(sphere, np.zeros(1))
+    pts, val = ref.depth_to_cloud(ic, out["sphere_dent_depth"])
+    sc = W.ShapeConfig(2, 0, 0.05, 0.5, 1e-2, 1e-9)
+    for f in range(3):
+        rt.optimize_shape(ic, pts, val, sc, ac, stats=False)
+    out["sphere_dent_phi3"] = rt.get_state()[1]
+    np.savez_compressed(OUT / "kat_rigs.npz", **out)
+
+
 if __name__ == "__main__":
+    kat_fixture()
     biped_fixture()
     humanoid_fixture()
     association_scenes()
