@@ -17,7 +17,7 @@
 namespace wt {
 
 constexpr int kVThreads = 256;    // per-vertex / per-pixel kernels
-constexpr double kFixPoint = 4294967296.0;        // 2^32: observation sums
+constexpr double kFixPoint = 17592186044416.0;     // 2^44: observation sums (<= 121 px/vertex, |x| < 4096 m)
 constexpr double kFixSys = 1099511627776.0;       // 2^40: JtJ / Jtr / shape sums
 constexpr double kFixRes = 17592186044416.0;      // 2^44: residual sum of squares
 constexpr int kRedCopies = 8;  // CTAs spread their fixed-point atomics over this many slot copies

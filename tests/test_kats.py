@@ -75,7 +75,8 @@ def test_single_vertex_hand_computed_residual(impl):
     pts, pv = rigs.frame_from_points(intr, [[0, 0, 1.01]])
     r = impl.associate(intr, v, n, valid, pts, pv, 5, 0.10)
     assert r["count"][0] == 1
-    assert np.abs(r["p_tilde"][0] - [0, 0, 1.01]).max() <= 1e-15
+    # reference: exact fp64 (1e-15); GPU: 2^-44 m fixed-point observation sums
+    assert np.abs(r["p_tilde"][0] - [0, 0, 1.01]).max() <= tol(impl, 1e-15, 1e-13)
     assert abs(r["residual"][0] - (-0.01)) <= 1e-9 * 0.01
 
 
@@ -96,7 +97,7 @@ def test_multiple_observations_average(impl):
     pts, pv = rigs.frame_from_points(intr, obs)
     r = impl.associate(intr, v, n, valid, pts, pv, 5, 0.10)
     assert r["count"][0] == 3
-    assert np.abs(r["p_tilde"][0] - obs.sum(0) / 3.0).max() <= 1e-12
+    assert np.abs(r["p_tilde"][0] - obs.sum(0) / 3.0).max() <= 1e-12  # both arms
 
 
 def test_matches_brute_force_whenever_window_reaches(impl):
