@@ -132,10 +132,33 @@ def trajectory(bundle, frame: int, seq: int) -> np.ndarray:
     return humanoid_trajectory(bundle.link_count, frame, phase_offset=0.7 * seq)
 
 
+def cpu_port(bundle, intr, cfg, frames_host, seconds: float, theta0) -> dict:
+    """Fallback when oracle/_ref was not built: the C restatement
+    (oracle/wt_oracle.c, single thread) over a bounded sample."""
+    from oracle import c_oracle
+    ot = c_oracle.OracleTracker(bundle, intr.c(), theta0)
+    c = cfg.c()
+    ot.load_depth(frames_host[0])
+    ot.track_loaded(c)
+    n, t0 = 0, time.perf_counter()
+    while n + 1 < len(frames_host):
+        ot.load_depth(frames_host[n + 1])
+        ot.track_loaded(c)
+        n += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": f"{n} frames of the same workload after 1 warm-up frame, C restatement of the reference "
+                      f"(oracle/wt_oracle.c, 1 thread), {dt:.1f} s"}
+
+
 def cpu_reference(bundle, intr, cfg, frames_host, seconds: float, theta0) -> dict:
     """The reference's own track_frame (oracle/_ref) on all host threads over a
     bounded sample of the same frames."""
     from oracle import ref
+    if not ref.available():
+        return cpu_port(bundle, intr, cfg, frames_host, seconds, theta0)
     rm = ref.RefModel.from_bundle(bundle)
     rt = ref.RefTracker(rm, theta0)
     c = cfg.c()
@@ -294,6 +317,23 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.synchronize()
     e2e_ms = sum(e_st[k].elapsed_time(e_en[k]) for k in range(args.steps))
 
+    # ---- the sequence driver: all K frames in one call from pinned host memory ----
+    # (uploads overlap the solves; no L2 flush inside a sequence, so reported
+    # beside e2e rather than as it)
+    reset()
+    seq_frames = frames_host[0][args.warmup + 1: args.warmup + 1 + args.steps]
+    th_out = np.zeros((args.steps, bundle.link_count))
+    jt_out = np.zeros((args.steps, bundle.link_count, 3))
+    trackers[0].set_state(theta=trajectory(bundle, args.warmup, rank * S), frame_index=args.warmup)
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    q0.record(st0)
+    W.check(L.wt_gpu_track_sequence(trackers[0]._ctx, seq_frames.data_ptr(), args.steps, 1.0, C.byref(ccfg),
+                                    th_out.ctypes.data, jt_out.ctypes.data), trackers[0]._ctx)
+    q1.record(st0)
+    torch.cuda.synchronize()
+    seq_ms = q0.elapsed_time(q1)
+
     # ---- per-kernel device times inside the real frame (events between kernels) ----
     kinds = (C.c_int32 * 512)()
     ms = (C.c_float * 512)()
@@ -354,6 +394,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                    "associated_vertices": A},
         "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": 4 * P * S,
                 "d2h_bytes_per_step": S * (8 * bundle.link_count + 32 * (cfg.kin.iterations + cfg.shape.iterations))},
+        "e2e_sequence": {"value": args.steps / (seq_ms * 1e-3), "unit": "frames/s",
+                         "api": "wt_gpu_track_sequence (one call, K pinned host frames, uploads overlapped, "
+                                "theta + joints read back)", "h2d_bytes_per_step": 4 * P,
+                         "d2h_bytes_per_step": 32 * bundle.link_count, "l2": "not flushed inside the sequence"},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dk["achieved_gbs"], "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
                      "traffic": None, "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"]},
