@@ -236,7 +236,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     trackers = [Tracker(bundle, intr, trajectory(bundle, 0, rank * S + s), device=local_rank) for s in range(S)]
     L = W.lib()
     ccfg = cfg.c()
-    nframes = args.warmup + args.steps + 1
+    nprof = 3  # profiled frames (per-kernel event timing) after the timed ones
+    nframes = args.warmup + max(args.steps, nprof + 1) + 1
     P = intr.width * intr.height
     # frames rendered on the GPU straight into HBM, plus pinned host copies
     frames_dev = [torch.empty((nframes, intr.height, intr.width), dtype=torch.float32, device=dev) for _ in range(S)]
@@ -339,7 +340,6 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     ms = (C.c_float * 512)()
     n = C.c_int32()
     per_kind = {}
-    nprof = 3
     nker = 0
     # profile frames that follow the tracker's state (steady tracking)
     trackers[0].set_state(theta=trajectory(bundle, args.warmup, rank * S), phi=np.zeros((bundle.vertex_count, 3)),
@@ -409,8 +409,12 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_reference(bundle, intr, cfg, [frames_host[0][f].numpy() for f in range(nframes)],
-                                             args.cpu_seconds, trajectory(bundle, 0, 0))
+        # a bounded CPU sample of the same workload: enough frames of the same
+        # trajectory for ~cpu_seconds of reference work (rendered on the GPU)
+        ncpu = int(args.cpu_seconds * 40) + 2
+        cpu_frames = [trackers[0].render_depth(trajectory(bundle, f, 0), frame=f)[0] for f in range(ncpu)]
+        line["cpu_baseline"] = cpu_reference(bundle, intr, cfg, cpu_frames, args.cpu_seconds,
+                                             trajectory(bundle, 0, 0))
     print(json.dumps(line), flush=True)
     for t_ in trackers:
         t_.close()

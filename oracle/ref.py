@@ -33,7 +33,7 @@ def build() -> bool:
     the GPU box, which only receives the prebuilt .so)."""
     if not REF_SRC.exists():
         return LIB_PATH.exists()
-    subprocess.run(["make", "-s", "-j8", "-C", str(HERE / "ref")], check=True)
+    subprocess.run(["make", "-s", "-j8", "-C", str(HERE / "ref"), "all", "adapter"], check=True)
     return LIB_PATH.exists()
 
 
