@@ -336,11 +336,11 @@ void optimize_shape(TrackerState& state, const CloudFrame& frame, const Intrinsi
 
 TrackOutputs run_tracking(const ModelBundle& bundle, SequenceReader& reader, const TrackConfig& cfg,
                           const Pose& init, const FrameCallback& callback) {
-  const ModelBundle tracked_storage = cfg.mode == TrackMode::rigid ? rigidify(bundle) : ModelBundle{};
-  const ModelBundle& tracked = cfg.mode == TrackMode::rigid ? tracked_storage : bundle;
-  TrackerState state = make_tracker(tracked, init);
+  // as tracker.cpp:75-77: the bundle is tracked as given (callers rigidify
+  // for the rigid mode, e.g. bindings.cpp:250-251)
+  TrackerState state = make_tracker(bundle, init);
   const Intrinsics intr = reader.header().intrinsics();
-  Sequence seq(tracked, intr);
+  Sequence seq(bundle, intr);
   seq.upload(state);
 
   TrackOutputs out;

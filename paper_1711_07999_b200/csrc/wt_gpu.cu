@@ -1065,7 +1065,7 @@ int wt_gpu_track_sequence(wt_gpu_ctx* c, const float* frames, int32_t n_frames, 
       run_graph(c, track_key(c, cfg, shape_now, 1.0), [&] { enq_track(c, cfg, shape_now); });
       c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
       ++c->frame_index;
-      wt::k_record<<<1, 32, 0, c->stream>>>(c->dm, c->ds.theta, rec_theta + static_cast<size_t>(f) * L,
+      wt::k_record<<<1, 64, 0, c->stream>>>(c->dm, c->ds, rec_theta + static_cast<size_t>(f) * L,
                                             rec_joints + static_cast<size_t>(f) * L * 3);
       check_launch();
     }
@@ -1084,7 +1084,10 @@ int wt_gpu_joint_positions(wt_gpu_ctx* c, double* joints_out) {
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
     ensure_seq(c, 1);
-    wt::k_record<<<1, 32, 0, c->stream>>>(c->dm, c->ds.theta, nullptr, c->rec_buf);
+    // FK of the current theta into the hook state, then the origins
+    WT_CUDA(cudaMemcpyAsync(c->hs.theta, c->ds.theta, sizeof(double) * c->L, cudaMemcpyDeviceToDevice, c->stream));
+    wt::k_fk<<<1, 128, 0, c->stream>>>(c->dm, c->hs);
+    wt::k_record<<<1, 64, 0, c->stream>>>(c->dm, c->hs, nullptr, c->rec_buf);
     check_launch();
     WT_CUDA(cudaMemcpyAsync(joints_out, c->rec_buf, sizeof(double) * c->L * 3, cudaMemcpyDeviceToHost,
                             c->stream));

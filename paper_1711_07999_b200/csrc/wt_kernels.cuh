@@ -1189,16 +1189,15 @@ __global__ void k_solve_vertices(int n, const double* dr, const double* r, const
 }
 
 // run_tracking's per-frame record (tracker.cpp:84-90): theta and the world
-// origin of every link, transform_point(forward_kinematics(theta)[j], 0).
-// One thread: L <= 64 links, off the per-iteration path.
-__global__ void k_record(DevModel m, const double* theta, double* theta_out, double* joints_out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  DQ fk[64];
-  fk_all(m.links, m.L, theta, fk);
-  const double zero[3] = {0.0, 0.0, 0.0};
-  for (int j = 0; j < m.L; ++j) {
-    if (theta_out) theta_out[j] = theta[j];
-    if (joints_out) dq_transform_point(fk[j], zero, joints_out + 3 * j);
+// origin of every link, transform_point(H_0j, 0), from the FK the frame's
+// last pose-solve tail (or k_fk) left in s.fk for the current theta.
+__global__ void k_record(DevModel m, DevState s, double* theta_out, double* joints_out) {
+  const int j = threadIdx.x;
+  if (j >= m.L) return;
+  if (theta_out) theta_out[j] = s.theta[j];
+  if (joints_out) {
+    const double zero[3] = {0.0, 0.0, 0.0};
+    dq_transform_point(dq_load(s.fk + 8 * j), zero, joints_out + 3 * j);
   }
 }
 

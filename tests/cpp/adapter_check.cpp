@@ -132,8 +132,10 @@ int main(int argc, char** argv) {
       cfg.kin.iterations = 5;
       cfg.shape.iterations = 2;
       SequenceReader ra(seq), rb(seq);
-      const TrackOutputs a = run_tracking(bundle, ra, cfg, pose_at(sk, 0));
-      const TrackOutputs b = gpu::run_tracking(bundle, rb, cfg, pose_at(sk, 0));
+      // callers rigidify for the rigid mode (bindings.cpp:250-251)
+      const ModelBundle tracked = mode == TrackMode::rigid ? rigidify(bundle) : bundle;
+      const TrackOutputs a = run_tracking(tracked, ra, cfg, pose_at(sk, 0));
+      const TrackOutputs b = gpu::run_tracking(tracked, rb, cfg, pose_at(sk, 0));
       double th = 0.0, jt = 0.0;
       for (int f = 0; f < a.estimate.frame_count(); ++f) {
         th = std::max(th, max_abs(a.estimate.theta[static_cast<std::size_t>(f)], b.estimate.theta[static_cast<std::size_t>(f)]));
