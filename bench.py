@@ -56,7 +56,8 @@ def alg_bytes(kind: str, V: int, P: int, A: int, Vvis: int) -> float:
         "normals+bucket": 77 * V + 37 * V + 16 * P,  # K2 + K3 histogram/scan
         "scatter": 8 * Vvis,                  # K3 scatter part (items)
         "search+average": 12 * P + 16 * Vvis + 8 * P + 72 * V,  # K4 + K5
-        "pose_system+solve": 4 * V + 61 * A,  # K6 + K7
+        "pose_system": 4 * V + 61 * A,        # K6
+        "pose_solve": 0,                      # K7 (+K0 FK): one CTA, latency only
         "shape_step": 81 * V,                 # K8
         "shape_stats": 72 * V,
         "fk": 0,

@@ -92,8 +92,8 @@ EXPORTS = [
     "wt_gpu_solve_vertices", "wt_gpu_render_depth", "wt_gpu_stream", "wt_gpu_track_async", "wt_gpu_sync",
     "wt_gpu_profile_frame", "wt_gpu_track_sequence", "wt_gpu_joint_positions",
 ]
-KERNEL_KINDS = ["fk", "skin", "normals+bucket", "scatter", "search+average", "pose_system+solve",
-                "shape_step", "shape_stats"]
+KERNEL_KINDS = ["fk", "skin", "normals+bucket", "scatter", "search+average", "pose_system",
+                "shape_step", "shape_stats", "pose_solve"]
 
 
 class WarptrackError(RuntimeError):

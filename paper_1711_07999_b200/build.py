@@ -28,11 +28,13 @@ UNITS = [
 ]
 
 
-def _run(cmd: list[str]) -> None:
+def _run(cmd: list[str], echo: bool = False) -> None:
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
         raise RuntimeError(f"command failed: {' '.join(cmd)}")
+    if echo:
+        sys.stderr.write(proc.stdout + proc.stderr)
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -48,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         cmd = [NVCC] + COMMON + extra + ["-c", str(CSRC / unit), "-o", str(obj)]
         if verbose:
             cmd += ["-Xptxas", "-v"]
-        _run(cmd)
+        _run(cmd, echo=verbose)
         objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
     _run([NVCC] + ARCH + ["-shared", "-o", str(tmp)] + objs + ["-lcudart"])

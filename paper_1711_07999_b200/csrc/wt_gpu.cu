@@ -203,7 +203,7 @@ void check_launch() {
 }
 
 // kernel kinds reported by wt_gpu_profile_frame
-enum { K_FK = 0, K_SKIN, K_NORMALS, K_SCATTER, K_SEARCH, K_POSE, K_SHAPE, K_SHAPE_AFTER, K_NKIND };
+enum { K_FK = 0, K_SKIN, K_NORMALS, K_SCATTER, K_SEARCH, K_POSE, K_SHAPE, K_SHAPE_AFTER, K_POSE_SOLVE, K_NKIND };
 
 void mark(wt_gpu_ctx* c, int kind) {
   check_launch();
@@ -388,15 +388,16 @@ int pose_q(int L) {
   return ne <= 32 * 8 ? 8 : ne <= 32 * 16 ? 16 : ne <= 32 * 32 ? 32 : 68;
 }
 
-template <int Q>
+template <int Q, int TPL>
 void launch_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt::PoseArgs& pa) {
-  wt::k_pose_system<Q><<<pose_grid(c), pose_threads(c), wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32),
-                         c->stream>>>(c->dm, s, phi, pa);
+  wt::k_pose_system<Q, TPL><<<pose_grid(c), pose_threads(c),
+                              wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32), c->stream>>>(c->dm, s, phi,
+                                                                                                  pa);
 }
 
-template <int Q>
+template <int Q, int TPL>
 void pose_attr(wt_gpu_ctx* c) {
-  WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system<Q, TPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32))));
 }
 
@@ -414,13 +415,19 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
   pa.count_in = count_in;
   pa.res_in = res_in;
   pa.dbg = c->pose_dbg;
-  switch (pose_q(c->L)) {
-    case 8: launch_pose<8>(c, s, phi, pa); break;
-    case 16: launch_pose<16>(c, s, phi, pa); break;
-    case 32: launch_pose<32>(c, s, phi, pa); break;
-    default: launch_pose<68>(c, s, phi, pa); break;
+  if (wt::pose_tiles(c->L) <= 32) {
+    launch_pose<1, 1>(c, s, phi, pa);
+  } else {
+    switch (pose_q(c->L)) {
+      case 8: launch_pose<8, 0>(c, s, phi, pa); break;
+      case 16: launch_pose<16, 0>(c, s, phi, pa); break;
+      case 32: launch_pose<32, 0>(c, s, phi, pa); break;
+      default: launch_pose<68, 0>(c, s, phi, pa); break;
+    }
   }
   mark(c, K_POSE);
+  wt::k_pose_solve<<<1, 256, wt::pose_solve_smem_bytes(c->L), c->stream>>>(c->dm, s, pa);
+  mark(c, K_POSE_SOLVE);
 }
 
 int shape_grid(const wt_gpu_ctx* c) { return std::max(1, std::min(vgrid(c->V), 4 * 148)); }
@@ -762,11 +769,15 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8 + 4 * 296 + 8);
     if (wt::pose_smem_bytes(L, c->NP, pose_threads(c) / 32) > 227 * 1024)
       fail(WT_EINVAL, "skeleton too large for the pose kernel's shared memory");
-    switch (pose_q(L)) {
-      case 8: pose_attr<8>(c); break;
-      case 16: pose_attr<16>(c); break;
-      case 32: pose_attr<32>(c); break;
-      default: pose_attr<68>(c); break;
+    if (wt::pose_tiles(L) <= 32) {
+      pose_attr<1, 1>(c);
+    } else {
+      switch (pose_q(L)) {
+        case 8: pose_attr<8, 0>(c); break;
+        case 16: pose_attr<16, 0>(c); break;
+        case 32: pose_attr<32, 0>(c); break;
+        default: pose_attr<68, 0>(c); break;
+      }
     }
     WT_CUDA(cudaStreamSynchronize(c->stream));
   });

@@ -220,21 +220,30 @@ __device__ __forceinline__ bool blend_vertex(const double* s_off, double4 w, uch
 // FK / link offsets / dchain for the current theta (skeleton.cpp:56-108),
 // executed by one whole CTA. Also used by the pose-solve tail.
 
-__device__ void block_fk(const DevModel& m, const DevState& s, const double* theta_in) {
+// The link table and tree depths block_fk reads, staged in shared memory
+// ahead of time (the pose kernel stages them in its prologue so its solve
+// tail pays no global-memory latency for them).
+struct FkTables {
+  LinkDesc sl[64];
+  int dep[64];
+};
+
+__device__ __forceinline__ void fk_stage(const DevModel& m, FkTables& t) {
+  const int n4 = m.L * static_cast<int>(sizeof(LinkDesc) / sizeof(double));
+  const double* src = reinterpret_cast<const double*>(m.links);
+  double* dst = reinterpret_cast<double*>(t.sl);
+  for (int k = threadIdx.x; k < n4; k += blockDim.x) dst[k] = src[k];
+  for (int j = threadIdx.x; j < m.L; j += blockDim.x) t.dep[j] = m.link_depth[j];
+}
+
+// Requires fk_stage(m, t) and a barrier before the call.
+__device__ void fk_run(const DevModel& m, const DevState& s, const double* theta_in, const FkTables& t,
+                       long long* stamps = nullptr) {
   __shared__ DQ fk[64];
   __shared__ DQ loc[64];
   __shared__ double cs[64][2];
-  __shared__ int par[64];
-  __shared__ int dep[64];
-  __shared__ LinkDesc sl[64];
   const int L = m.L;
-  {
-    const int n4 = L * static_cast<int>(sizeof(LinkDesc) / sizeof(double));
-    const double* src = reinterpret_cast<const double*>(m.links);
-    double* dst = reinterpret_cast<double*>(sl);
-    for (int k = threadIdx.x; k < n4; k += blockDim.x) dst[k] = src[k];
-  }
-  __syncthreads();
+  const LinkDesc* sl = t.sl;
   // joint transforms and local offsets in parallel (one link per thread);
   // each joint's half-angle sincos is evaluated once ...
   for (int j = threadIdx.x; j < L; j += blockDim.x) {
@@ -244,17 +253,23 @@ __device__ void block_fk(const DevModel& m, const DevState& s, const double* the
     sincos(th * 0.5, &sn, &cn);
     cs[j][0] = cn;
     cs[j][1] = sn;
-    par[j] = l.parent;
-    dep[j] = m.link_depth[j];
     loc[j] = dq_compose(dq_load(l.offset), dq_joint_cs(l.kind, l.axis, th, cn, sn));
   }
   __syncthreads();
-  // ... the parent chain one tree level at a time ...
-  for (int d = 0; d <= m.max_depth; ++d) {
-    for (int j = threadIdx.x; j < L; j += blockDim.x)
-      if (dep[j] == d) fk[j] = par[j] < 0 ? loc[j] : dq_compose(fk[par[j]], loc[j]);
-    __syncthreads();
+  if (stamps && threadIdx.x == 0) stamps[0] = clock64();
+  // ... then every link's chain independently, composed from the root down
+  // (the same left fold as forward_kinematics, so bitwise the same result)
+  // with no barrier per tree level ...
+  for (int j = threadIdx.x; j < L; j += blockDim.x) {
+    int path[64];
+    int n = 0;
+    for (int q = j; q >= 0; q = sl[q].parent) path[n++] = q;
+    DQ acc = loc[path[n - 1]];
+    for (int d = n - 2; d >= 0; --d) acc = dq_compose(acc, loc[path[d]]);
+    fk[j] = acc;
   }
+  __syncthreads();
+  if (stamps && threadIdx.x == 0) stamps[1] = clock64();
   // ... then offsets and the dchain blocks in parallel (skeleton.cpp:71-108)
   for (int j = threadIdx.x; j < L; j += blockDim.x) {
     dq_store(fk[j], s.fk + 8 * j);
@@ -269,6 +284,13 @@ __device__ void block_fk(const DevModel& m, const DevState& s, const double* the
     const DQ k_to_j = dq_compose(dq_inverse(fk[kl]), fk[j]);
     dq_store(dq_compose(dq_compose(pre, dj), dq_compose(k_to_j, dq_load(sl[j].bind_inv))), s.dchain + 8 * p);
   }
+}
+
+__device__ void block_fk(const DevModel& m, const DevState& s, const double* theta_in) {
+  __shared__ FkTables t;
+  fk_stage(m, t);
+  __syncthreads();
+  fk_run(m, s, theta_in, t);
 }
 
 __global__ void k_fk(DevModel m, DevState s) { block_fk(m, s, s.theta); }
@@ -611,14 +633,14 @@ __device__ __forceinline__ bool observed_mean(const unsigned long long* acc, int
 // thread updates trailing entries (i,j) listed in the (ea, eb) upper-triangle
 // table. A is row-major (lower triangle used, overwritten); b is overwritten;
 // x receives the solution. Must be called by all threads of the CTA.
-__device__ int block_ldlt_solve(int L, double* A, double* b, double* x, const unsigned short* ea,
+__device__ int block_ldlt_solve(int L, int lda, double* A, double* b, double* x, const unsigned short* ea,
                                 const unsigned short* eb, int NT) {
   __shared__ int s_ok;
   __shared__ double inv_d[64];
   if (threadIdx.x == 0) s_ok = 1;
   __syncthreads();
   for (int k = 0; k < L; ++k) {
-    const double dk = A[k * L + k];
+    const double dk = A[k * lda + k];
     if (!(dk > 0.0)) {  // uniform: every thread read the same pivot
       if (threadIdx.x == 0) s_ok = 0;
       break;
@@ -626,7 +648,7 @@ __device__ int block_ldlt_solve(int L, double* A, double* b, double* x, const un
     const double inv = __drcp_rn(dk);
     for (int e = threadIdx.x; e < NT; e += blockDim.x) {
       const int r = ea[e], c = eb[e];  // r <= c: update lower entry (c, r)
-      if (r > k) A[c * L + r] -= A[c * L + k] * A[r * L + k] * inv;
+      if (r > k) A[c * lda + r] -= A[c * lda + k] * A[r * lda + k] * inv;
     }
     if (threadIdx.x == 0) inv_d[k] = inv;
     __syncthreads();
@@ -638,7 +660,7 @@ __device__ int block_ldlt_solve(int L, double* A, double* b, double* x, const un
     for (int k = 0; k < L; ++k) {  // forward: (unit) L z = b
       const double zk = b[k];
       __syncwarp();
-      for (int i = k + 1 + lane; i < L; i += 32) b[i] -= A[i * L + k] * inv_d[k] * zk;
+      for (int i = k + 1 + lane; i < L; i += 32) b[i] -= A[i * lda + k] * inv_d[k] * zk;
       __syncwarp();
     }
     for (int k = lane; k < L; k += 32) b[k] *= inv_d[k];  // D y = z
@@ -646,13 +668,67 @@ __device__ int block_ldlt_solve(int L, double* A, double* b, double* x, const un
     for (int k = L - 1; k >= 0; --k) {  // backward: L^T x = y
       const double xk = b[k];
       __syncwarp();
-      for (int i = lane; i < k; i += 32) b[i] -= A[k * L + i] * inv_d[i] * xk;
+      for (int i = lane; i < k; i += 32) b[i] -= A[k * lda + i] * inv_d[i] * xk;
       if (lane == 0) x[k] = xk;
       __syncwarp();
     }
   }
   __syncthreads();
   return ok;
+}
+
+// One-warp LDL^T solve for L <= N <= 32 (N a compile-time padding, the
+// system is extended with an identity block), with the same factorisation
+// and failure rule as block_ldlt_solve: lane i holds row i in registers,
+// column k travels by shuffles (cheap on sm_100: ~9 cycles), the forward
+// substitution is fused into the elimination and the backward one reads the
+// unit-L factor written back to A (row stride lda). Returns 1 on success (x
+// written), 0 when a pivot is not strictly positive. Call from a full warp.
+template <int N>
+__device__ int warp_ldlt_solve(int L, int lda, double* A, const double* b, double* x) {
+  const int lane = threadIdx.x & 31;
+  const bool row = lane < L;
+  double a[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    a[j] = row ? (j < L ? A[lane * lda + j] : 0.0) : (j == lane ? 1.0 : 0.0);
+  }
+  double bi = row ? b[lane] : 0.0;
+  int ok = 1;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double dk = __shfl_sync(0xffffffffu, a[k], k);
+    ok &= dk > 0.0 ? 1 : 0;  // uniform; padded pivots are 1
+    const double inv = __drcp_rn(dk);
+    const double zk = __shfl_sync(0xffffffffu, bi, k);
+    const bool act = lane > k;
+    const double lik = a[k] * inv;
+#pragma unroll
+    for (int j = k + 1; j < N; ++j) {
+      const double cj = __shfl_sync(0xffffffffu, a[k], j);  // A[j][k], unscaled
+      if (act && j <= lane) a[j] -= lik * cj;
+    }
+    if (act) {
+      bi -= lik * zk;
+      a[k] = lik;
+    }
+  }
+  if (!ok) return 0;
+  double dd = 1.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    if (row && j < lane) A[lane * lda + j] = a[j];
+    if (j == lane) dd = a[j];
+  }
+  __syncwarp();
+  double yi = bi * __drcp_rn(dd);
+  for (int k = L - 1; k >= 0; --k) {
+    const double xk = __shfl_sync(0xffffffffu, yi, k);
+    if (lane < k) yi -= A[k * lda + lane] * xk;
+  }
+  if (row) x[lane] = yi;
+  __syncwarp();
+  return 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -678,105 +754,197 @@ struct PoseArgs {
 // W warps: offsets, dchain, per-warp row tiles [W][32][L|1], per-warp
 // residuals, per-warp entry partials [W][NE], pair tables, entry table.
 __host__ __device__ inline size_t pose_smem_bytes(int L, int NP, int warps) {
-  const int Lp = L | 1;
+  const int Lr = (L + 1) | 1;
   const int NE = L * (L + 1) / 2 + L;
-  return sizeof(double) * (8 * L + 8 * NP + warps * 32 * Lp + warps * 32 + warps * NE) +
-         sizeof(int) * (L + 1 + NP) + sizeof(unsigned short) * 2 * NE + 64;
+  return sizeof(double) * (8 * L + 8 * NP + warps * 32 * Lr + warps * NE) +
+         sizeof(int) * (L + 1 + NP) + sizeof(unsigned short) * 2 * NE + 64 +
+         (sizeof(double) + sizeof(int)) * warps * 64 + 16;
 }
 
-template <int Q>
+// Upper 4x4 tiles of the L x (L+1) block [JtJ | Jtr]: tile (bi, bj), bj >= bi.
+__host__ __device__ inline int pose_tiles(int L) {
+  const int nbr = (L + 3) >> 2, nbc = (L + 4) >> 2;
+  int n = 0;
+  for (int bi = 0; bi < nbr; ++bi) n += nbc - bi;
+  return n;
+}
+
+// TPL = 1: every lane owns one 4x4 tile of [JtJ | Jtr] (needs pose_tiles(L)
+// <= 32, i.e. L <= 27): per row 8 shared loads feed 16 FMAs. TPL = 0: lane-
+// owned entries e = lane + 32 q (Q of them), any L <= 64.
+template <int Q, int TPL>
 __global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
   extern __shared__ __align__(16) double psm[];
   const int L = m.L;
-  const int Lp = L | 1;
+  const int Lr = (L + 1) | 1;  // row stride: L Jacobian entries + the residual, odd
   const int NT = L * (L + 1) / 2;
   const int NE = NT + L;  // upper JtJ, then Jtr
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* s_off = psm;                       // 8L
   double* s_dch = s_off + 8 * L;             // 8NP
-  double* rows = s_dch + 8 * m.NP;           // nw * 32 * Lp
-  double* rres = rows + nw * 32 * Lp;        // nw * 32
-  double* part = rres + nw * 32;             // nw * NE (lane-owned entries)
+  double* rows = s_dch + 8 * m.NP;           // nw * 32 * Lr
+  long long* part = reinterpret_cast<long long*>(rows + nw * 32 * Lr);  // nw * NE
   int* s_poff = reinterpret_cast<int*>(part + nw * NE);  // L+1
   int* s_pth = s_poff + (L + 1);                          // NP
   unsigned short* ea = reinterpret_cast<unsigned short*>(s_pth + m.NP);
   unsigned short* eb = ea + NE;
+  double* qres = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(eb + NE) + 15) & ~static_cast<uintptr_t>(15));  // nw * 64
+  int* qidx = reinterpret_cast<int*>(qres + nw * 64);                             // nw * 64
 
   const long long t0 = clock64();
   if (a.dbg && threadIdx.x == 0) {
     unsigned long long g0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
-    a.dbg[8 + 3 * 296 + blockIdx.x] = static_cast<long long>(g0);
+    a.dbg[8 + 3 * 296 + (blockIdx.x % 296)] = static_cast<long long>(g0);
   }
-#pragma unroll 4
-  for (int k = threadIdx.x; k < 8 * L; k += blockDim.x) s_off[k] = s.offsets[k];
-#pragma unroll 8
-  for (int k = threadIdx.x; k < 8 * m.NP; k += blockDim.x) s_dch[k] = s.dchain[k];
-  for (int k = threadIdx.x; k <= L; k += blockDim.x) s_poff[k] = m.pair_off[k];
-#pragma unroll 4
-  for (int k = threadIdx.x; k < m.NP; k += blockDim.x) s_pth[k] = m.pair_theta[k];
-  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
-    if (e < NT) {  // row-major upper triangle
-      int r = 0, rem = e;
-      while (rem >= L - r) {
-        rem -= L - r;
-        ++r;
+  {
+    // stage offsets, dchain and pair tables: all loads of a thread first
+    constexpr int U = 4;
+    const int n_off = 8 * L, n_dch = 8 * m.NP;
+    for (int k0 = threadIdx.x; k0 < n_off + n_dch; k0 += U * blockDim.x) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * blockDim.x;
+        v[u] = k < n_off ? __ldg(s.offsets + k) : (k < n_off + n_dch ? __ldg(s.dchain + (k - n_off)) : 0.0);
       }
-      ea[e] = static_cast<unsigned short>(r);
-      eb[e] = static_cast<unsigned short>(r + rem);
-    } else {
-      ea[e] = static_cast<unsigned short>(e - NT);
-      eb[e] = 0xFFFF;  // pairs with the residual
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * blockDim.x;
+        if (k < n_off + n_dch) s_off[k] = v[u];  // s_dch follows s_off contiguously
+      }
     }
   }
-  for (int e = threadIdx.x; e < nw * NE; e += blockDim.x) part[e] = 0.0;
+  for (int k = threadIdx.x; k <= L; k += blockDim.x) s_poff[k] = __ldg(m.pair_off + k);
+  for (int k = threadIdx.x; k < m.NP; k += blockDim.x) s_pth[k] = __ldg(m.pair_theta + k);
+  if (TPL == 0) {
+    for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+      if (e < NT) {  // row-major upper triangle
+        int r = 0, rem = e;
+        while (rem >= L - r) {
+          rem -= L - r;
+          ++r;
+        }
+        ea[e] = static_cast<unsigned short>(r);
+        eb[e] = static_cast<unsigned short>(r + rem);
+      } else {
+        ea[e] = static_cast<unsigned short>(e - NT);
+        eb[e] = static_cast<unsigned short>(L);  // pairs with the residual (row[L])
+      }
+    }
+  }
+  // this lane's tile (TPL == 1)
+  int tbi = -1, tbj = -1;
+  if (TPL == 1) {
+    const int nbr = (L + 3) >> 2, nbc = (L + 4) >> 2;
+    int t = lane;
+    for (int bi = 0; bi < nbr; ++bi) {
+      if (t < nbc - bi) {
+        tbi = bi;
+        tbj = bi + t;
+        break;
+      }
+      t -= nbc - bi;
+    }
+  }
   __syncthreads();
 
-  // Warp-level accumulation: each warp takes 32 consecutive vertices, builds
-  // the rows of its associated ones (fill_row) in its own shared tile and
-  // adds their outer products to lane-owned entries -- no block barriers.
-  double rsum = 0.0;
-  long long nassoc = 0;
-  double* wrows = rows + warp * 32 * Lp;
-  double* wres = rres + warp * 32;
-  double* wpart = part + warp * NE;
-  const int gw = blockIdx.x * nw + warp, tw = gridDim.x * nw;
-  for (int base = gw * 32; base < m.V; base += tw * 32) {
-    const int i = base + lane;
-    double r = 0.0;
-    bool has_row = false;
-    if (i < m.V) {
-      long long cnt = 0;
+  // Warp g of TW owns vertices g, g + TW, g + 2 TW, ... (every warp gets the
+  // same count to within one, spread over the whole mesh, so no warp holds a
+  // region of expensive deep-chain vertices) and scans them 32 at a time,
+  // queueing the associated ones; full batches of 32 queued vertices build
+  // their rows (fill_row) in a warp-private shared tile, every lane busy, and
+  // the batch's outer products are accumulated in fp64 registers in
+  // ascending queue order, then added to 2^-40 fixed-point integers.
+  constexpr int NACC = TPL == 1 ? 16 : Q;
+  // fixed-point accumulators: the warp's NE entries in shared memory, each
+  // owned by exactly one lane (no atomics)
+  long long* wpart = part + warp * NE;
+  for (int e = lane; e < NE; e += 32) wpart[e] = 0;
+  int eidx[NACC];  // entry of each accumulator slot of this lane, -1 = none
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) {
+    int e = -1;
+    if (TPL == 1) {
+      const int ra = 4 * tbi + q / 4, cb = 4 * tbj + q % 4;
+      if (tbi >= 0 && ra < L && cb <= L && (cb == L || ra <= cb))
+        e = cb == L ? NT + ra : ra * L - ra * (ra - 1) / 2 + (cb - ra);
+    } else {
+      e = lane + 32 * q < NE ? lane + 32 * q : -1;
+    }
+    eidx[q] = e;
+  }
+  __syncwarp();
+  long long rsq = 0, nassoc = 0;  // sum r^2 (2^-44 fixed point), associated count
+  double* wrows = rows + warp * 32 * Lr;
+  const int TW = gridDim.x * nw, gw = blockIdx.x * nw + warp;
+  int* wq = qidx + warp * 64;       // warp-private queue of associated vertices
+  double* wqr = qres + warp * 64;   // ... and their residuals
+  int qn = 0;                       // warp-uniform queue length (< 32 between chunks)
+  for (int jb = 0;; jb += 32) {
+    const bool more = gw + TW * jb < m.V;
+    if (more) {
+      // scan 32 owned vertices: association and residual (association.cpp:132-136);
+      // the posed vertex and normal are fetched with the sums (one round trip)
+      const int i = gw + TW * (jb + lane);
       bool have = false;
-      const double4 v = s.pv[i];
-      const float4 n = s.pn[i];
-      if (a.count_in) {
-        cnt = a.count_in[i];
-        have = cnt > 0;
-        r = have ? a.res_in[i] : 0.0;
-      } else {
-        double pt[3];
-        have = observed_mean(s.acc, i, pt, &cnt);
-        if (have)
-          r = static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
-              static_cast<double>(n.z) * (pt[2] - v.z);
+      double r = 0.0;
+      if (i < m.V) {
+        if (a.count_in) {
+          have = a.count_in[i] > 0;
+          r = have ? a.res_in[i] : 0.0;
+        } else {
+          const ulonglong2 a01 = reinterpret_cast<const ulonglong2*>(s.acc)[2 * i];
+          const ulonglong2 a23 = reinterpret_cast<const ulonglong2*>(s.acc)[2 * i + 1];
+          const double4 v = s.pv[i];
+          const float4 n = s.pn[i];
+          const long long c = static_cast<long long>(a23.y);
+          have = c > 0;
+          if (have) {
+            const double inv = 1.0 / static_cast<double>(c);
+            const double px = unfix(a01.x, kFixPoint) * inv, py = unfix(a01.y, kFixPoint) * inv,
+                         pz = unfix(a23.x, kFixPoint) * inv;
+            r = static_cast<double>(n.x) * (px - v.x) + static_cast<double>(n.y) * (py - v.y) +
+                static_cast<double>(n.z) * (pz - v.z);
+          }
+        }
       }
       if (have) {
-        rsum += r * r;
+        rsq += fix(r * r, kFixRes);
         ++nassoc;
+      }
+      const unsigned hm = __ballot_sync(0xffffffffu, have);
+      if (have) {
+        const int pos = qn + __popc(hm & ((1u << lane) - 1u));
+        wq[pos] = i;
+        wqr[pos] = r;
+      }
+      qn += __popc(hm);
+      __syncwarp();
+    }
+    // rows of full batches (and of the remainder at the end), every lane busy
+    while (qn >= 32 || (!more && qn > 0)) {
+      const int nrows = qn < 32 ? qn : 32;
+      bool has_row = false;
+      if (lane < nrows) {
+        const int i = wq[lane];
+        const double r = wqr[lane];
+        const float4 n = s.pn[i];
         DQ raw;
         double sign[4];
         const double4 wv = m.wgt[i];
         const uchar4 lk = m.wlink[i];
+        const double4 a0 = m.v0[i];
+        const double4 f = phi[i];
         if (n.w != 0.0f && blend_vertex(s_off, wv, lk, raw, sign)) {
-          const double4 a0 = m.v0[i];
-          const double4 f = phi[i];
           const double rest[3] = {a0.x + f.x, a0.y + f.y, a0.z + f.z};
           const double nn[3] = {n.x, n.y, n.z};
           double r8[8];
           dq_point_plane_row(raw, rest, nn, r8);
-          double* row = wrows + lane * Lp;
+          double* row = wrows + lane * Lr;
           for (int k = 0; k < L; ++k) row[k] = 0.0;
+          row[L] = r;
           const unsigned char li[4] = {lk.x, lk.y, lk.z, lk.w};
           const double wi[4] = {wv.x, wv.y, wv.z, wv.w};
           for (int e = 0; e < 4; ++e) {
@@ -789,80 +957,157 @@ __global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, 
               row[s_pth[p]] += coeff * dot;
             }
           }
-          wres[lane] = r;
           has_row = true;
         }
       }
-    }
-    unsigned mask = __ballot_sync(0xffffffffu, has_row);
-    __syncwarp();
-    if (mask) {
-      // lane-owned entries e = lane + 32 q accumulate in registers over the
-      // batch's rows (ascending vertex order: deterministic)
-      double acc[Q];
+      unsigned mask = __ballot_sync(0xffffffffu, has_row);
+      __syncwarp();
+      if (mask) {
+        double acc[NACC];
 #pragma unroll
-      for (int q = 0; q < Q; ++q) acc[q] = 0.0;
-      while (mask) {
-        const int t = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const double* row = wrows + t * Lp;
-        const double rt = wres[t];
+        for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
+        if (TPL == 1) {
+          if (tbi >= 0) {
+            const int ca = 4 * tbi, cb = 4 * tbj;
+            while (mask) {
+              const int t = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const double* row = wrows + t * Lr;
+              double ra[4], rb[4];
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int e = lane + 32 * q;
-          if (e < NE) {
-            const int ca = ea[e], cb = eb[e];
-            acc[q] += row[ca] * (cb == 0xFFFF ? rt : row[cb]);
+              for (int u = 0; u < 4; ++u) {
+                ra[u] = row[min(ca + u, L)];  // clamped: in-bounds, discarded beyond L
+                rb[u] = row[min(cb + u, L)];
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[4 * u + v] += ra[u] * rb[v];
+            }
+          }
+        } else {
+          while (mask) {
+            const int t = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const double* row = wrows + t * Lr;
+#pragma unroll
+            for (int q = 0; q < NACC; ++q) {
+              const int e = lane + 32 * q;
+              if (e < NE) acc[q] += row[ea[e]] * row[eb[e]];
+            }
           }
         }
-      }
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const int e = lane + 32 * q;
-        if (e < NE) wpart[e] += acc[q];
+        for (int q = 0; q < NACC; ++q)
+          if (eidx[q] >= 0) wpart[eidx[q]] += fix(acc[q], kFixSys);
       }
+      // drop the processed rows from the queue
+      const int rest_n = qn - nrows;
+      int qi = 0;
+      double qr = 0.0;
+      if (lane < rest_n) {
+        qi = wq[nrows + lane];
+        qr = wqr[nrows + lane];
+      }
+      __syncwarp();
+      if (lane < rest_n) {
+        wq[lane] = qi;
+        wqr[lane] = qr;
+      }
+      qn = rest_n;
+      __syncwarp();
     }
-    __syncwarp();
+    if (!more) break;
   }
   const long long t1 = clock64();
-  unsigned long long g_main = 0, g_start = 0;
-  if (a.dbg) {
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_main));
+  unsigned long long g_main = 0;
+  if (a.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_main));
+  // per-CTA integer sums (exact), then fixed-point atomics spread over
+  // kRedCopies slot copies to avoid same-address serialisation
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    rsq += __shfl_xor_sync(0xffffffffu, rsq, o);
+    nassoc += __shfl_xor_sync(0xffffffffu, nassoc, o);
   }
-  block_sum2(rsum, nassoc);
+  __shared__ long long s_rsq[32], s_na[32];
+  if (lane == 0) {
+    s_rsq[warp] = rsq;
+    s_na[warp] = nassoc;
+  }
   __syncthreads();
-  // fixed-point atomics (associative, so the result is order independent),
-  // spread over kRedCopies slot copies to avoid same-address serialisation
   unsigned long long* red = s.red + (blockIdx.x % kRedCopies) * (NE + 2);
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
-    double acc = 0.0;
-    for (int w = 0; w < nw; ++w) acc += part[w * NE + e];  // fixed order
-    red_add(red + e, fix(acc, kFixSys));
+    long long sum = 0;
+    for (int w = 0; w < nw; ++w) sum += part[w * NE + e];
+    if (sum) red_add(red + e, sum);
   }
   if (threadIdx.x == 0) {
-    red_add(red + NE, fix(rsum, kFixRes));
-    red_add(red + NE + 1, nassoc);
+    long long r2 = 0, na = 0;
+    for (int w = 0; w < nw; ++w) {
+      r2 += s_rsq[w];
+      na += s_na[w];
+    }
+    if (r2) red_add(red + NE, r2);
+    if (na) red_add(red + NE + 1, na);
   }
   if (a.dbg && threadIdx.x == 0) {
     unsigned long long g_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
-    a.dbg[8 + 3 * blockIdx.x] = static_cast<long long>(g_main);
-    a.dbg[8 + 3 * blockIdx.x + 1] = static_cast<long long>(g_end);
-    a.dbg[8 + 3 * blockIdx.x + 2] = t1 - t0;
+    const int slot = blockIdx.x % 296;
+    a.dbg[8 + 3 * slot] = static_cast<long long>(g_main);
+    a.dbg[8 + 3 * slot + 1] = static_cast<long long>(g_end);
+    a.dbg[8 + 3 * slot + 2] = t1 - t0;
   }
-  if (!last_block(s.tickets + 1)) return;
-  const long long t2 = clock64();
+  if (a.dbg && threadIdx.x == 0 && blockIdx.x == 0) a.dbg[0] = t1 - t0;
+}
 
-  // ---- last CTA: assemble, prior, solve, update, stats, FK ---------------
-  double* A = rows;                  // L*L (nw*32*Lp >= L*L for L <= 64 with 4+ warps)
-  double* jtr = rres;                // L <= nw*32
-  double* jtj_d = part;              // diag of JtJ (L)
+// K7 (+K0): the pose-solve step, one CTA right after k_pose_system in the
+// same stream: fold the reduction copies into JtJ / Jtr, add the prior
+// (kinopt.cpp:113-117), damp and factor (solve_step, kinopt.cpp:121-130;
+// a failed factorisation skips the step, :166-168), theta -= x with the
+// optional clamp (:161-165), the iteration stats (:153-169) and FK / offsets
+// / dchain for the new theta (skeleton.cpp:56-108). A kernel of its own, so
+// the serial solve is not register-capped by the reduction kernel.
+__host__ __device__ inline size_t pose_solve_smem_bytes(int L) {
+  const int NE = L * (L + 1) / 2 + L;
+  return sizeof(double) * L * (L | 1) + sizeof(unsigned short) * 2 * NE + 16;
+}
+
+__global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevState s, PoseArgs a) {
+  __shared__ FkTables fkt;
+  extern __shared__ __align__(16) double solve_sm[];  // pose_solve_smem_bytes(L)
+  __shared__ double jtr[64];
   __shared__ double s_theta[64];
   __shared__ double s_x[64];
   __shared__ double s_rsum;
   __shared__ long long s_nassoc;
-  __shared__ int s_finite, s_ok;
+  __shared__ int s_finite;
+  const int L = m.L;
+  const int Lp = L | 1;
+  const int NT = L * (L + 1) / 2;
+  const int NE = NT + L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* A = solve_sm;                                                // L * Lp
+  unsigned short* ea = reinterpret_cast<unsigned short*>(A + L * Lp);  // NE
+  unsigned short* eb = ea + NE;
+  const long long t2 = clock64();
+  fk_stage(m, fkt);
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    int ca, cb;
+    if (e < NT) {
+      int r = 0, rem = e;
+      while (rem >= L - r) {
+        rem -= L - r;
+        ++r;
+      }
+      ca = r;
+      cb = r + rem;
+    } else {
+      ca = e - NT;
+      cb = 0xFFFF;
+    }
+    ea[e] = static_cast<unsigned short>(ca);
+    eb[e] = static_cast<unsigned short>(cb);
     unsigned long long sum = 0ull;
 #pragma unroll
     for (int c = 0; c < kRedCopies; ++c) {
@@ -870,12 +1115,11 @@ __global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, 
       s.red[c * (NE + 2) + e] = 0ull;
     }
     const double val = unfix(sum, kFixSys);
-    const int ca = ea[e], cb = eb[e];
     if (cb == 0xFFFF) {
       jtr[ca] = val;
     } else {
-      A[ca * L + cb] = val;
-      A[cb * L + ca] = val;
+      A[ca * Lp + cb] = val;
+      A[cb * Lp + ca] = val;
     }
   }
   if (threadIdx.x == 0) {
@@ -889,67 +1133,97 @@ __global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, 
     s_rsum = unfix(rs, kFixRes);
     s_nassoc = static_cast<long long>(na);
     s_finite = 1;
-    s_ok = 0;
   }
-  for (int k = threadIdx.x; k < L; k += blockDim.x) s_theta[k] = s.theta[k];
-  __syncthreads();
-  // default-pose prior (lambda_s S)^2 on the diagonal (kinopt.cpp:113-117)
   for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    const double p = a.lambda_s * m.s_diag[k];
-    A[k * L + k] += p * p;
+    s_theta[k] = s.theta[k];
+    s_x[k] = m.s_diag[k];  // staged S for the prior
+  }
+  __syncthreads();
+  // default-pose prior (lambda_s S)^2 on the diagonal (kinopt.cpp:113-117),
+  // then A = JtJ + lambda_k diag(JtJ) + floor I (kinopt.cpp:121-126)
+  for (int k = threadIdx.x; k < L; k += blockDim.x) {
+    const double p = a.lambda_s * s_x[k];
+    const double jd = A[k * Lp + k] + p * p;
     jtr[k] += p * p * s_theta[k];
+    A[k * Lp + k] = a.solve ? jd + a.lambda_k * jd + a.diag_floor : jd;
   }
   __syncthreads();
   if (!a.solve) {
-    for (int e = threadIdx.x; e < L * L; e += blockDim.x) s.sys_out[e] = A[e];
+    for (int e = threadIdx.x; e < L * L; e += blockDim.x) s.sys_out[e] = A[(e / L) * Lp + e % L];
     for (int k = threadIdx.x; k < L; k += blockDim.x) s.sys_out[L * L + k] = jtr[k];
     return;
   }
-  // A = JtJ + lambda_k diag(JtJ) + floor I
-  for (int k = threadIdx.x; k < L; k += blockDim.x) jtj_d[k] = A[k * L + k];
-  __syncthreads();
-  for (int k = threadIdx.x; k < L; k += blockDim.x)
-    A[k * L + k] = A[k * L + k] + a.lambda_k * jtj_d[k] + a.diag_floor;
-  __syncthreads();
   for (int e = threadIdx.x; e < L * L; e += blockDim.x)
-    if (!isfinite(A[e])) s_finite = 0;
+    if (!isfinite(A[(e / L) * Lp + e % L])) s_finite = 0;
   for (int k = threadIdx.x; k < L; k += blockDim.x)
     if (!isfinite(jtr[k])) s_finite = 0;
   __syncthreads();
   const long long t3 = clock64();
-  {
-    const int ok = s_finite ? block_ldlt_solve(L, A, jtr, s_x, ea, eb, NT) : 0;
-    if (threadIdx.x == 0) s_ok = ok;
-  }
-  __syncthreads();
-  const long long t4 = clock64();
-  if (threadIdx.x == 0) {
-    const int ok = s_ok;
-    double nrm = 0.0;
-    if (ok) {
-      for (int k = 0; k < L; ++k) {
-        double t = s_theta[k] - s_x[k];
+  if (L <= 32) {
+    if (warp == 0) {
+      int ok = 0;
+      if (s_finite) {
+        if (L <= 8) ok = warp_ldlt_solve<8>(L, Lp, A, jtr, s_x);
+        else if (L <= 16) ok = warp_ldlt_solve<16>(L, Lp, A, jtr, s_x);
+        else if (L <= 20) ok = warp_ldlt_solve<20>(L, Lp, A, jtr, s_x);
+        else if (L <= 24) ok = warp_ldlt_solve<24>(L, Lp, A, jtr, s_x);
+        else ok = warp_ldlt_solve<32>(L, Lp, A, jtr, s_x);
+      }
+      // theta -= x (kinopt.cpp:161-165), optional clamp, iteration stats
+      double xk = 0.0;
+      if (ok && lane < L) {
+        xk = s_x[lane];
+        double t = s_theta[lane] - xk;
         if (a.clamp && a.limit > 0.0) t = fmin(fmax(t, -a.limit), a.limit);
-        s_theta[k] = t;
-        nrm += s_x[k] * s_x[k];
+        s_theta[lane] = t;
+      }
+      double nrm = xk * xk;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+      if (lane == 0) {
+        KinStat st;
+        st.residual_sum = s_rsum;
+        st.associated = static_cast<int>(s_nassoc);
+        st.step_norm = ok ? sqrt(nrm) : 0.0;
+        st.skipped = ok ? 0 : 1;
+        s.kin_stats[a.iteration] = st;
       }
     }
-    KinStat st;
-    st.residual_sum = s_rsum;
-    st.associated = static_cast<int>(s_nassoc);
-    st.step_norm = ok ? sqrt(nrm) : 0.0;
-    st.skipped = ok ? 0 : 1;
-    s.kin_stats[a.iteration] = st;
+    __syncthreads();
+  } else {
+    // general L (<= 64): block LDL^T over the (ea, eb) table
+    const int ok = s_finite ? block_ldlt_solve(L, Lp, A, jtr, s_x, ea, eb, NT) : 0;
+    if (threadIdx.x == 0) {
+      double nrm = 0.0;
+      if (ok) {
+        for (int k = 0; k < L; ++k) {
+          double t = s_theta[k] - s_x[k];
+          if (a.clamp && a.limit > 0.0) t = fmin(fmax(t, -a.limit), a.limit);
+          s_theta[k] = t;
+          nrm += s_x[k] * s_x[k];
+        }
+      }
+      KinStat st;
+      st.residual_sum = s_rsum;
+      st.associated = static_cast<int>(s_nassoc);
+      st.step_norm = ok ? sqrt(nrm) : 0.0;
+      st.skipped = ok ? 0 : 1;
+      s.kin_stats[a.iteration] = st;
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  const long long t4 = clock64();
   for (int k = threadIdx.x; k < L; k += blockDim.x) s.theta[k] = s_theta[k];
-  block_fk(m, s, s_theta);
+  __shared__ long long fk_st[2];
+  fk_run(m, s, s_theta, fkt, a.dbg ? fk_st : nullptr);
+  if (a.dbg) __syncthreads();
   if (a.dbg && threadIdx.x == 0) {
-    a.dbg[0] = t1 - t0;
-    a.dbg[1] = t2 - t1;
+    a.dbg[1] = 0;
     a.dbg[2] = t3 - t2;
     a.dbg[3] = t4 - t3;
     a.dbg[4] = clock64() - t4;
+    a.dbg[5] = fk_st[0] - t4;        // sincos + local transforms
+    a.dbg[6] = fk_st[1] - fk_st[0];  // level chain
   }
 }
 
@@ -1169,7 +1443,7 @@ __global__ void k_solve_step(int n, const double* jtj, const double* jtr, double
   for (int k = threadIdx.x; k < n; k += blockDim.x)
     if (!isfinite(b[k])) fin = 0;
   __syncthreads();
-  const int ok = fin ? block_ldlt_solve(n, A, b, x, ea, eb, NT) : 0;
+  const int ok = fin ? block_ldlt_solve(n, n, A, b, x, ea, eb, NT) : 0;
   for (int k = threadIdx.x; k < n; k += blockDim.x) out[k] = ok ? x[k] : 0.0;
   if (threadIdx.x == 0) out[n] = ok ? 1.0 : 0.0;
 }

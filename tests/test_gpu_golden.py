@@ -214,3 +214,37 @@ def test_errors_surface():
     rc = lib.wt_gpu_track_loaded(t._ctx, None, None)
     assert rc == W.WT_EINVAL
     t.close()
+
+
+@pytest.mark.parametrize("links", [6, 27, 28, 40])
+def test_long_chains_against_oracle(links):
+    """Both JtJ accumulation layouts (4x4 lane tiles up to 27 links, lane-
+    owned entries beyond) and both solvers (one-warp LDL^T up to 32 links,
+    block LDL^T beyond): normal system and two pose iterations on a cloud vs
+    the C oracle."""
+    from . import rigs
+    rng = np.random.default_rng(links)
+    b, pose = rigs.random_rig(rng, links, 400)
+    intr = Intrinsics(40.0, 40.0, 80.0, 60.0, 160, 120)  # wide view: the rig spans x in [-2, 2]
+    g = Tracker(b, intr, pose)
+    o = c_oracle.OracleTracker(b, intr.c(), pose)
+    V = b.vertex_count
+    count = (rng.random(V) < 0.5).astype(np.int32)
+    res = rng.uniform(-0.01, 0.01, V) * count
+    jtj, jtr = g.normal_system(pose, KinSolverConfig(), count, res)
+    ojtj, ojtr = o.normal_system(pose, KinSolverConfig().c(), count, res)
+    # rows use the fp32-stored normals: 2^-24 relative per entry
+    assert np.abs(jtj - ojtj).max() <= 1e-6 * np.abs(ojtj).max()
+    assert np.abs(jtr - ojtr).max() <= 1e-6 * np.abs(ojtr).max()
+    # a cloud of the posed vertices nudged along z, one point per pixel
+    v, n, valid = g.skin(pose)
+    pts, pv = rigs.frame_from_points(intr, v[valid.astype(bool)] + [0.0, 0.0, 0.004])
+    g.load_cloud(pts, pv)
+    o.load_cloud(pts, pv)
+    kin = KinSolverConfig(iterations=2)
+    sg = g.optimize_pose(kin)
+    so = o.optimize_pose(kin.c(), AssocConfig().c())
+    assert [s.associated for s in sg] == [s.associated for s in so]
+    assert sg[0].associated > 20
+    assert np.abs(g.get_state()[0] - o.get_state()[0]).max() <= 1e-6
+    g.close()

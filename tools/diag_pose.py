@@ -13,7 +13,7 @@ for f in range(1, 5):
     d, _ = trk.render_depth(trajectory(bundle, f, 0), frame=f)
     trk.track_frame(cfg, depth=d)
     L.wt_gpu_debug_pose(trk._ctx, buf.ctypes.data)
-    print("frame", f, "main", buf[0], "atomics+wait", buf[1], "assemble", buf[2], "cholesky", buf[3], "update+fk", buf[4])
+    print("frame", f, "main", buf[0], "atomics+wait", buf[1], "assemble", buf[2], "cholesky", buf[3], "update+fk", buf[4], "(fk: local", buf[5], "levels", buf[6], ")")
 
 rec = buf[8:8 + 3 * 296].reshape(296, 3)
 st = buf[8 + 3 * 296: 8 + 4 * 296]
