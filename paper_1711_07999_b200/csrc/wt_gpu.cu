@@ -145,6 +145,7 @@ struct wt_gpu_ctx {
   int* hook_cnt = nullptr;
   double* hook_res = nullptr;
   long long* pose_dbg = nullptr;  // WT_DEBUG_POSE: last-CTA timing of the pose kernel
+  long long* search_dbg = nullptr;  // WT_DEBUG_SEARCH: per-CTA timing of the search kernel
 
   // profiling: when set during capture, an event is recorded after every
   // kernel so per-kernel device time inside the real frame graph is known
@@ -364,8 +365,16 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   sa.cut2 = a->cutoff * a->cutoff;
   sa.write_winners = winners ? 1 : 0;
   sa.winners = winners;
-  const int grid = std::max(1, std::min(vgrid(c->P), 4 * 148));
-  wt::k_search<<<grid, wt::kVThreads, 0, c->stream>>>(s, f, sa);
+  sa.dbg = c->search_dbg;
+  {
+    const char* ex = getenv("WT_SEARCH_EXPERIMENT");  // diagnostics only
+    const int bits = ex ? atoi(ex) : 0;
+    sa.no_acc = bits & 1;
+    sa.exp = bits;
+  }
+  // one wave of 128-thread CTAs (3 per SM fit the staged boxes); warps stride over the runs
+  const int grid = std::max(1, std::min((c->P + 127) / 128, 3 * 148));
+  wt::k_search<<<grid, wt::kSearchWarps * 32, wt::search_smem_bytes(), c->stream>>>(s, f, sa);
   mark(c, K_SEARCH);
 }
 
@@ -762,13 +771,17 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     c->d_depth = c->mem.alloc<float>(c->P);
     c->d_valid = c->mem.alloc<uint8_t>(c->P);
     c->d_pts_hi = c->mem.alloc<double>(3 * static_cast<size_t>(c->P));
-    c->d_vlist = c->mem.alloc<int>(c->P);
+    // valid-pixel list: one run of 32 entries per 32-column row segment
+    c->d_vlist = c->mem.alloc<int>(32 * c->din.H * ((c->din.W + 31) / 32));
     c->d_nvalid = c->mem.alloc<int>(1);
     c->d_winners = c->mem.alloc<int>(c->P);
     ensure_stats(c, 16, 8);
     if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8 + 4 * 296 + 8);
+    if (getenv("WT_DEBUG_SEARCH")) c->search_dbg = c->mem.alloc<long long>(8 * 4096);
     if (wt::pose_smem_bytes(L, c->NP, pose_threads(c) / 32) > 227 * 1024)
       fail(WT_EINVAL, "skeleton too large for the pose kernel's shared memory");
+    WT_CUDA(cudaFuncSetAttribute(wt::k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(wt::search_smem_bytes())));
     if (wt::pose_tiles(L) <= 32) {
       pose_attr<1, 1>(c);
     } else {
@@ -837,8 +850,9 @@ int wt_gpu_get_state(wt_gpu_ctx* c, double* theta, double* phi, int32_t* frame_i
 static void ingest(wt_gpu_ctx* c, const float* depth_dev, double scale, const double* cloud_dev,
                    const uint8_t* valid_dev) {
   WT_CUDA(cudaMemsetAsync(c->d_nvalid, 0, sizeof(int), c->stream));
-  wt::k_ingest<<<vgrid(c->P), wt::kVThreads, 0, c->stream>>>(c->din, depth_dev, scale, cloud_dev, valid_dev,
-                                                              c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid);
+  const int segs = (c->din.W + wt::kIngestSeg - 1) / wt::kIngestSeg;
+  wt::k_ingest<<<segs * c->din.H, wt::kIngestSeg, 0, c->stream>>>(c->din, depth_dev, scale, cloud_dev, valid_dev,
+                                                                   c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid);
   check_launch();
 }
 
@@ -928,6 +942,14 @@ void enq_track(wt_gpu_ctx* c, const wt_track_config* cfg, bool shape_now) {
 }  // namespace
 
 void* wt_gpu_stream(wt_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+// Debug: per-CTA timing of the last search launch (needs WT_DEBUG_SEARCH at create).
+int wt_gpu_debug_search(wt_gpu_ctx* c, long long* out) {
+  if (!c || !c->search_dbg) return 0;
+  cudaMemcpy(out, c->search_dbg, sizeof(long long) * 8 * 4096, cudaMemcpyDeviceToHost);
+  cudaMemset(c->search_dbg, 0, sizeof(long long) * 8 * 4096);
+  return 1;
+}
 
 // Debug: last pose kernel's last-CTA timing (needs WT_DEBUG_POSE at create).
 int wt_gpu_debug_pose(wt_gpu_ctx* c, long long* out) {
