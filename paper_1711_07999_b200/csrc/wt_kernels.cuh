@@ -391,20 +391,21 @@ __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, D
     if (compute) {
       double ax = 0, ay = 0, az = 0;
       const int r0 = m.ring_off[i], r1 = m.ring_off[i + 1];
-      for (int r = r0; r < r1; r += 4) {
-        // four incident triangles per step: index loads, then all eight
-        // position gathers in flight, then the cross products in CSR order
-        int2 bc[4];
+      for (int r = r0; r < r1; r += 8) {
+        // eight incident triangles per step (most vertices have <= 8): index
+        // loads, then all sixteen position gathers in flight, then the cross
+        // products in CSR order
+        int2 bc[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(i, i);
-        double4 pb[4], pc[4];
+        for (int q = 0; q < 8; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(i, i);
+        double4 pb[8], pc[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
           pb[q] = s.pv[bc[q].x];
           pc[q] = s.pv[bc[q].y];
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
           if (r + q >= r1) break;
           const double ex = pb[q].x - vx, ey = pb[q].y - vy, ez = pb[q].z - vz;
           const double fx = pc[q].x - vx, fy = pc[q].y - vy, fz = pc[q].z - vz;
