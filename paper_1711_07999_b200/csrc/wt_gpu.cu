@@ -372,9 +372,9 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
     sa.no_acc = bits & 1;
     sa.exp = bits;
   }
-  // one wave of 128-thread CTAs (3 per SM fit the staged boxes); warps stride over the runs
-  const int grid = std::max(1, std::min((c->P + 127) / 128, 3 * 148));
-  wt::k_search<<<grid, wt::kSearchWarps * 32, wt::search_smem_bytes(), c->stream>>>(s, f, sa);
+  // 8 lanes per valid pixel; at most P pixels (the list is padded per 32 columns)
+  const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, 16 * 148));
+  wt::k_search<<<grid, wt::kVThreads, 0, c->stream>>>(s, f, sa);
   mark(c, K_SEARCH);
 }
 
@@ -777,11 +777,9 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     c->d_winners = c->mem.alloc<int>(c->P);
     ensure_stats(c, 16, 8);
     if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8 + 4 * 296 + 8);
-    if (getenv("WT_DEBUG_SEARCH")) c->search_dbg = c->mem.alloc<long long>(8 * 4096);
+    if (getenv("WT_DEBUG_SEARCH")) c->search_dbg = c->mem.alloc<long long>(8 * 4096);  // unused by the current kernel
     if (wt::pose_smem_bytes(L, c->NP, pose_threads(c) / 32) > 227 * 1024)
       fail(WT_EINVAL, "skeleton too large for the pose kernel's shared memory");
-    WT_CUDA(cudaFuncSetAttribute(wt::k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(wt::search_smem_bytes())));
     if (wt::pose_tiles(L) <= 32) {
       pose_attr<1, 1>(c);
     } else {

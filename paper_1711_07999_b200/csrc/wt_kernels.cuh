@@ -589,30 +589,6 @@ __device__ __forceinline__ void scan_span(const DevState& s, int e0, int e1, dou
   if (best_i >= 0) best_x = __longlong_as_double(bk);
 }
 
-// staged items as structure of arrays: consecutive items, consecutive banks
-struct BoxItems {
-  double* x;
-  double* y;
-  double* z;
-  int* idx;
-};
-
-__device__ __forceinline__ void scan_items_smem(const BoxItems& it, int e0, int e1, double px, double py, double pz,
-                                                double cut2, double& best_x, int& best_i) {
-  const long long ck = d2_key(cut2);
-  long long bk = best_i < 0 ? LLONG_MAX : d2_key(best_x);
-#pragma unroll 2
-  for (int e = e0; e < e1; ++e) {
-    const long long xk = d2_key(exact_d2(make_double4(it.x[e], it.y[e], it.z[e], 0.0), px, py, pz));
-    const int vi = it.idx[e];
-    if (xk <= ck && (xk < bk || (xk == bk && vi < best_i))) {
-      bk = xk;
-      best_i = vi;
-    }
-  }
-  if (best_i >= 0) best_x = __longlong_as_double(bk);
-}
-
 // Per-pixel result: the winner map entry and the scatter-average sums.
 __device__ __forceinline__ void search_emit(const DevState& s, const SearchArgs& a, int pix, int best_i, double px,
                                             double py, double pz) {
@@ -626,62 +602,22 @@ __device__ __forceinline__ void search_emit(const DevState& s, const SearchArgs&
   }
 }
 
-// Two phases so that no pixel's search is a long serial chain of L2 round
-// trips. (1) A warp takes 32 valid pixels (mostly neighbours in one image
-// row), stages the bucket items of the union of their (2K1+1)^2 cores -- a
-// small box of image rows, each one contiguous span of the row-major CSR --
-// into its shared-memory slice with coalesced loads, and every lane scans its
-// core there. A pixel is finished when the exact ring bound lb(K1+1) already
-// exceeds its best (or the cutoff). (2) Open pixels are queued and taken one
-// per warp: with the phase-1 best the outermost ring K* that could still
-// hold a winner or a tie is fixed up front, the lanes scan the rows of the
-// (2K*+1)^2 box outside the core in parallel, and the lexicographic (d^2,
-// index) minimum is reduced with shuffles. Boxes too large to stage fall
-// back to per-lane global scans of the core.
+// k_search: a group of 8 lanes per valid pixel (4 pixels per warp, taken
+// from the image-ordered 32-column runs of the valid-pixel list, so a warp's
+// pixels are row neighbours and share cache lines). Phase 1: lane r of the
+// group scans row r of the pixel's (2 K1 + 1)^2 core (K1 = 2) -- one span of
+// the row-major bucket CSR each, all rows in parallel -- and the group
+// reduces the lexicographic (d^2, index) minimum with shuffles. The pixel is
+// finished when the exact ring bound lb(K1 + 1) exceeds that best (or the
+// cutoff). Phase 2 (rare): the outermost ring K* that can still hold a winner
+// or a tie is fixed from the phase-1 best, and the group's lanes scan the
+// rows of the (2K*+1)^2 box outside the core, 8 rows at a time.
 constexpr int kNearRings = 2;
-constexpr int kSearchWarps = 4;
-constexpr int kBoxOffs = 256;   // staged box offsets per warp (ints): 5 rows x 37
-constexpr int kBoxItems = 448;  // staged items per warp (x, y, z, index as separate arrays)
+constexpr int kSearchGroup = 8;
 
-__host__ __device__ inline size_t search_smem_bytes() {
-  return kSearchWarps * (kBoxItems * (3 * sizeof(double) + sizeof(int)) + kBoxOffs * sizeof(int));
-}
-
-// Phase 2 of one queued pixel by the whole warp (see k_search).
-__device__ __forceinline__ void search_outer(const DevState& s, const DevFrame& f, const SearchArgs& a, int K1,
-                                             int qp, double b1, int bi1, double ifx, double ify) {
-  const int lane = threadIdx.x & 31;
-  const int w = a.window;
-  const int qu = qp % a.W, qv = qp / a.W;
-  const double qx = f.pts_hi[3 * qp], qy = f.pts_hi[3 * qp + 1], qz = f.pts_hi[3 * qp + 2];
-  const double atx = fabs((qu - a.cx) * ifx), aty = fabs((qv - a.cy) * ify);
-  // K*: the outermost ring not excluded by the phase-1 best
-  int ks = w;
-  if (a.prune) {
-    ks = K1;
-    for (int k = K1 + 1; k <= w; ++k) {
-      const double lb = ring_lb2(k, atx, aty, ifx, ify, qz);
-      if (lb > a.cut2 || lb > b1) break;
-      ks = k;
-    }
-  }
-  double bx = INFINITY;
-  int bi = -1;
-  for (int dr = lane - ks; dr <= ks; dr += 32) {
-    const int rr = qv + dr;
-    if (rr < 0 || rr >= a.H) continue;
-    const int r = rr * a.W;
-    const int c0 = max(qu - ks, 0), c1 = min(qu + ks, a.W - 1);
-    if (dr >= -K1 && dr <= K1) {  // the core columns were scanned in phase 1
-      const int l1 = min(qu - K1 - 1, c1), r0 = max(qu + K1 + 1, c0);
-      if (l1 >= c0) scan_span(s, s.poff[r + c0], s.poff[r + l1 + 1], qx, qy, qz, a.cut2, bx, bi);
-      if (r0 <= c1) scan_span(s, s.poff[r + r0], s.poff[r + c1 + 1], qx, qy, qz, a.cut2, bx, bi);
-    } else {
-      scan_span(s, s.poff[r + c0], s.poff[r + c1 + 1], qx, qy, qz, a.cut2, bx, bi);
-    }
-  }
+__device__ __forceinline__ void group_min(double& bx, int& bi) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = kSearchGroup / 2; o > 0; o >>= 1) {
     const double ox = __shfl_xor_sync(0xffffffffu, bx, o);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (oi >= 0 && (bi < 0 || ox < bx || (ox == bx && oi < bi))) {
@@ -689,32 +625,19 @@ __device__ __forceinline__ void search_outer(const DevState& s, const DevFrame& 
       bi = oi;
     }
   }
-  if (lane == 0) {
-    int best = bi1;
-    if (bi >= 0 && (best < 0 || bx < b1 || (bx == b1 && bi < best))) best = bi;
-    search_emit(s, a, qp, best, qx, qy, qz);
-  }
 }
 
-__global__ void __launch_bounds__(kSearchWarps * 32) k_search(DevState s, DevFrame f, SearchArgs a) {
-  extern __shared__ __align__(16) unsigned char ssm[];
+__global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
   const int nv = *f.n_valid;
   const int w = a.window;
   const int K1 = min(kNearRings, w);
   const double ifx = 1.0 / a.fx, ify = 1.0 / a.fy;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* sx = reinterpret_cast<double*>(ssm) + warp * 3 * kBoxItems;
-  const BoxItems sit{sx, sx + kBoxItems, sx + 2 * kBoxItems,
-                     reinterpret_cast<int*>(reinterpret_cast<double*>(ssm) + kSearchWarps * 3 * kBoxItems) +
-                         warp * kBoxItems};
-  int* sbp = reinterpret_cast<int*>(reinterpret_cast<double*>(ssm) + kSearchWarps * 3 * kBoxItems) +
-             kSearchWarps * kBoxItems + warp * kBoxOffs;
-  // warps are independent: warp g takes the list runs g, g + TW, ... (32 pixels each)
-  const int TW = gridDim.x * kSearchWarps;
-  const int gwarp = blockIdx.x * kSearchWarps + warp;
-  for (int base = gwarp * 32; base < nv; base += TW * 32) {
-    long long c0s = clock64();
-    const int j = base + lane;
+  const int lane = threadIdx.x & 31, sub = lane & (kSearchGroup - 1);
+  constexpr int PPW = 32 / kSearchGroup;  // pixels per warp
+  const int TW = gridDim.x * (blockDim.x >> 5);
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (int base = gw * PPW; base < nv; base += TW * PPW) {
+    const int j = base + lane / kSearchGroup;
     const int pix = j < nv ? f.vlist[j] : -1;
     const bool act = pix >= 0;
     const int pu = pix % a.W, pv = pix / a.W;
@@ -724,95 +647,17 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(DevState s, DevFra
       py = f.pts_hi[3 * pix + 1];
       pz = f.pts_hi[3 * pix + 2];
     }
-    // union box of the warp's cores (the run is one row segment)
-    const unsigned am = __ballot_sync(0xffffffffu, act);
-    if (!am) continue;
-    const int bx0 = max(static_cast<int>(__reduce_min_sync(0xffffffffu, act ? pu : 0x7fffffff)) - K1, 0);
-    const int bx1 = min(static_cast<int>(__reduce_max_sync(0xffffffffu, act ? pu : -1)) + K1, a.W - 1);
-    const int by0 = max(static_cast<int>(__reduce_min_sync(0xffffffffu, act ? pv : 0x7fffffff)) - K1, 0);
-    const int by1 = min(static_cast<int>(__reduce_max_sync(0xffffffffu, act ? pv : -1)) + K1, a.H - 1);
-    const int nrow = by1 - by0 + 1, pw = bx1 - bx0 + 2;  // pw offsets per box row (incl. end)
-    bool staged = nrow * pw <= kBoxOffs;
-    int total = 0;
-    if (staged) {
-      constexpr int U = 8;  // all of a lane's offset loads in flight at once
-      const int n = nrow * pw;
-      for (int e0 = lane; e0 < n; e0 += 32 * U) {
-        int v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = min(e0 + 32 * u, n - 1);
-          const int r = e / pw;
-          v[u] = __ldg(s.poff + (by0 + r) * a.W + bx0 + (e - r * pw));
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (e0 + 32 * u < n) sbp[e0 + 32 * u] = v[u];
-      }
-      __syncwarp();
-      total = sbp[(nrow - 1) * pw + pw - 1] - sbp[0];  // rows are consecutive in the CSR
-      if (nrow > 1) {  // not contiguous unless the box spans whole rows: sum the spans
-        total = 0;
-        for (int r = 0; r < nrow; ++r) total += sbp[r * pw + pw - 1] - sbp[r * pw];
-      }
-      staged = total <= kBoxItems;
-    }
-    if (staged) {
-      // copy the box rows' items, flattened over the rows, 4 loads in flight per lane
-      constexpr int U = 4;
-      for (int e0 = lane; e0 < total; e0 += 32 * U) {
-        double4 v[U];
-        int dsti[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = e0 + 32 * u;
-          int r = 0, acc = 0;
-          dsti[u] = -1;
-          if (e < total) {
-            for (;; ++r) {  // row of flat index e (nrow is small)
-              const int n = sbp[r * pw + pw - 1] - sbp[r * pw];
-              if (e < acc + n) break;
-              acc += n;
-            }
-            dsti[u] = e;
-            v[u] = s.items[sbp[r * pw] + (e - acc)];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (dsti[u] >= 0) {
-            sit.x[dsti[u]] = v[u].x;
-            sit.y[dsti[u]] = v[u].y;
-            sit.z[dsti[u]] = v[u].z;
-            sit.idx[dsti[u]] = static_cast<int>(__double_as_longlong(v[u].w));
-          }
-      }
-      __syncwarp();
-    }
-    long long c1s = clock64();
     double best_x = INFINITY;
     int best_i = -1;
-    if (act && !(a.exp & 4)) {
-      const int c0 = max(pu - K1, 0), c1 = min(pu + K1, a.W - 1);
-      if (staged) {
-        int dst = 0;
-        for (int r = 0; r < nrow; ++r) {
-          const int rr = by0 + r;
-          const int* br = sbp + r * pw;
-          if (rr >= pv - K1 && rr <= pv + K1) {
-            const int e0 = br[c0 - bx0] - br[0] + dst, e1 = br[c1 + 1 - bx0] - br[0] + dst;
-            scan_items_smem(sit, e0, e1, px, py, pz, a.cut2, best_x, best_i);
-          }
-          dst += br[pw - 1] - br[0];
-        }
-      } else {
-        for (int rr = max(pv - K1, 0); rr <= min(pv + K1, a.H - 1); ++rr) {
-          const int r = rr * a.W;
-          scan_span(s, s.poff[r + c0], s.poff[r + c1 + 1], px, py, pz, a.cut2, best_x, best_i);
-        }
+    if (act && sub <= 2 * K1) {
+      const int rr = pv - K1 + sub;
+      if (rr >= 0 && rr < a.H) {
+        const int r = rr * a.W;
+        const int c0 = max(pu - K1, 0), c1 = min(pu + K1, a.W - 1);
+        scan_span(s, __ldg(s.poff + r + c0), __ldg(s.poff + r + c1 + 1), px, py, pz, a.cut2, best_x, best_i);
       }
     }
-    long long c2s = clock64();
+    group_min(best_x, best_i);
     bool open = false;
     if (act) {
       bool done = K1 == w;
@@ -821,35 +666,44 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(DevState s, DevFra
         const double lb = ring_lb2(K1 + 1, atx, aty, ifx, ify, pz);
         done = lb > a.cut2 || lb > best_x;  // no vertex outside the core can win or tie
       }
-      if (done) search_emit(s, a, pix, best_i, px, py, pz);
       open = !done;
     }
-    __syncwarp();
-    long long c3s = clock64();
-    // phase 2: the warp's open pixels, one at a time, all lanes
-    unsigned om = __ballot_sync(0xffffffffu, open);
-    const int nopen = __popc(om);
-    if (a.exp & 2) om = 0;
-    while (om) {
-      const int t = __ffs(om) - 1;
-      om &= om - 1;
-      const int qp = __shfl_sync(0xffffffffu, pix, t);
-      const double b1 = __shfl_sync(0xffffffffu, best_x, t);
-      const int bi1 = __shfl_sync(0xffffffffu, best_i, t);
-      search_outer(s, f, a, K1, qp, b1, bi1, ifx, ify);
+    if (__any_sync(0xffffffffu, open)) {
+      // phase 2 for the open pixels of this warp (groups work independently)
+      double bx = INFINITY;
+      int bi = -1;
+      if (open) {
+        const double atx = fabs((pu - a.cx) * ifx), aty = fabs((pv - a.cy) * ify);
+        int ks = w;
+        if (a.prune) {
+          ks = K1;
+          for (int k = K1 + 1; k <= w; ++k) {
+            const double lb = ring_lb2(k, atx, aty, ifx, ify, pz);
+            if (lb > a.cut2 || lb > best_x) break;
+            ks = k;
+          }
+        }
+        const int c0 = max(pu - ks, 0), c1 = min(pu + ks, a.W - 1);
+        for (int dr = sub - ks; dr <= ks; dr += kSearchGroup) {
+          const int rr = pv + dr;
+          if (rr < 0 || rr >= a.H) continue;
+          const int r = rr * a.W;
+          if (dr >= -K1 && dr <= K1) {  // the core columns were scanned in phase 1
+            const int l1 = min(pu - K1 - 1, c1), r0 = max(pu + K1 + 1, c0);
+            if (l1 >= c0) scan_span(s, s.poff[r + c0], s.poff[r + l1 + 1], px, py, pz, a.cut2, bx, bi);
+            if (r0 <= c1) scan_span(s, s.poff[r + r0], s.poff[r + c1 + 1], px, py, pz, a.cut2, bx, bi);
+          } else {
+            scan_span(s, s.poff[r + c0], s.poff[r + c1 + 1], px, py, pz, a.cut2, bx, bi);
+          }
+        }
+      }
+      group_min(bx, bi);
+      if (open && bi >= 0 && (best_i < 0 || bx < best_x || (bx == best_x && bi < best_i))) {
+        best_x = bx;
+        best_i = bi;
+      }
     }
-    __syncwarp();
-    if (a.dbg && lane == 0 && gwarp < 4096) {
-      long long* d = a.dbg + 8 * gwarp;
-      d[0] = c1s - c0s;          // list, points, box offsets, item staging
-      d[1] = c2s - c1s;          // core scan
-      d[2] = c3s - c2s;          // bound check + emit
-      d[3] = clock64() - c3s;    // phase 2
-      d[4] = nopen;
-      d[5] = staged ? total : -1;
-      d[6] = __popc(am);
-      d[7] = 1;
-    }
+    if (act && sub == 0) search_emit(s, a, pix, best_i, px, py, pz);
   }
 }
 
