@@ -384,11 +384,13 @@ void enq_associate(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* 
   enq_search(c, s, a, winners);
 }
 
-int pose_threads(const wt_gpu_ctx* c) { return c->L <= 40 ? 256 : 128; }
+// 128-thread CTAs, four resident per SM (registers): one wave of 592 CTAs,
+// ~22 vertices per warp at C3 (one scan chunk each)
+int pose_threads(const wt_gpu_ctx*) { return 128; }
 
 int pose_grid(const wt_gpu_ctx* c) {
   const int warps = pose_threads(c) / 32;
-  return std::max(1, std::min((c->V + 32 * warps - 1) / (32 * warps), 2 * 148));
+  return std::max(1, std::min((c->V + 32 * warps - 1) / (32 * warps), 4 * 148));
 }
 
 // JtJ entries per lane (upper triangle + Jtr) held in registers

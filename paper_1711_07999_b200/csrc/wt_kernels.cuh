@@ -480,7 +480,20 @@ __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, int H) 
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= H) return;
   int base = 0;
-  for (int k = lane; k < row; k += 32) base += __ldcg(s.row_cnt + k);
+  {
+    // sum of the preceding rows' counts: 16 loads in flight per lane
+    constexpr int U = 16;
+    for (int k0 = lane; k0 < row; k0 += 32 * U) {
+      int v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + 32 * u;
+        v[u] = k < row ? __ldcg(s.row_cnt + k) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) base += v[u];
+    }
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
   int* cnt = s.pix_cnt + row * W;
@@ -872,7 +885,7 @@ __host__ __device__ inline int pose_tiles(int L) {
 // <= 32, i.e. L <= 27): per row 8 shared loads feed 16 FMAs. TPL = 0: lane-
 // owned entries e = lane + 32 q (Q of them), any L <= 64.
 template <int Q, int TPL>
-__global__ void __launch_bounds__(256, 2) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
+__global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
   extern __shared__ __align__(16) double psm[];
   const int L = m.L;
   const int Lr = (L + 1) | 1;  // row stride: L Jacobian entries + the residual, odd
