@@ -12,7 +12,7 @@ $cmd > $out/plain.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv $cmd > $out/ncu_launches.log 2>&1
 pcmd="python tools/profile_frame.py c3 3"
 $pcmd > $out/plain_prof.log 2>&1 || exit 2
-for k in k_search k_pose_system k_normals k_shape k_scatter k_pixoff k_skin; do
+for k in k_search k_pose_system k_pose_solve k_normals k_shape k_scatter k_pixoff k_skin; do
   ncu --set full --clock-control none --import-source on -k regex:"${k}" -s 6 -c 2 -o $out/full_$k $pcmd \
     > $out/ncu_full_$k.log 2>&1
 done
