@@ -746,6 +746,13 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     int* d_depth = c->mem.alloc<int>(L);
     upload(d_depth, depth.data(), L, c->stream);
     double* d_s = c->mem.alloc<double>(L);
+    // JtJ / Jtr entry table of the pose kernels: row-major upper triangle, then Jtr
+    std::vector<unsigned> pose_e;
+    for (int r = 0; r < L; ++r)
+      for (int cc = r; cc < L; ++cc) pose_e.push_back(static_cast<unsigned>(r) | (static_cast<unsigned>(cc) << 16));
+    for (int r = 0; r < L; ++r) pose_e.push_back(static_cast<unsigned>(r) | (static_cast<unsigned>(L) << 16));
+    unsigned* d_pe = c->mem.alloc<unsigned>(pose_e.size());
+    upload(d_pe, pose_e.data(), pose_e.size(), c->stream);
     upload(d_v0, v0.data(), V, c->stream);
     upload(d_wg, wg.data(), V, c->stream);
     upload(d_wl, wl.data(), V, c->stream);
@@ -759,7 +766,7 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     upload(d_pow, c->pair_owner.data(), c->NP, c->stream);
     upload(d_s, c->s_diag.data(), L, c->stream);
     c->dm = wt::DevModel{V, L, c->NP, K, d_v0, d_wg, d_wl, d_roff, d_ring, d_nbr,
-                         d_links, d_poff, d_pth, d_plk, d_pow, d_s, d_depth, max_depth};
+                         d_links, d_poff, d_pth, d_plk, d_pow, d_s, d_depth, max_depth, d_pe};
 
     alloc_state(c, c->ds, false);
     c->hs = c->ds;  // hooks share the per-vertex buffers, own theta/fk/offsets/dchain

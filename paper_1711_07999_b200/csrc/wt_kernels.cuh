@@ -40,6 +40,7 @@ struct DevModel {
   const double* s_diag;    // [L] influence counts S
   const int* link_depth;   // [L] depth in the tree (root 0)
   int max_depth;
+  const unsigned* pose_e;  // [NE] JtJ/Jtr entry e -> (row | col << 16), col = L for Jtr
 };
 
 struct DevIntr {
@@ -246,6 +247,10 @@ __device__ void fk_run(const DevModel& m, const DevState& s, const double* theta
   __shared__ double cs[64][2];
   const int L = m.L;
   const LinkDesc* sl = t.sl;
+  // this thread's first dchain pair indices, in flight during the FK chain
+  const int p0 = threadIdx.x;
+  const int own0 = p0 < m.NP ? __ldg(m.pair_owner + p0) : 0;
+  const int lnk0 = p0 < m.NP ? __ldg(m.pair_link + p0) : 0;
   // joint transforms and local offsets in parallel (one link per thread);
   // each joint's half-angle sincos is evaluated once ...
   for (int j = threadIdx.x; j < L; j += blockDim.x) {
@@ -278,7 +283,7 @@ __device__ void fk_run(const DevModel& m, const DevState& s, const double* theta
     dq_store(dq_compose(fk[j], dq_load(sl[j].bind_inv)), s.offsets + 8 * j);
   }
   for (int p = threadIdx.x; p < m.NP; p += blockDim.x) {
-    const int j = m.pair_owner[p], kl = m.pair_link[p];
+    const int j = p == p0 ? own0 : m.pair_owner[p], kl = p == p0 ? lnk0 : m.pair_link[p];
     const LinkDesc& lk = sl[kl];
     const DQ off = dq_load(lk.offset);
     const DQ pre = lk.parent < 0 ? off : dq_compose(fk[lk.parent], off);
@@ -1203,52 +1208,91 @@ __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevState s, P
   unsigned short* ea = reinterpret_cast<unsigned short*>(A + L * Lp);  // NE
   unsigned short* eb = ea + NE;
   const long long t2 = clock64();
-  fk_stage(m, fkt);
-  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
-    int ca, cb;
-    if (e < NT) {
-      int r = 0, rem = e;
-      while (rem >= L - r) {
-        rem -= L - r;
-        ++r;
-      }
-      ca = r;
-      cb = r + rem;
-    } else {
-      ca = e - NT;
-      cb = 0xFFFF;
-    }
-    ea[e] = static_cast<unsigned short>(ca);
-    eb[e] = static_cast<unsigned short>(cb);
-    unsigned long long sum = 0ull;
+  // every global load of the prologue in one round: reduction copies, entry
+  // table, theta, S, the link table
+  unsigned long long sum[4] = {0ull, 0ull, 0ull, 0ull};
+  unsigned ent[4] = {0u, 0u, 0u, 0u};
+  {
+    unsigned long long v[4][kRedCopies];
 #pragma unroll
-    for (int c = 0; c < kRedCopies; ++c) {
-      sum += __ldcg(s.red + c * (NE + 2) + e);
-      s.red[c * (NE + 2) + e] = 0ull;
+    for (int q = 0; q < 4; ++q) {
+      const int e = threadIdx.x + q * blockDim.x;
+      if (e < NE) {
+        ent[q] = __ldg(m.pose_e + e);
+#pragma unroll
+        for (int c = 0; c < kRedCopies; ++c) v[q][c] = __ldcg(s.red + c * (NE + 2) + e);
+      }
     }
-    const double val = unfix(sum, kFixSys);
-    if (cb == 0xFFFF) {
+    double th = 0.0, sd = 0.0;
+    if (threadIdx.x < L) {
+      th = s.theta[threadIdx.x];
+      sd = __ldg(m.s_diag + threadIdx.x);
+    }
+    unsigned long long rv[2 * kRedCopies];
+    if (threadIdx.x == blockDim.x - 1) {
+#pragma unroll
+      for (int c = 0; c < kRedCopies; ++c) {
+        rv[2 * c] = __ldcg(s.red + c * (NE + 2) + NE);
+        rv[2 * c + 1] = __ldcg(s.red + c * (NE + 2) + NE + 1);
+      }
+    }
+    fk_stage(m, fkt);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < kRedCopies; ++c) sum[q] += v[q][c];
+    if (threadIdx.x < L) {
+      s_theta[threadIdx.x] = th;
+      s_x[threadIdx.x] = sd;  // staged S for the prior
+    }
+    if (threadIdx.x == blockDim.x - 1) {
+      unsigned long long rs = 0ull, na = 0ull;
+#pragma unroll
+      for (int c = 0; c < kRedCopies; ++c) {
+        rs += rv[2 * c];
+        na += rv[2 * c + 1];
+        s.red[c * (NE + 2) + NE] = 0ull;
+        s.red[c * (NE + 2) + NE + 1] = 0ull;
+      }
+      s_rsum = unfix(rs, kFixRes);
+      s_nassoc = static_cast<long long>(na);
+      s_finite = 1;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = threadIdx.x + q * blockDim.x;
+    if (e >= NE) continue;
+#pragma unroll
+    for (int c = 0; c < kRedCopies; ++c) s.red[c * (NE + 2) + e] = 0ull;  // self-cleaning
+    const int ca = ent[q] & 0xFFFF, cb = ent[q] >> 16;
+    ea[e] = static_cast<unsigned short>(ca);
+    eb[e] = static_cast<unsigned short>(cb == L ? 0xFFFF : cb);
+    const double val = unfix(sum[q], kFixSys);
+    if (cb == L) {
       jtr[ca] = val;
     } else {
       A[ca * Lp + cb] = val;
       A[cb * Lp + ca] = val;
     }
   }
-  if (threadIdx.x == 0) {
-    unsigned long long rs = 0ull, na = 0ull;
+  for (int e = threadIdx.x + 4 * blockDim.x; e < NE; e += blockDim.x) {  // L > 43: the rest
+    unsigned long long t = 0ull;
     for (int c = 0; c < kRedCopies; ++c) {
-      rs += __ldcg(s.red + c * (NE + 2) + NE);
-      na += __ldcg(s.red + c * (NE + 2) + NE + 1);
-      s.red[c * (NE + 2) + NE] = 0ull;
-      s.red[c * (NE + 2) + NE + 1] = 0ull;
+      t += __ldcg(s.red + c * (NE + 2) + e);
+      s.red[c * (NE + 2) + e] = 0ull;
     }
-    s_rsum = unfix(rs, kFixRes);
-    s_nassoc = static_cast<long long>(na);
-    s_finite = 1;
-  }
-  for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    s_theta[k] = s.theta[k];
-    s_x[k] = m.s_diag[k];  // staged S for the prior
+    const unsigned en = __ldg(m.pose_e + e);
+    const int ca = en & 0xFFFF, cb = en >> 16;
+    ea[e] = static_cast<unsigned short>(ca);
+    eb[e] = static_cast<unsigned short>(cb == L ? 0xFFFF : cb);
+    const double val = unfix(t, kFixSys);
+    if (cb == L) {
+      jtr[ca] = val;
+    } else {
+      A[ca * Lp + cb] = val;
+      A[cb * Lp + ca] = val;
+    }
   }
   __syncthreads();
   // default-pose prior (lambda_s S)^2 on the diagonal (kinopt.cpp:113-117),
