@@ -24,6 +24,7 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
 
 UNITS = [
     ("wt_gpu.cu", []),
+    ("wt_exact.cu", ["-fmad=false"]),
     ("wt_render.cu", ["-fmad=false"]),
 ]
 

@@ -20,6 +20,12 @@
 #include "wt_kernels.cuh"
 
 namespace wt {
+// wt_exact.cu (compiled without FMA contraction)
+void launch_skin(cudaStream_t st, int grid, int L, const DevModel& m, const DevState& s, const double4* phi);
+void launch_normals(cudaStream_t st, int grid, const DevModel& m, const DevState& s, const DevIntr& in,
+                    int do_bucket, int zero_acc, int compute);
+void launch_fk(cudaStream_t st, const DevModel& m, const DevState& s);
+void launch_pose_solve(cudaStream_t st, int L, const DevModel& m, const DevState& s, const PoseArgs& a);
 void render_launch(cudaStream_t st, int V, int L, int T, const double* offsets, const double* v0,
                    const double* phi, const double* wgt, const int* wlink, const int* wcount,
                    const int* tri, const int* dom, double fx, double fy, double cx, double cy,
@@ -328,19 +334,18 @@ void ensure_stats(wt_gpu_ctx* c, int nk, int ns) {
 // ---- kernel launch helpers (all on ctx->stream) ------------------------------
 
 void enq_fk(wt_gpu_ctx* c, const wt::DevState& s) {
-  wt::k_fk<<<1, 128, 0, c->stream>>>(c->dm, s);
+  wt::launch_fk(c->stream, c->dm, s);
   mark(c, K_FK);
 }
 
 void enq_skin(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi) {
-  wt::k_skin<<<vgrid(c->V), wt::kVThreads, sizeof(double) * 8 * c->L, c->stream>>>(c->dm, s, phi);
+  wt::launch_skin(c->stream, vgrid(c->V), c->L, c->dm, s, phi);
   mark(c, K_SKIN);
 }
 
 void enq_normals(wt_gpu_ctx* c, const wt::DevState& s, bool bucket, bool zero_acc,
                  bool compute = true) {
-  wt::k_normals<<<vgrid(c->V), wt::kVThreads, 0, c->stream>>>(
-      c->dm, s, c->din, bucket ? 1 : 0, zero_acc ? 1 : 0, compute ? 1 : 0);
+  wt::launch_normals(c->stream, vgrid(c->V), c->dm, s, c->din, bucket ? 1 : 0, zero_acc ? 1 : 0, compute ? 1 : 0);
   mark(c, K_NORMALS);
 }
 
@@ -437,7 +442,7 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
     }
   }
   mark(c, K_POSE);
-  wt::k_pose_solve<<<1, 256, wt::pose_solve_smem_bytes(c->L), c->stream>>>(c->dm, s, pa);
+  wt::launch_pose_solve(c->stream, c->L, c->dm, s, pa);
   mark(c, K_POSE_SOLVE);
 }
 
@@ -708,9 +713,11 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
       ring_off[i] = d->vtri_offsets[i];
       for (int k = d->vtri_offsets[i]; k < d->vtri_offsets[i + 1]; ++k) {
         const int* t = d->triangles + 3 * d->vtri_items[k];
+        // (b, c) follow i cyclically; bits 30-31 of .x carry i's position in
+        // the triangle so the kernel rebuilds (f0, f1, f2) in stored order
         if (t[0] == i) ring[k] = make_int2(t[1], t[2]);
-        else if (t[1] == i) ring[k] = make_int2(t[2], t[0]);
-        else if (t[2] == i) ring[k] = make_int2(t[0], t[1]);
+        else if (t[1] == i) ring[k] = make_int2(t[2] | (1 << 30), t[0]);
+        else if (t[2] == i) ring[k] = make_int2(t[0] | (2 << 30), t[1]);
         else fail(WT_EINVAL, "vertex->triangle CSR lists a triangle that does not contain the vertex");
       }
     }
@@ -1126,7 +1133,7 @@ int wt_gpu_joint_positions(wt_gpu_ctx* c, double* joints_out) {
     ensure_seq(c, 1);
     // FK of the current theta into the hook state, then the origins
     WT_CUDA(cudaMemcpyAsync(c->hs.theta, c->ds.theta, sizeof(double) * c->L, cudaMemcpyDeviceToDevice, c->stream));
-    wt::k_fk<<<1, 128, 0, c->stream>>>(c->dm, c->hs);
+    wt::launch_fk(c->stream, c->dm, c->hs);
     wt::k_record<<<1, 64, 0, c->stream>>>(c->dm, c->hs, nullptr, c->rec_buf);
     check_launch();
     WT_CUDA(cudaMemcpyAsync(joints_out, c->rec_buf, sizeof(double) * c->L * 3, cudaMemcpyDeviceToHost,

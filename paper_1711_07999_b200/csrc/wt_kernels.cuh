@@ -122,7 +122,7 @@ __device__ __forceinline__ bool last_block(unsigned* ticket) {
 
 // Block-wide exclusive scan over n ints in shared memory (in place);
 // returns the total. blockDim.x must be a multiple of 32.
-__device__ int block_exclusive_scan(int* a, int n) {
+__device__ inline int block_exclusive_scan(int* a, int n) {
   __shared__ int warp_tot[32];
   __shared__ int carry;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -240,7 +240,7 @@ __device__ __forceinline__ void fk_stage(const DevModel& m, FkTables& t) {
 }
 
 // Requires fk_stage(m, t) and a barrier before the call.
-__device__ void fk_run(const DevModel& m, const DevState& s, const double* theta_in, const FkTables& t,
+__device__ inline void fk_run(const DevModel& m, const DevState& s, const double* theta_in, const FkTables& t,
                        long long* stamps = nullptr) {
   __shared__ DQ fk[64];
   __shared__ DQ loc[64];
@@ -293,14 +293,15 @@ __device__ void fk_run(const DevModel& m, const DevState& s, const double* theta
   }
 }
 
-__device__ void block_fk(const DevModel& m, const DevState& s, const double* theta_in) {
+__device__ inline void block_fk(const DevModel& m, const DevState& s, const double* theta_in) {
   __shared__ FkTables t;
   fk_stage(m, t);
   __syncthreads();
   fk_run(m, s, theta_in, t);
 }
 
-__global__ void k_fk(DevModel m, DevState s) { block_fk(m, s, s.theta); }
+static __global__ void k_fk(DevModel m, DevState s) { block_fk(m, s, s.theta); }
+
 
 // ---------------------------------------------------------------------------
 // frame ingest: depth_to_cloud (seqio.cpp:419-437) in fp64 and the list of
@@ -311,7 +312,7 @@ __global__ void k_fk(DevModel m, DevState s) { block_fk(m, s, s.theta); }
 
 constexpr int kIngestSeg = 256;
 
-__global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const float* depth, double scale,
+static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const float* depth, double scale,
                                                       const double* cloud, const uint8_t* cloud_valid,
                                                       uint8_t* pvalid, double* pts_hi, int* vlist,
                                                       int* n_valid) {
@@ -356,10 +357,11 @@ __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const float* 
   }
 }
 
+
 // ---------------------------------------------------------------------------
 // K1 skinning: v = normalize(blend)(v0 + phi) (skinmesh.cpp:112-121).
 
-__global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, const double4* phi) {
+static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, const double4* phi) {
   extern __shared__ double s_off[];
   load_offsets(m, s, s_off);
   __syncthreads();
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, cons
 // K2 normals (skinmesh.cpp:125-139) fused with K3a: back-face cull, projection
 // with lround semantics (association.cpp:29-37,49-51) and the bin histogram.
 
-__global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, DevIntr in,
+static __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, DevIntr in,
                                                        int do_bucket, int zero_acc, int compute) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m.V) {
@@ -394,26 +396,35 @@ __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, D
     double nx = 0, ny = 0, nz = 0;
     bool valid;
     if (compute) {
+      // normals exactly as skin() (skinmesh.cpp:125-139): per incident
+      // triangle (f0, f1, f2) in CSR order, acc += (v1 - v0) x (v2 - v0);
+      // this unit is compiled without FMA contraction, so the sums round
+      // like the reference's
       double ax = 0, ay = 0, az = 0;
       const int r0 = m.ring_off[i], r1 = m.ring_off[i + 1];
       for (int r = r0; r < r1; r += 8) {
         // eight incident triangles per step (most vertices have <= 8): index
-        // loads, then all sixteen position gathers in flight, then the cross
-        // products in CSR order
+        // loads, then all sixteen position gathers in flight
         int2 bc[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(i, i);
         double4 pb[8], pc[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          pb[q] = s.pv[bc[q].x];
+          pb[q] = s.pv[bc[q].x & 0x3FFFFFFF];
           pc[q] = s.pv[bc[q].y];
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           if (r + q >= r1) break;
-          const double ex = pb[q].x - vx, ey = pb[q].y - vy, ez = pb[q].z - vz;
-          const double fx = pc[q].x - vx, fy = pc[q].y - vy, fz = pc[q].z - vz;
+          // ring entry: b, c follow i cyclically; bits 30-31 of .x = position of i
+          const int rot = static_cast<int>(static_cast<unsigned>(bc[q].x) >> 30);
+          const double4 pi = v;
+          const double4& f0 = rot == 0 ? pi : (rot == 1 ? pc[q] : pb[q]);
+          const double4& f1 = rot == 0 ? pb[q] : (rot == 1 ? pi : pc[q]);
+          const double4& f2 = rot == 0 ? pc[q] : (rot == 1 ? pb[q] : pi);
+          const double ex = f1.x - f0.x, ey = f1.y - f0.y, ez = f1.z - f0.z;
+          const double fx = f2.x - f0.x, fy = f2.y - f0.y, fz = f2.z - f0.z;
           ax += ey * fz - ez * fy;
           ay += ez * fx - ex * fz;
           az += ex * fy - ey * fx;
@@ -478,9 +489,10 @@ __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, D
 // the preceding rows' counts (warp reduction); the row is read in coalesced
 // 32-pixel chunks, all loads first, then scanned chunk by chunk with
 // shuffles. Clears the per-pixel counts for the next association.
+
 constexpr int kRowChunks = 64;  // rows up to 2048 pixels
 
-__global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, int H) {
+static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, int H) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= H) return;
@@ -533,7 +545,7 @@ __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, int H) 
 // K3c: scatter into pixel order (association.cpp:60-66; unordered within a
 // pixel -- the winner rule is a lexicographic (d^2, index) minimum, so bucket
 // order never changes a result). Clears the row counts for the next pass.
-__global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevState s, int H) {
+static __global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevState s, int H) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < H) s.row_cnt[i] = 0;
   if (i >= m.V) return;
@@ -645,7 +657,7 @@ __device__ __forceinline__ void group_min(double& bx, int& bi) {
   }
 }
 
-__global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
+static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
   const int nv = *f.n_valid;
   const int w = a.window;
   const int K1 = min(kNearRings, w);
@@ -750,7 +762,7 @@ __device__ __forceinline__ bool observed_mean(const unsigned long long* acc, int
 // thread updates trailing entries (i,j) listed in the (ea, eb) upper-triangle
 // table. A is row-major (lower triangle used, overwritten); b is overwritten;
 // x receives the solution. Must be called by all threads of the CTA.
-__device__ int block_ldlt_solve(int L, int lda, double* A, double* b, double* x, const unsigned short* ea,
+__device__ inline int block_ldlt_solve(int L, int lda, double* A, double* b, double* x, const unsigned short* ea,
                                 const unsigned short* eb, int NT) {
   __shared__ int s_ok;
   __shared__ double inv_d[64];
@@ -802,7 +814,7 @@ __device__ int block_ldlt_solve(int L, int lda, double* A, double* b, double* x,
 // unit-L factor written back to A (row stride lda). Returns 1 on success (x
 // written), 0 when a pivot is not strictly positive. Call from a full warp.
 template <int N>
-__device__ int warp_ldlt_solve(int L, int lda, double* A, const double* b, double* x) {
+__device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b, double* x) {
   const int lane = threadIdx.x & 31;
   const bool row = lane < L;
   double a[N];
@@ -890,7 +902,7 @@ __host__ __device__ inline int pose_tiles(int L) {
 // <= 32, i.e. L <= 27): per row 8 shared loads feed 16 FMAs. TPL = 0: lane-
 // owned entries e = lane + 32 q (Q of them), any L <= 64.
 template <int Q, int TPL>
-__global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
+static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
   extern __shared__ __align__(16) double psm[];
   const int L = m.L;
   const int Lr = (L + 1) | 1;  // row stride: L Jacobian entries + the residual, odd
@@ -1178,6 +1190,7 @@ __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevState s, 
   if (a.dbg && threadIdx.x == 0 && blockIdx.x == 0) a.dbg[0] = t1 - t0;
 }
 
+
 // K7 (+K0): the pose-solve step, one CTA right after k_pose_system in the
 // same stream: fold the reduction copies into JtJ / Jtr, add the prior
 // (kinopt.cpp:113-117), damp and factor (solve_step, kinopt.cpp:121-130;
@@ -1190,7 +1203,7 @@ __host__ __device__ inline size_t pose_solve_smem_bytes(int L) {
   return sizeof(double) * L * (L | 1) + sizeof(unsigned short) * 2 * NE + 16;
 }
 
-__global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevState s, PoseArgs a) {
+static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevState s, PoseArgs a) {
   __shared__ FkTables fkt;
   extern __shared__ __align__(16) double solve_sm[];  // pose_solve_smem_bytes(L)
   __shared__ double jtr[64];
@@ -1383,6 +1396,7 @@ __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevState s, P
   }
 }
 
+
 // ---------------------------------------------------------------------------
 // K8: per-vertex regularised 3x3 shape step (optimize_shape body,
 // shapeopt.cpp:78-96, solve_vertex :25-48), Jacobi: reads phi_in, writes
@@ -1439,7 +1453,7 @@ struct ShapeArgs {
   int pad;
 };
 
-__global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState s, const double4* phi_in,
+static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState s, const double4* phi_in,
                                                      double4* phi_out, ShapeArgs a) {
   extern __shared__ double s_off[];
   load_offsets(m, s, s_off);
@@ -1532,7 +1546,7 @@ __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState s, con
 
 // Closing measurement pass of optimize_shape (shapeopt.cpp:112-129): mean
 // |r| over observed vertices of a fresh association; fills mean_abs_r_after.
-__global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, DevState s, int n_its) {
+static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, DevState s, int n_its) {
   double abs_r = 0.0;
   long long observed = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
@@ -1568,7 +1582,7 @@ __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, DevState 
 
 // solve_step on an explicit system (kinopt.cpp:121-130): out[0..n) = x,
 // out[n] = 1 on success, 0 for NotPositiveDefinite.
-__global__ void k_solve_step(int n, const double* jtj, const double* jtr, double lambda_k,
+static __global__ void k_solve_step(int n, const double* jtj, const double* jtr, double lambda_k,
                              double diag_floor, double* out) {
   extern __shared__ double sm[];
   double* A = sm;
@@ -1604,7 +1618,7 @@ __global__ void k_solve_step(int n, const double* jtj, const double* jtr, double
   if (threadIdx.x == 0) out[n] = ok ? 1.0 : 0.0;
 }
 
-__global__ void k_solve_vertices(int n, const double* dr, const double* r, const double* phi,
+static __global__ void k_solve_vertices(int n, const double* dr, const double* r, const double* phi,
                                  const double* nd, const int* ncount, double lphi, double lnbr,
                                  double lw, double floor_, double* delta, uint8_t* singular) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1621,7 +1635,7 @@ __global__ void k_solve_vertices(int n, const double* dr, const double* r, const
 // run_tracking's per-frame record (tracker.cpp:84-90): theta and the world
 // origin of every link, transform_point(H_0j, 0), from the FK the frame's
 // last pose-solve tail (or k_fk) left in s.fk for the current theta.
-__global__ void k_record(DevModel m, DevState s, double* theta_out, double* joints_out) {
+static __global__ void k_record(DevModel m, DevState s, double* theta_out, double* joints_out) {
   const int j = threadIdx.x;
   if (j >= m.L) return;
   if (theta_out) theta_out[j] = s.theta[j];
