@@ -213,6 +213,13 @@ int wt_gpu_track_frame_cloud(wt_gpu_ctx* ctx, const double* points, const uint8_
  * n_frames; the final Phi stays in the context (wt_gpu_get_state). */
 int wt_gpu_track_sequence(wt_gpu_ctx* ctx, const float* frames, int32_t n_frames, double depth_scale,
                           const wt_track_config* cfg, double* theta_out, double* joints_out);
+/* reconstruction_error_frame (metrics.cpp:110-142) of the current state (theta,
+ * Phi) against the loaded frame: for every vertex visible in the z-buffer of
+ * the posed mesh (front-facing, in frame, within 1 mm of the depth at its
+ * pixel) the distance to the nearest valid observed point, exact (brute force,
+ * fp64). dist [V] receives NaN for vertices that are not visible; n_visible
+ * (nullable) their count. */
+int wt_gpu_recon_error(wt_gpu_ctx* ctx, double* dist, int32_t* n_visible);
 /* Link origins at the current theta, [L*3] (tracker.cpp:84-86). */
 int wt_gpu_joint_positions(wt_gpu_ctx* ctx, double* joints_out);
 /* optimize_pose (kinopt.cpp:132-171) / optimize_shape (shapeopt.cpp:50-130)

@@ -340,3 +340,15 @@ def run_tracking(model: RefModel, path, cfg: W.TrackConfigC, init_theta=None):
     init = None if init_theta is None else np.ascontiguousarray(init_theta, float)
     _check(lib().wtref_run_tracking(model.h, str(path).encode(), C.byref(cfg), _p(init), _p(th), _p(jt), _p(ph)))
     return dict(theta=th, joints=jt, final_phi=ph)
+
+
+def recon_error(model: RefModel, theta, intr: W.Intrinsics, points, valid, phi=None, threads: int = 0):
+    """reconstruction_error_frame (metrics.cpp:110-142): visible-vertex distances."""
+    V = model.sizes()[1]
+    d = np.zeros(V)
+    n = C.c_int()
+    _check(lib().wtref_recon_error(model.h, _p(np.ascontiguousarray(theta, float)),
+                                   _p(None if phi is None else np.ascontiguousarray(phi, float)), C.byref(intr),
+                                   _p(np.ascontiguousarray(points, float)), _p(np.ascontiguousarray(valid, np.uint8)),
+                                   threads, _p(d), C.byref(n)))
+    return d[:n.value]

@@ -743,5 +743,23 @@ int wtref_run_tracking(const wtref_model* m, const char* path, const wt_track_co
   });
 }
 
+// reconstruction_error_frame (metrics.cpp:110-142) of the model posed at
+// (theta, phi) against an organized cloud: distances of the visible vertices
+// in ascending vertex order, count in *n.
+int wtref_recon_error(const wtref_model* m, const double* theta, const double* phi, const wt_intrinsics* intr,
+                      const double* points, const uint8_t* valid, int threads, double* dist, int* n) {
+  return guarded([&] {
+    const Skeleton& sk = m->bundle.skeleton;
+    const auto off = link_offsets(sk, to_pose(theta, sk.joint_count()));
+    const std::size_t nv = m->bundle.mesh.v0.size();
+    const PosedMesh posed = phi ? skin(m->bundle.mesh, off, vec3s(phi, nv), 1) : skin(m->bundle.mesh, off, 1);
+    const Intrinsics in = to_intr(intr);
+    const std::vector<double> d =
+        reconstruction_error_frame(posed, m->bundle.mesh.triangles, to_cloud(in, points, valid), in, threads);
+    std::copy(d.begin(), d.end(), dist);
+    *n = static_cast<int>(d.size());
+  });
+}
+
 }  // extern "C"
 

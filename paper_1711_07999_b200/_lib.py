@@ -90,7 +90,7 @@ EXPORTS = [
     "wt_gpu_track_frame_cloud", "wt_gpu_optimize_pose", "wt_gpu_optimize_shape", "wt_gpu_skin",
     "wt_gpu_associate", "wt_gpu_associate_posed", "wt_gpu_normal_system", "wt_gpu_solve_step",
     "wt_gpu_solve_vertices", "wt_gpu_render_depth", "wt_gpu_stream", "wt_gpu_track_async", "wt_gpu_sync",
-    "wt_gpu_profile_frame", "wt_gpu_track_sequence", "wt_gpu_joint_positions",
+    "wt_gpu_profile_frame", "wt_gpu_track_sequence", "wt_gpu_joint_positions", "wt_gpu_recon_error",
 ]
 KERNEL_KINDS = ["fk", "skin", "normals+bucket", "scatter", "search+average", "pose_system",
                 "shape_step", "shape_stats", "pose_solve"]
@@ -166,6 +166,7 @@ def _declare(L: C.CDLL) -> None:
     L.wt_gpu_sync.argtypes = [vp]
     L.wt_gpu_track_sequence.argtypes = [vp, vp, C.c_int32, C.c_double, P(TrackConfigC), vp, vp]
     L.wt_gpu_joint_positions.argtypes = [vp, vp]
+    L.wt_gpu_recon_error.argtypes = [vp, vp, P(C.c_int32)]
     L.wt_gpu_profile_frame.argtypes = [vp, P(TrackConfigC), vp, vp, C.c_int32, P(C.c_int32)]
 
 

@@ -25,6 +25,9 @@ void launch_skin(cudaStream_t st, int grid, int L, const DevModel& m, const DevS
 void launch_normals(cudaStream_t st, int grid, const DevModel& m, const DevState& s, const DevIntr& in,
                     int do_bucket, int zero_acc, int compute);
 void launch_fk(cudaStream_t st, const DevModel& m, const DevState& s);
+void recon_launch(cudaStream_t st, const DevModel& m, const DevState& s, const DevIntr& in, int T, const int* tri,
+                  double* v3, unsigned long long* zbits, int* owner, const uint8_t* pvalid, const double* pts,
+                  double* ox, double* oy, double* oz, int* vis_list, int* counters, double* dist);
 void launch_pose_solve(cudaStream_t st, int L, const DevModel& m, const DevState& s, const PoseArgs& a);
 void render_launch(cudaStream_t st, int V, int L, int T, const double* offsets, const double* v0,
                    const double* phi, const double* wgt, const int* wlink, const int* wcount,
@@ -147,6 +150,12 @@ struct wt_gpu_ctx {
   uint8_t* r_vis = nullptr;
   std::vector<double> h_v0, h_wgt;
   std::vector<int> h_wlink, h_wcount, h_tri;
+
+  // reconstruction error buffers (lazily built)
+  double* rc_obs = nullptr;  // [3P] observed points, SoA
+  int* rc_vis = nullptr;     // [V] visible vertices
+  int* rc_cnt = nullptr;     // [2] visible / observed counts
+  double* rc_dist = nullptr; // [V]
 
   int* hook_cnt = nullptr;
   double* hook_res = nullptr;
@@ -1241,6 +1250,34 @@ int wt_gpu_skin(wt_gpu_ctx* c, const double* theta, const double* phi, double* v
       }
       if (valid) valid[i] = pn[i].w != 0.0f ? 1 : 0;
     }
+  });
+}
+
+// reconstruction_error_frame (metrics.cpp:110-142) of the current state
+// against the loaded frame: dist[V], NaN for vertices that are not visible.
+int wt_gpu_recon_error(wt_gpu_ctx* c, double* dist, int32_t* n_visible) {
+  if (!c || !dist) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    require_frame(c);
+    ensure_render(c);
+    if (!c->rc_obs) {
+      c->rc_obs = c->mem.alloc<double>(3 * static_cast<size_t>(c->P));
+      c->rc_vis = c->mem.alloc<int>(c->V);
+      c->rc_cnt = c->mem.alloc<int>(2);
+      c->rc_dist = c->mem.alloc<double>(c->V);
+    }
+    enq_fk(c, c->ds);
+    enq_skin(c, c->ds, c->phi[c->cur]);
+    wt::recon_launch(c->stream, c->dm, c->ds, c->din, c->T, c->r_tri, c->r_vpos, c->r_zbits, c->r_owner, c->d_valid,
+                     c->d_pts_hi, c->rc_obs, c->rc_obs + c->P, c->rc_obs + 2 * static_cast<size_t>(c->P), c->rc_vis,
+                     c->rc_cnt, c->rc_dist);
+    check_launch();
+    WT_CUDA(cudaMemcpyAsync(dist, c->rc_dist, sizeof(double) * c->V, cudaMemcpyDeviceToHost, c->stream));
+    int cnt[2] = {0, 0};
+    WT_CUDA(cudaMemcpyAsync(cnt, c->rc_cnt, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    if (n_visible) *n_visible = cnt[0];
   });
 }
 

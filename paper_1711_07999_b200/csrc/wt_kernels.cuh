@@ -383,6 +383,50 @@ static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState 
   s.pv[i] = out;
 }
 
+// Vertex normal exactly as skin() (skinmesh.cpp:125-139): per incident
+// triangle (f0, f1, f2) in CSR order, acc += (v1 - v0) x (v2 - v0), then
+// acc / |acc|; returns the PosedMesh valid flag (blend ok and |acc| > 1e-20).
+// Bitwise the reference's when compiled without FMA contraction (wt_exact.cu).
+__device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* pv, int i, const double4& v,
+                                              double& nx, double& ny, double& nz) {
+  double ax = 0, ay = 0, az = 0;
+  const int r0 = m.ring_off[i], r1 = m.ring_off[i + 1];
+  for (int r = r0; r < r1; r += 8) {
+    // eight incident triangles per step (most vertices have <= 8): index
+    // loads, then all sixteen position gathers in flight
+    int2 bc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(i, i);
+    double4 pb[8], pc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      pb[q] = pv[bc[q].x & 0x3FFFFFFF];
+      pc[q] = pv[bc[q].y];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (r + q >= r1) break;
+      // ring entry: b, c follow i cyclically; bits 30-31 of .x = position of i
+      const int rot = static_cast<int>(static_cast<unsigned>(bc[q].x) >> 30);
+      const double4& f0 = rot == 0 ? v : (rot == 1 ? pc[q] : pb[q]);
+      const double4& f1 = rot == 0 ? pb[q] : (rot == 1 ? v : pc[q]);
+      const double4& f2 = rot == 0 ? pc[q] : (rot == 1 ? pb[q] : v);
+      const double ex = f1.x - f0.x, ey = f1.y - f0.y, ez = f1.z - f0.z;
+      const double fx = f2.x - f0.x, fy = f2.y - f0.y, fz = f2.z - f0.z;
+      ax += ey * fz - ez * fy;
+      ay += ez * fx - ex * fz;
+      az += ex * fy - ey * fx;
+    }
+  }
+  const double len = sqrt(ax * ax + ay * ay + az * az);
+  nx = ny = nz = 0.0;
+  if (!(len > 1e-20)) return false;
+  nx = ax / len;
+  ny = ay / len;
+  nz = az / len;
+  return v.w != 0.0;
+}
+
 // ---------------------------------------------------------------------------
 // K2 normals (skinmesh.cpp:125-139) fused with K3a: back-face cull, projection
 // with lround semantics (association.cpp:29-37,49-51) and the bin histogram.
@@ -396,49 +440,7 @@ static __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevSta
     double nx = 0, ny = 0, nz = 0;
     bool valid;
     if (compute) {
-      // normals exactly as skin() (skinmesh.cpp:125-139): per incident
-      // triangle (f0, f1, f2) in CSR order, acc += (v1 - v0) x (v2 - v0);
-      // this unit is compiled without FMA contraction, so the sums round
-      // like the reference's
-      double ax = 0, ay = 0, az = 0;
-      const int r0 = m.ring_off[i], r1 = m.ring_off[i + 1];
-      for (int r = r0; r < r1; r += 8) {
-        // eight incident triangles per step (most vertices have <= 8): index
-        // loads, then all sixteen position gathers in flight
-        int2 bc[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(i, i);
-        double4 pb[8], pc[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          pb[q] = s.pv[bc[q].x & 0x3FFFFFFF];
-          pc[q] = s.pv[bc[q].y];
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (r + q >= r1) break;
-          // ring entry: b, c follow i cyclically; bits 30-31 of .x = position of i
-          const int rot = static_cast<int>(static_cast<unsigned>(bc[q].x) >> 30);
-          const double4 pi = v;
-          const double4& f0 = rot == 0 ? pi : (rot == 1 ? pc[q] : pb[q]);
-          const double4& f1 = rot == 0 ? pb[q] : (rot == 1 ? pi : pc[q]);
-          const double4& f2 = rot == 0 ? pc[q] : (rot == 1 ? pb[q] : pi);
-          const double ex = f1.x - f0.x, ey = f1.y - f0.y, ez = f1.z - f0.z;
-          const double fx = f2.x - f0.x, fy = f2.y - f0.y, fz = f2.z - f0.z;
-          ax += ey * fz - ez * fy;
-          ay += ez * fx - ex * fz;
-          az += ex * fy - ey * fx;
-        }
-      }
-      const double len = sqrt(ax * ax + ay * ay + az * az);
-      valid = v.w != 0.0;
-      if (len > 1e-20) {
-        nx = ax / len;
-        ny = ay / len;
-        nz = az / len;
-      } else {
-        valid = false;
-      }
+      valid = vertex_normal(m, s.pv, i, v, nx, ny, nz);
       s.pn[i] = make_float4(static_cast<float>(nx), static_cast<float>(ny), static_cast<float>(nz),
                             valid ? 1.0f : 0.0f);
     } else {  // normals given (loose-vertex association)

@@ -168,6 +168,17 @@ __global__ void k_visibility(int P, const int* owner, const int* tri, const int*
   }
 }
 
+// rasterize (synth.cpp:139-191) of fp64 vertices [V*3]: depth bits and the
+// winning triangle per pixel (0x7F7F7F7F where no triangle reached it).
+void raster_launch(cudaStream_t st, int T, const double* vpos, const int* tri, double fx, double fy, double cx,
+                   double cy, int W, int H, unsigned long long* zbits, int* owner) {
+  const int P = W * H;
+  cudaMemsetAsync(zbits, 0xFF, sizeof(unsigned long long) * P, st);
+  cudaMemsetAsync(owner, 0x7F, sizeof(int) * P, st);
+  k_raster<<<(T + 127) / 128, 128, 0, st>>>(T, vpos, tri, fx, fy, cx, cy, W, H, 0, zbits, owner);
+  k_raster<<<(T + 127) / 128, 128, 0, st>>>(T, vpos, tri, fx, fy, cx, cy, W, H, 1, zbits, owner);
+}
+
 void render_launch(cudaStream_t st, int V, int L, int T, const double* offsets, const double* v0,
                    const double* phi, const double* wgt, const int* wlink, const int* wcount,
                    const int* tri, const int* dom, double fx, double fy, double cx, double cy,

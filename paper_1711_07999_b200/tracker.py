@@ -253,6 +253,15 @@ class Tracker:
               self._ctx)
         return th, jt
 
+    def reconstruction_error(self, per_vertex: bool = False) -> np.ndarray:
+        """reconstruction_error_frame (metrics.cpp:110-142) of the current
+        state against the loaded frame: distances of the visible vertices in
+        ascending vertex order (per_vertex=True: [V] with NaN where hidden)."""
+        d = np.zeros(self.bundle.vertex_count)
+        n = C.c_int32()
+        check(lib().wt_gpu_recon_error(self._ctx, ptr(d), C.byref(n)), self._ctx)
+        return d if per_vertex else d[~np.isnan(d)]
+
     def joint_positions(self) -> np.ndarray:
         """Link origins at the current theta (tracker.cpp:84-86), [L,3]."""
         out = np.zeros((self.bundle.link_count, 3))

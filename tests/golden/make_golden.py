@@ -101,6 +101,10 @@ def humanoid_fixture() -> None:
         out[f"{tag}_theta"] = np.array(th)
         if tag == "dynamic":
             out["dynamic_phi"] = np.array(ph)
+    # reconstruction error of the frame-3 dynamic state against frame 3
+    pts, val = ref.depth_to_cloud(intr, depths[3])
+    out["recon_frame3"] = ref.recon_error(rm, out["dynamic_theta"][2], intr, pts, val,
+                                          phi=np.asarray(out["dynamic_phi"][2], np.float64))
     np.savez_compressed(OUT / "humanoid7k_320x240.npz", **model_arrays(b),
                         intr=np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height]),
                         theta0=humanoid_trajectory(L, 0), depths=np.array(depths), **out)

@@ -250,3 +250,37 @@ def test_long_chains_against_oracle(links):
     assert sg[0].associated > 20
     assert np.abs(g.get_state()[0] - o.get_state()[0]).max() <= 1e-6
     g.close()
+
+
+def test_reconstruction_error_bitwise():
+    """reconstruction_error_frame (metrics.cpp:110-142): same visible set and
+    bitwise the same distances as the reference (exact brute-force NN)."""
+    z, b, ci = load_golden("humanoid7k_320x240")
+    trk = Tracker(b, pyintr(ci))
+    trk.set_state(z["dynamic_theta"][2], np.asarray(z["dynamic_phi"][2], np.float64), 3)
+    trk.load_depth(z["depths"][3])
+    d = trk.reconstruction_error()
+    assert d.shape == z["recon_frame3"].shape
+    assert np.array_equal(d, z["recon_frame3"])
+    per = trk.reconstruction_error(per_vertex=True)
+    assert np.isnan(per).sum() == b.vertex_count - d.size
+    trk.load_depth(np.zeros((ci.height, ci.width), np.float32))  # no observations: zeros
+    assert np.all(trk.reconstruction_error() == 0.0)
+    trk.close()
+
+
+@pytest.mark.ref
+def test_reconstruction_error_matches_live_reference():
+    from oracle import ref
+    from .helpers import humanoid, intr320, theta_at
+    b = humanoid(7000)
+    intr = intr320()
+    rm = ref.RefModel.from_bundle(b)
+    depth, _ = rm.render_depth(theta_at(b, 6), intr.c(), frame=6)
+    th = theta_at(b, 5)
+    trk = Tracker(b, intr, th)
+    trk.load_depth(depth)
+    pts, val = ref.depth_to_cloud(intr.c(), depth)
+    want = ref.recon_error(rm, th, intr.c(), pts, val)
+    assert np.array_equal(trk.reconstruction_error(), want)
+    trk.close()
