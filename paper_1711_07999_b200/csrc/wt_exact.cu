@@ -16,18 +16,20 @@ void raster_launch(cudaStream_t st, int T, const double* vpos, const int* tri, d
                    double cy, int W, int H, unsigned long long* zbits, int* owner);
 
 void launch_skin(cudaStream_t st, int grid, int L, const DevModel& m, const DevState& s, const double4* phi) {
-  k_skin<<<grid, kVThreads, sizeof(double) * 8 * L, st>>>(m, s, phi);
+  launch_pdl(k_skin, dim3(grid), dim3(kVThreads), sizeof(double) * 8 * L, st, m, s, phi);
 }
 
 void launch_normals(cudaStream_t st, int grid, const DevModel& m, const DevState& s, const DevIntr& in,
                     int do_bucket, int zero_acc, int compute) {
-  k_normals<<<grid, kVThreads, 0, st>>>(m, s, in, do_bucket, zero_acc, compute);
+  launch_pdl(k_normals, dim3(grid), dim3(kVThreads), 0, st, m, s, in, do_bucket, zero_acc, compute);
 }
 
-void launch_fk(cudaStream_t st, const DevModel& m, const DevState& s) { k_fk<<<1, 128, 0, st>>>(m, s); }
+void launch_fk(cudaStream_t st, const DevModel& m, const DevState& s) {
+  launch_pdl(k_fk, dim3(1), dim3(128), 0, st, m, s);
+}
 
 void launch_pose_solve(cudaStream_t st, int L, const DevModel& m, const DevState& s, const PoseArgs& a) {
-  k_pose_solve<<<1, 256, pose_solve_smem_bytes(L), st>>>(m, s, a);
+  launch_pdl(k_pose_solve, dim3(1), dim3(256), pose_solve_smem_bytes(L), st, m, s, a);
 }
 
 }  // namespace wt

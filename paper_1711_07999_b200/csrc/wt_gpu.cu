@@ -359,9 +359,11 @@ void enq_normals(wt_gpu_ctx* c, const wt::DevState& s, bool bucket, bool zero_ac
 }
 
 void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
-  wt::k_pixoff<<<(c->din.H + 7) / 8, wt::kVThreads, 0, c->stream>>>(s, c->din.W, c->din.H);
+  WT_CUDA(wt::launch_pdl(wt::k_pixoff, dim3((c->din.H + 7) / 8), dim3(wt::kVThreads), 0, c->stream, s, c->din.W,
+                         c->din.H));
   mark(c, K_SCATTER);
-  wt::k_scatter<<<vgrid(std::max(c->V, c->din.H)), wt::kVThreads, 0, c->stream>>>(c->dm, s, c->din.H);
+  WT_CUDA(wt::launch_pdl(wt::k_scatter, dim3(vgrid(std::max(c->V, c->din.H))), dim3(wt::kVThreads), 0, c->stream,
+                         c->dm, s, c->din.H));
   mark(c, K_SCATTER);
 }
 
@@ -388,7 +390,7 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   }
   // 8 lanes per valid pixel; at most P pixels (the list is padded per 32 columns)
   const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, 16 * 148));
-  wt::k_search<<<grid, wt::kVThreads, 0, c->stream>>>(s, f, sa);
+  WT_CUDA(wt::launch_pdl(wt::k_search, dim3(grid), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
   mark(c, K_SEARCH);
 }
 
@@ -415,9 +417,8 @@ int pose_q(int L) {
 
 template <int Q, int TPL>
 void launch_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt::PoseArgs& pa) {
-  wt::k_pose_system<Q, TPL><<<pose_grid(c), pose_threads(c),
-                              wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32), c->stream>>>(c->dm, s, phi,
-                                                                                                  pa);
+  WT_CUDA(wt::launch_pdl(wt::k_pose_system<Q, TPL>, dim3(pose_grid(c)), dim3(pose_threads(c)),
+                         wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32), c->stream, c->dm, s, phi, pa));
 }
 
 template <int Q, int TPL>
@@ -465,8 +466,8 @@ void enq_shape(wt_gpu_ctx* c, const wt_shape_config* sc, int it, const double4* 
   sa.diag_floor = sc->diag_floor;
   sa.iteration = it;
   sa.pad = 0;
-  wt::k_shape<<<shape_grid(c), wt::kVThreads, sizeof(double) * 8 * c->L, c->stream>>>(c->dm, c->ds,
-                                                                                     in, out, sa);
+  WT_CUDA(wt::launch_pdl(wt::k_shape, dim3(shape_grid(c)), dim3(wt::kVThreads), sizeof(double) * 8 * c->L, c->stream,
+                         c->dm, c->ds, in, out, sa));
   mark(c, K_SHAPE);
 }
 
@@ -499,7 +500,8 @@ int enq_optimize_shape(wt_gpu_ctx* c, int cur, const wt_shape_config* sc, const 
   if (stats_pass && sc->iterations > 0) {
     enq_skin(c, c->ds, c->phi[cur]);
     enq_associate(c, c->ds, a, nullptr);
-    wt::k_shape_after<<<shape_grid(c), wt::kVThreads, 0, c->stream>>>(c->dm, c->ds, sc->iterations);
+    WT_CUDA(wt::launch_pdl(wt::k_shape_after, dim3(shape_grid(c)), dim3(wt::kVThreads), 0, c->stream, c->dm, c->ds,
+                           sc->iterations));
     mark(c, K_SHAPE_AFTER);
   }
   return cur;

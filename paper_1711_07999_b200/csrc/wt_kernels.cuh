@@ -10,7 +10,10 @@
 // integer atomics are associative), so a frame is bitwise reproducible.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 
 #include "wt_dq.cuh"
@@ -88,6 +91,34 @@ struct DevFrame {
   const int* vlist;      // valid pixel indices
   const int* n_valid;
 };
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: the frame graph's kernels are launched with
+// programmatic stream serialisation, so kernel N+1's CTAs become resident
+// while kernel N drains (hiding the launch gap); each kernel lets its
+// successor launch right away and waits for its predecessor's memory before
+// touching any of it. Without PDL both instructions are no-ops.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool use_pdl = getenv("WT_NO_PDL") == nullptr;  // A/B switch for measurements
+  cfg.attrs = attr;
+  cfg.numAttrs = use_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -300,7 +331,7 @@ __device__ inline void block_fk(const DevModel& m, const DevState& s, const doub
   fk_run(m, s, theta_in, t);
 }
 
-static __global__ void k_fk(DevModel m, DevState s) { block_fk(m, s, s.theta); }
+static __global__ void k_fk(DevModel m, DevState s) { pdl_entry(); block_fk(m, s, s.theta); }
 
 
 // ---------------------------------------------------------------------------
@@ -362,6 +393,7 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
 // K1 skinning: v = normalize(blend)(v0 + phi) (skinmesh.cpp:112-121).
 
 static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, const double4* phi) {
+  pdl_entry();
   extern __shared__ double s_off[];
   load_offsets(m, s, s_off);
   __syncthreads();
@@ -433,6 +465,7 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
 
 static __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, DevIntr in,
                                                        int do_bucket, int zero_acc, int compute) {
+  pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m.V) {
     const double4 v = s.pv[i];
@@ -495,6 +528,7 @@ static __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevSta
 constexpr int kRowChunks = 64;  // rows up to 2048 pixels
 
 static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, int H) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= H) return;
@@ -548,6 +582,7 @@ static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, 
 // pixel -- the winner rule is a lexicographic (d^2, index) minimum, so bucket
 // order never changes a result). Clears the row counts for the next pass.
 static __global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevState s, int H) {
+  pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < H) s.row_cnt[i] = 0;
   if (i >= m.V) return;
@@ -660,6 +695,7 @@ __device__ __forceinline__ void group_min(double& bx, int& bi) {
 }
 
 static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
+  pdl_entry();
   const int nv = *f.n_valid;
   const int w = a.window;
   const int K1 = min(kNearRings, w);
@@ -837,10 +873,10 @@ __device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b
 #pragma unroll
     for (int j = k + 1; j < N; ++j) {
       const double cj = __shfl_sync(0xffffffffu, a[k], j);  // A[j][k], unscaled
-      if (act && j <= lane) a[j] -= lik * cj;
+      if (act && j <= lane) a[j] = __fma_rn(-lik, cj, a[j]);  // explicit FMA (exact unit)
     }
     if (act) {
-      bi -= lik * zk;
+      bi = __fma_rn(-lik, zk, bi);
       a[k] = lik;
     }
   }
@@ -855,7 +891,7 @@ __device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b
   double yi = bi * __drcp_rn(dd);
   for (int k = L - 1; k >= 0; --k) {
     const double xk = __shfl_sync(0xffffffffu, yi, k);
-    if (lane < k) yi -= A[k * lda + lane] * xk;
+    if (lane < k) yi = __fma_rn(-A[k * lda + lane], xk, yi);
   }
   if (row) x[lane] = yi;
   __syncwarp();
@@ -905,6 +941,7 @@ __host__ __device__ inline int pose_tiles(int L) {
 // owned entries e = lane + 32 q (Q of them), any L <= 64.
 template <int Q, int TPL>
 static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
+  pdl_entry();
   extern __shared__ __align__(16) double psm[];
   const int L = m.L;
   const int Lr = (L + 1) | 1;  // row stride: L Jacobian entries + the residual, odd
@@ -1206,6 +1243,7 @@ __host__ __device__ inline size_t pose_solve_smem_bytes(int L) {
 }
 
 static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevState s, PoseArgs a) {
+  pdl_entry();
   __shared__ FkTables fkt;
   extern __shared__ __align__(16) double solve_sm[];  // pose_solve_smem_bytes(L)
   __shared__ double jtr[64];
@@ -1457,6 +1495,7 @@ struct ShapeArgs {
 
 static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState s, const double4* phi_in,
                                                      double4* phi_out, ShapeArgs a) {
+  pdl_entry();
   extern __shared__ double s_off[];
   load_offsets(m, s, s_off);
   __syncthreads();
@@ -1549,6 +1588,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
 // Closing measurement pass of optimize_shape (shapeopt.cpp:112-129): mean
 // |r| over observed vertices of a fresh association; fills mean_abs_r_after.
 static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, DevState s, int n_its) {
+  pdl_entry();
   double abs_r = 0.0;
   long long observed = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
