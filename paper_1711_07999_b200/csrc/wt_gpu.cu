@@ -118,6 +118,7 @@ struct wt_gpu_ctx {
   double4* phi_scratch = nullptr;
   int cur = 0;
   int frame_index = 0;
+  bool fk_valid = false;  // ds.fk / offsets / dchain are the FK of ds.theta (skips k_fk at frame start)
 
   // frame
   float* d_depth = nullptr;
@@ -303,7 +304,7 @@ void alloc_state(wt_gpu_ctx* c, wt::DevState& s, bool hook) {
     s.pv = c->mem.alloc<double4>(c->V);
     s.pn = c->mem.alloc<float4>(c->V);
     s.vpix = c->mem.alloc<int>(c->V);
-    s.vslot = c->mem.alloc<int>(c->V);
+    s.cursor = c->mem.alloc<int>(c->P);
     s.pix_cnt = c->mem.alloc<int>(c->P);
     s.row_cnt = c->mem.alloc<int>(c->din.H);
     s.poff = c->mem.alloc<int>(c->P + 1);
@@ -472,8 +473,8 @@ void enq_shape(wt_gpu_ctx* c, const wt_shape_config* sc, int it, const double4* 
 }
 
 // optimize_pose (kinopt.cpp:132-171) as a static kernel sequence.
-void enq_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* k, const wt_assoc_config* a) {
-  enq_fk(c, c->ds);
+void enq_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* k, const wt_assoc_config* a, bool need_fk) {
+  if (need_fk) enq_fk(c, c->ds);
   const int refresh = std::max(1, k->assoc_refresh);
   for (int it = 0; it < k->iterations; ++it) {
     enq_skin(c, c->ds, c->phi[c->cur]);
@@ -749,6 +750,18 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     uchar4* d_wl = c->mem.alloc<uchar4>(V);
     int* d_roff = c->mem.alloc<int>(V + 1);
     int2* d_ring = c->mem.alloc<int2>(ring.size());
+    // padded 8-slot copy of the ring for vertices with <= 8 incident triangles
+    std::vector<int2> ring8(static_cast<size_t>(V) * 8, make_int2(-1, -1));
+    for (int i = 0; i < V; ++i) {
+      const int n = ring_off[i + 1] - ring_off[i];
+      if (n > 8) {
+        ring8[static_cast<size_t>(i) * 8] = make_int2(-2, -2);
+        continue;
+      }
+      for (int q = 0; q < n; ++q) ring8[static_cast<size_t>(i) * 8 + q] = ring[ring_off[i] + q];
+    }
+    int2* d_ring8 = c->mem.alloc<int2>(ring8.size());
+    upload(d_ring8, ring8.data(), ring8.size(), c->stream);
     int* d_nbr = c->mem.alloc<int>(nbr.size());
     wt::LinkDesc* d_links = c->mem.alloc<wt::LinkDesc>(L);
     int* d_poff = c->mem.alloc<int>(L + 1);
@@ -783,7 +796,7 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     upload(d_plk, c->pair_link.data(), c->NP, c->stream);
     upload(d_pow, c->pair_owner.data(), c->NP, c->stream);
     upload(d_s, c->s_diag.data(), L, c->stream);
-    c->dm = wt::DevModel{V, L, c->NP, K, d_v0, d_wg, d_wl, d_roff, d_ring, d_nbr,
+    c->dm = wt::DevModel{V, L, c->NP, K, d_v0, d_wg, d_wl, d_roff, d_ring, d_ring8, d_nbr,
                          d_links, d_poff, d_pth, d_plk, d_pow, d_s, d_depth, max_depth, d_pe};
 
     alloc_state(c, c->ds, false);
@@ -838,7 +851,10 @@ int wt_gpu_set_state(wt_gpu_ctx* c, const double* theta, const double* phi, int3
   if (!c) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
-    if (theta) upload(c->ds.theta, theta, c->L, c->stream);
+    if (theta) {
+      upload(c->ds.theta, theta, c->L, c->stream);
+      c->fk_valid = false;
+    }
     if (phi) {
       std::vector<double4> ph(static_cast<size_t>(c->V));
       for (int i = 0; i < c->V; ++i) ph[i] = make_double4(phi[3 * i], phi[3 * i + 1], phi[3 * i + 2], 0.0);
@@ -921,13 +937,14 @@ int wt_gpu_track_loaded(wt_gpu_ctx* c, const wt_track_config* cfg, wt_frame_stat
                   static_cast<double>(cfg->assoc.window_radius), cfg->assoc.cutoff,
                   shape_now ? 1.0 : 0.0, static_cast<double>(cfg->shape.iterations),
                   cfg->shape.lambda_phi, cfg->shape.lambda_nbr, cfg->shape.lambda_w,
-                  cfg->shape.diag_floor, static_cast<double>(cfg->shape_stats), static_cast<double>(start)}};
+                  cfg->shape.diag_floor, static_cast<double>(cfg->shape_stats), static_cast<double>(start),
+                  c->fk_valid ? 0.0 : 1.0}};
+    const bool need_fk = !c->fk_valid;
     run_graph(c, key, [&] {
-      enq_optimize_pose(c, &cfg->kin, &cfg->assoc);
-      if (shape_now)
-        enq_optimize_shape(c, start, &cfg->shape, &cfg->assoc, cfg->shape_stats != 0,
-                           cfg->kin.iterations == 0);
+      enq_optimize_pose(c, &cfg->kin, &cfg->assoc, need_fk);
+      if (shape_now) enq_optimize_shape(c, start, &cfg->shape, &cfg->assoc, cfg->shape_stats != 0, false);
     });
+    c->fk_valid = true;
     c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
     const int nk = cfg->kin.iterations, ns = shape_now ? cfg->shape.iterations : 0;
     if (stats) {
@@ -956,13 +973,13 @@ GraphKey track_key(const wt_gpu_ctx* c, const wt_track_config* cfg, bool shape_n
                    static_cast<double>(cfg->assoc.window_radius), cfg->assoc.cutoff, shape_now ? 1.0 : 0.0,
                    static_cast<double>(cfg->shape.iterations), cfg->shape.lambda_phi, cfg->shape.lambda_nbr,
                    cfg->shape.lambda_w, cfg->shape.diag_floor, static_cast<double>(cfg->shape_stats),
-                   static_cast<double>(c->cur)}};
+                   static_cast<double>(c->cur), c->fk_valid ? 0.0 : 1.0}};
 }
 
+// one frame; FK of the current theta is recomputed first unless still valid
 void enq_track(wt_gpu_ctx* c, const wt_track_config* cfg, bool shape_now) {
-  enq_optimize_pose(c, &cfg->kin, &cfg->assoc);
-  if (shape_now)
-    enq_optimize_shape(c, c->cur, &cfg->shape, &cfg->assoc, cfg->shape_stats != 0, cfg->kin.iterations == 0);
+  enq_optimize_pose(c, &cfg->kin, &cfg->assoc, !c->fk_valid);
+  if (shape_now) enq_optimize_shape(c, c->cur, &cfg->shape, &cfg->assoc, cfg->shape_stats != 0, false);
 }
 }  // namespace
 
@@ -999,6 +1016,7 @@ int wt_gpu_track_async(wt_gpu_ctx* c, const wt_track_config* cfg) {
     ensure_stats(c, cfg->kin.iterations, cfg->shape.iterations);
     const int start = c->cur;
     run_graph(c, track_key(c, cfg, shape_now, 1.0), [&] { enq_track(c, cfg, shape_now); });
+    c->fk_valid = true;
     c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
     ++c->frame_index;
   });
@@ -1039,6 +1057,7 @@ int wt_gpu_profile_frame(wt_gpu_ctx* c, const wt_track_config* cfg, int32_t* kin
     WT_CUDA(cudaGraphLaunch(ex, c->stream));
     WT_CUDA(cudaStreamSynchronize(c->stream));
     cudaGraphExecDestroy(ex);
+    c->fk_valid = true;
     c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
     ++c->frame_index;
     const int n = static_cast<int>(c->prof_events.size());
@@ -1121,6 +1140,7 @@ int wt_gpu_track_sequence(wt_gpu_ctx* c, const float* frames, int32_t n_frames, 
                              (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
       const int start = c->cur;
       run_graph(c, track_key(c, cfg, shape_now, 1.0), [&] { enq_track(c, cfg, shape_now); });
+      c->fk_valid = true;
       c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
       ++c->frame_index;
       wt::k_record<<<1, 64, 0, c->stream>>>(c->dm, c->ds, rec_theta + static_cast<size_t>(f) * L,
@@ -1179,8 +1199,10 @@ int wt_gpu_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* kin, const wt_assoc
     GraphKey key{{2.0, static_cast<double>(kin->iterations), static_cast<double>(kin->assoc_refresh),
                   kin->lambda_k, kin->lambda_s, kin->diag_floor, static_cast<double>(kin->clamp_limits),
                   kin->limit, static_cast<double>(assoc->window_radius), assoc->cutoff,
-                  static_cast<double>(c->cur)}};
-    run_graph(c, key, [&] { enq_optimize_pose(c, kin, assoc); });
+                  static_cast<double>(c->cur), c->fk_valid ? 0.0 : 1.0}};
+    const bool need_fk = !c->fk_valid;
+    run_graph(c, key, [&] { enq_optimize_pose(c, kin, assoc, need_fk); });
+    c->fk_valid = true;
     const int nk = kin->iterations;
     if (nk) WT_CUDA(cudaMemcpyAsync(c->h_kin, c->ds.kin_stats, sizeof(wt::KinStat) * nk,
                                     cudaMemcpyDeviceToHost, c->stream));
@@ -1203,8 +1225,11 @@ int wt_gpu_optimize_shape(wt_gpu_ctx* c, const wt_shape_config* shape, const wt_
     const int start = c->cur;
     GraphKey key{{3.0, static_cast<double>(shape->iterations), shape->lambda_phi, shape->lambda_nbr,
                   shape->lambda_w, shape->diag_floor, static_cast<double>(assoc->window_radius),
-                  assoc->cutoff, static_cast<double>(with_stats_pass), static_cast<double>(start)}};
-    run_graph(c, key, [&] { enq_optimize_shape(c, start, shape, assoc, with_stats_pass != 0, true); });
+                  assoc->cutoff, static_cast<double>(with_stats_pass), static_cast<double>(start),
+                  c->fk_valid ? 0.0 : 1.0}};
+    const bool need_fk = !c->fk_valid;
+    run_graph(c, key, [&] { enq_optimize_shape(c, start, shape, assoc, with_stats_pass != 0, need_fk); });
+    c->fk_valid = true;
     c->cur = (shape->iterations % 2) ? start ^ 1 : start;
     const int ns = shape->iterations;
     if (ns) WT_CUDA(cudaMemcpyAsync(c->h_shape, c->ds.shape_stats, sizeof(wt::ShapeStat) * ns,
@@ -1270,6 +1295,7 @@ int wt_gpu_recon_error(wt_gpu_ctx* c, double* dist, int32_t* n_visible) {
       c->rc_dist = c->mem.alloc<double>(c->V);
     }
     enq_fk(c, c->ds);
+    c->fk_valid = true;
     enq_skin(c, c->ds, c->phi[c->cur]);
     wt::recon_launch(c->stream, c->dm, c->ds, c->din, c->T, c->r_tri, c->r_vpos, c->r_zbits, c->r_owner, c->d_valid,
                      c->d_pts_hi, c->rc_obs, c->rc_obs + c->P, c->rc_obs + 2 * static_cast<size_t>(c->P), c->rc_vis,

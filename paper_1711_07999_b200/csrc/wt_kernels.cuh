@@ -33,7 +33,9 @@ struct DevModel {
   const double4* wgt;      // skin weights, entry order kept (entry 0 = pivot)
   const uchar4* wlink;     // skin links, 0xFF = unused
   const int* ring_off;     // [V+1] incident triangles of each vertex (CSR order)
-  const int2* ring;        // (b,c): face cross = (v_b - v_i) x (v_c - v_i)
+  const int2* ring;        // (b,c) follow i in its triangle; bits 30-31 of b: position of i
+  const int2* ring8;       // [V*8] the same for vertices with <= 8 triangles, padded with x = -1;
+                           // x = -2 in slot 0: more than 8, use the CSR
   const int* nbr;          // [K][V] neighbour ELL, -1 padded
   const LinkDesc* links;   // [L]
   const int* pair_off;     // [L+1] dchain pairs of each link
@@ -72,7 +74,7 @@ struct DevState {
   double4* pv;        // posed vertices (x,y,z, blend ok), fp64
   float4* pn;         // normals (x,y,z, valid)
   int* vpix;          // bucket pixel (row-major) or -1
-  int* vslot;         // slot within the pixel's bucket
+  int* cursor;        // [P] k_scatter's fill position per pixel (set by k_pixoff)
   int* pix_cnt;       // [P] bucket sizes (self-cleaning: cleared by k_pixoff)
   int* row_cnt;       // [H] bucketed vertices per image row (cleared by k_scatter)
   int* poff;          // [P+1] row-major pixel offsets: the VertexBuckets CSR
@@ -422,22 +424,38 @@ static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState 
 __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* pv, int i, const double4& v,
                                               double& nx, double& ny, double& nz) {
   double ax = 0, ay = 0, az = 0;
-  const int r0 = m.ring_off[i], r1 = m.ring_off[i + 1];
+  // up to eight incident triangles straight from the padded table (no offset
+  // load first), else the CSR eight at a time; all gathers of a step in flight
+  const int4* r8 = reinterpret_cast<const int4*>(m.ring8 + 8 * static_cast<size_t>(i));
+  const int4 q01 = r8[0], q23 = r8[1], q45 = r8[2], q67 = r8[3];
+  const bool packed = q01.x != -2;
+  const int r0 = packed ? 0 : m.ring_off[i], r1 = packed ? 8 : m.ring_off[i + 1];
   for (int r = r0; r < r1; r += 8) {
-    // eight incident triangles per step (most vertices have <= 8): index
-    // loads, then all sixteen position gathers in flight
     int2 bc[8];
+    if (packed) {
+      bc[0] = make_int2(q01.x, q01.y);
+      bc[1] = make_int2(q01.z, q01.w);
+      bc[2] = make_int2(q23.x, q23.y);
+      bc[3] = make_int2(q23.z, q23.w);
+      bc[4] = make_int2(q45.x, q45.y);
+      bc[5] = make_int2(q45.z, q45.w);
+      bc[6] = make_int2(q67.x, q67.y);
+      bc[7] = make_int2(q67.z, q67.w);
+    } else {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(i, i);
+      for (int q = 0; q < 8; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(-1, -1);
+    }
+    const int nq = packed ? 8 : min(8, r1 - r);
     double4 pb[8], pc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      pb[q] = pv[bc[q].x & 0x3FFFFFFF];
-      pc[q] = pv[bc[q].y];
+      const bool ok = bc[q].x != -1;  // -1 / -2 are sentinels (position bits 3: never a real entry)
+      pb[q] = pv[ok ? (bc[q].x & 0x3FFFFFFF) : i];
+      pc[q] = pv[ok ? bc[q].y : i];
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      if (r + q >= r1) break;
+      if (q >= nq || bc[q].x == -1) break;
       // ring entry: b, c follow i cyclically; bits 30-31 of .x = position of i
       const int rot = static_cast<int>(static_cast<unsigned>(bc[q].x) >> 30);
       const double4& f0 = rot == 0 ? v : (rot == 1 ? pc[q] : pb[q]);
@@ -488,8 +506,9 @@ static __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevSta
       reinterpret_cast<ulonglong2*>(s.acc)[2 * i + 1] = make_ulonglong2(0ull, 0ull);
     }
     if (do_bucket) {
-      // bucket_occupancy (association.cpp:39-56): per-pixel slot and per-row
-      // count, both warp-aggregated
+      // bucket_occupancy (association.cpp:39-56): per-pixel and per-row
+      // counts as fire-and-forget reductions (no value comes back, so no
+      // round trip); the slot inside the pixel is taken later, in k_scatter
       int pix = -1, row = -1;
       if (valid && !(nx * vx + ny * vy + nz * vz > 0.0) && vz > 0.0) {
         const double pu = in.fx * vx / vz + in.cx;
@@ -500,21 +519,11 @@ static __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevSta
           pix = row * in.W + static_cast<int>(ru);
         }
       }
-      const unsigned act = __activemask();
-      const int lane = threadIdx.x & 31;
-      unsigned peers = __match_any_sync(act, pix);
-      int slot = 0;
       if (pix >= 0) {
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(&s.pix_cnt[pix], __popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        slot = base + __popc(peers & ((1u << lane) - 1u));
+        atomicAdd(&s.pix_cnt[pix], 1);
+        atomicAdd(&s.row_cnt[row], 1);
       }
-      peers = __match_any_sync(act, row);
-      if (row >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s.row_cnt[row], __popc(peers));
       s.vpix[i] = pix;
-      s.vslot[i] = slot;
     }
   }
 }
@@ -571,6 +580,7 @@ static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, 
     const int c = t * 32 + lane;
     if (c < W) {
       off[c] = run + incl - v[t];
+      s.cursor[row * W + c] = run + incl - v[t];
       cnt[c] = 0;
     }
     run += __shfl_sync(0xffffffffu, incl, 31);
@@ -587,9 +597,11 @@ static __global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevSta
   if (i < H) s.row_cnt[i] = 0;
   if (i >= m.V) return;
   const int pix = s.vpix[i];
-  if (pix < 0) return;
   const double4 v = s.pv[i];
-  s.items[s.poff[pix] + s.vslot[i]] = make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(i)));
+  if (pix < 0) return;
+  // k_pixoff left cursor[pix] = poff[pix]: the returned value is the slot
+  s.items[atomicAdd(&s.cursor[pix], 1)] =
+      make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(i)));
 }
 
 // ---------------------------------------------------------------------------

@@ -284,3 +284,21 @@ def test_reconstruction_error_matches_live_reference():
     want = ref.recon_error(rm, th, intr.c(), pts, val)
     assert np.array_equal(trk.reconstruction_error(), want)
     trk.close()
+
+
+def test_set_state_invalidates_cached_fk():
+    """The frame graph skips the leading FK while theta is unchanged since the
+    last solve; set_state must force it again."""
+    z, b, ci = load_golden("humanoid7k_320x240")
+    c = track_cfg("dynamic", 5, 2)
+    a = Tracker(b, pyintr(ci), z["theta0"])
+    a.track_frame(c, depth=z["depths"][2])
+    b2 = Tracker(b, pyintr(ci), z["theta0"])
+    b2.track_frame(c, depth=z["depths"][1])  # FK now cached for another theta
+    b2.set_state(z["theta0"], np.zeros((b.vertex_count, 3)), 0)
+    b2.track_frame(c, depth=z["depths"][2])
+    ta, pa, _ = a.get_state()
+    tb, pb, _ = b2.get_state()
+    assert np.array_equal(ta, tb) and np.array_equal(pa, pb)
+    a.close()
+    b2.close()
