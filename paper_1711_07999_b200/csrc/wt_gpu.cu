@@ -161,7 +161,6 @@ struct wt_gpu_ctx {
   int* hook_cnt = nullptr;
   double* hook_res = nullptr;
   long long* pose_dbg = nullptr;  // WT_DEBUG_POSE: last-CTA timing of the pose kernel
-  long long* search_dbg = nullptr;  // WT_DEBUG_SEARCH: per-CTA timing of the search kernel
 
   // profiling: when set during capture, an event is recorded after every
   // kernel so per-kernel device time inside the real frame graph is known
@@ -382,13 +381,6 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   sa.cut2 = a->cutoff * a->cutoff;
   sa.write_winners = winners ? 1 : 0;
   sa.winners = winners;
-  sa.dbg = c->search_dbg;
-  {
-    const char* ex = getenv("WT_SEARCH_EXPERIMENT");  // diagnostics only
-    const int bits = ex ? atoi(ex) : 0;
-    sa.no_acc = bits & 1;
-    sa.exp = bits;
-  }
   // 8 lanes per valid pixel; at most P pixels (the list is padded per 32 columns)
   const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, 16 * 148));
   WT_CUDA(wt::launch_pdl(wt::k_search, dim3(grid), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
@@ -817,7 +809,6 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     c->d_winners = c->mem.alloc<int>(c->P);
     ensure_stats(c, 16, 8);
     if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8 + 4 * 296 + 8);
-    if (getenv("WT_DEBUG_SEARCH")) c->search_dbg = c->mem.alloc<long long>(8 * 4096);  // unused by the current kernel
     if (wt::pose_smem_bytes(L, c->NP, pose_threads(c) / 32) > 227 * 1024)
       fail(WT_EINVAL, "skeleton too large for the pose kernel's shared memory");
     if (wt::pose_tiles(L) <= 32) {
@@ -984,14 +975,6 @@ void enq_track(wt_gpu_ctx* c, const wt_track_config* cfg, bool shape_now) {
 }  // namespace
 
 void* wt_gpu_stream(wt_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
-
-// Debug: per-CTA timing of the last search launch (needs WT_DEBUG_SEARCH at create).
-int wt_gpu_debug_search(wt_gpu_ctx* c, long long* out) {
-  if (!c || !c->search_dbg) return 0;
-  cudaMemcpy(out, c->search_dbg, sizeof(long long) * 8 * 4096, cudaMemcpyDeviceToHost);
-  cudaMemset(c->search_dbg, 0, sizeof(long long) * 8 * 4096);
-  return 1;
-}
 
 // Debug: last pose kernel's last-CTA timing (needs WT_DEBUG_POSE at create).
 int wt_gpu_debug_pose(wt_gpu_ctx* c, long long* out) {

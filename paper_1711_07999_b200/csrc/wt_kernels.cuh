@@ -17,7 +17,6 @@
 #include <cstdint>
 
 #include "wt_dq.cuh"
-#include "wt_tma.cuh"
 
 namespace wt {
 
@@ -632,9 +631,6 @@ struct SearchArgs {
   double cut2;  // cutoff^2 (association.cpp:75,98)
   int write_winners;
   int* winners;
-  long long* dbg;  // optional per-CTA timing (WT_DEBUG_SEARCH): start, phase-1 end, end, queue length
-  int no_acc;      // diagnostics only (WT_SEARCH_EXPERIMENT bit 0): skip the observation sums
-  int exp;         // diagnostics only: bit 1 skip phase 2, bit 2 skip the core scan
 };
 
 __device__ __forceinline__ double ring_lb2(int k, double atx, double aty, double ifx, double ify, double z) {
@@ -672,7 +668,7 @@ __device__ __forceinline__ void scan_span(const DevState& s, int e0, int e1, dou
 __device__ __forceinline__ void search_emit(const DevState& s, const SearchArgs& a, int pix, int best_i, double px,
                                             double py, double pz) {
   if (a.write_winners) a.winners[pix] = best_i;
-  if (best_i >= 0 && !a.no_acc) {
+  if (best_i >= 0) {
     unsigned long long* acc = s.acc + 4 * static_cast<size_t>(best_i);
     red_add(acc + 0, fix(px, kFixPoint));
     red_add(acc + 1, fix(py, kFixPoint));

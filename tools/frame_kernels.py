@@ -1,6 +1,4 @@
-"""Per-kernel in-graph times (events between kernels) of one C3 frame under
-WT_SEARCH_EXPERIMENT bits (diagnostics: 1 = no observation sums, 2 = no
-phase 2, 4 = no core scan)."""
+"""Per-kernel in-graph times (events between kernels) of a few C3 frames."""
 import ctypes as C
 import sys
 
