@@ -382,7 +382,8 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   sa.write_winners = winners ? 1 : 0;
   sa.winners = winners;
   // 8 lanes per valid pixel; at most P pixels (the list is padded per 32 columns)
-  const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, 16 * 148));
+  // one wave (5 CTAs per SM fit the registers); warps stride over the 4-pixel groups
+  const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, 5 * 148));
   WT_CUDA(wt::launch_pdl(wt::k_search, dim3(grid), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
   mark(c, K_SEARCH);
 }

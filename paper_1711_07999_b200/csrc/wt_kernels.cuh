@@ -338,11 +338,12 @@ static __global__ void k_fk(DevModel m, DevState s) { pdl_entry(); block_fk(m, s
 // ---------------------------------------------------------------------------
 // frame ingest: depth_to_cloud (seqio.cpp:419-437) in fp64 and the list of
 // valid pixels. CTAs cover 256-pixel segments of one image row; each warp
-// compacts the valid pixels of its 32 columns in image order into a run of
-// 32 list entries padded with -1, so a search warp always gets the valid
-// pixels of one 32-column row segment (a small, fixed search box).
+// compacts the valid pixels of its 32 columns in image order into a run
+// padded with -1 to a multiple of 4 entries, so the 4 pixels of a search
+// warp are row neighbours from at most two 32-column segments.
 
 constexpr int kIngestSeg = 256;
+constexpr int kRunAlign = 4;  // = pixels per search warp (32 / kSearchGroup)
 
 static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const float* depth, double scale,
                                                       const double* cloud, const uint8_t* cloud_valid,
@@ -381,11 +382,13 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
   const int lane = threadIdx.x & 31;
   const unsigned m = __ballot_sync(0xffffffffu, valid);
   if (m) {
+    // a run padded to a multiple of kRunAlign (the pixels of one search warp)
+    const int n = __popc(m), padded = (n + kRunAlign - 1) & ~(kRunAlign - 1);
     int base = 0;
-    if (lane == 0) base = atomicAdd(n_valid, 32);
+    if (lane == 0) base = atomicAdd(n_valid, padded);
     base = __shfl_sync(0xffffffffu, base, 0);
     if (valid) vlist[base + __popc(m & ((1u << lane) - 1u))] = i;
-    if (lane >= __popc(m)) vlist[base + lane] = -1;
+    if (lane >= n && lane < padded) vlist[base + lane] = -1;
   }
 }
 
