@@ -862,6 +862,15 @@ __device__ inline int block_ldlt_solve(int L, int lda, double* A, double* b, dou
 // substitution is fused into the elimination and the backward one reads the
 // unit-L factor written back to A (row stride lda). Returns 1 on success (x
 // written), 0 when a pivot is not strictly positive. Call from a full warp.
+//
+// The pivot loop is NOT unrolled: a fully unrolled N = 20 elimination is
+// ~10k straight-line instructions that run once per launch from a cold
+// instruction cache (ncu: stall_no_instruction dominated the solving warp,
+// 18k cycles). Instead each lane's register row is rotated by one after
+// every pivot so the pivot column is always a[0] and the body indexes
+// registers statically; it does N-1 (instead of N-1-k) shuffle/FMA pairs per
+// pivot but stays a few hundred instructions, resident after the first pass.
+// The arithmetic (operands and order of every FMA) is unchanged.
 template <int N>
 __device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b, double* x) {
   const int lane = threadIdx.x & 31;
@@ -872,34 +881,37 @@ __device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b
     a[j] = row ? (j < L ? A[lane * lda + j] : 0.0) : (j == lane ? 1.0 : 0.0);
   }
   double bi = row ? b[lane] : 0.0;
+  double dinv = 1.0;
   int ok = 1;
-#pragma unroll
+#pragma unroll 1
   for (int k = 0; k < N; ++k) {
-    const double dk = __shfl_sync(0xffffffffu, a[k], k);
+    // a[t] holds this lane's entry of column k + t
+    const double dk = __shfl_sync(0xffffffffu, a[0], k);
     ok &= dk > 0.0 ? 1 : 0;  // uniform; padded pivots are 1
     const double inv = __drcp_rn(dk);
     const double zk = __shfl_sync(0xffffffffu, bi, k);
     const bool act = lane > k;
-    const double lik = a[k] * inv;
+    const double lik = a[0] * inv;
+    if (lane == k) dinv = inv;
+    // Unpredicated: entries with k + t > lane (or lane <= k) are upper-
+    // triangle values no later pivot reads, so updating them is harmless;
+    // every entry that is read gets exactly the FMA the predicated form did.
+    double cj[N];
 #pragma unroll
-    for (int j = k + 1; j < N; ++j) {
-      const double cj = __shfl_sync(0xffffffffu, a[k], j);  // A[j][k], unscaled
-      if (act && j <= lane) a[j] = __fma_rn(-lik, cj, a[j]);  // explicit FMA (exact unit)
-    }
+    for (int t = 1; t < N; ++t) cj[t] = __shfl_sync(0xffffffffu, a[0], k + t);  // A[k+t][k], unscaled
+#pragma unroll
+    for (int t = 1; t < N; ++t) a[t] = __fma_rn(-lik, cj[t], a[t]);  // explicit FMA (exact unit)
     if (act) {
       bi = __fma_rn(-lik, zk, bi);
-      a[k] = lik;
+      if (row) A[lane * lda + k] = lik;
     }
+#pragma unroll
+    for (int t = 0; t + 1 < N; ++t) a[t] = a[t + 1];
+    a[N - 1] = 0.0;
   }
   if (!ok) return 0;
-  double dd = 1.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    if (row && j < lane) A[lane * lda + j] = a[j];
-    if (j == lane) dd = a[j];
-  }
   __syncwarp();
-  double yi = bi * __drcp_rn(dd);
+  double yi = bi * dinv;
   for (int k = L - 1; k >= 0; --k) {
     const double xk = __shfl_sync(0xffffffffu, yi, k);
     if (lane < k) yi = __fma_rn(-A[k * lda + lane], xk, yi);
