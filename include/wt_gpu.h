@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define WT_ABI_VERSION 1
+#define WT_ABI_VERSION 2
 
 enum {
   WT_OK = 0,
@@ -243,6 +243,31 @@ int wt_gpu_sync(wt_gpu_ctx* ctx);
  * 5 pose system+solve, 6 shape step, 7 shape stats pass. */
 int wt_gpu_profile_frame(wt_gpu_ctx* ctx, const wt_track_config* cfg, int32_t* kinds, float* ms,
                          int32_t cap, int32_t* n_out);
+
+/* ---- batched sequences --------------------------------------------------- */
+/* n_seq independent tracking sequences of ONE model, tracked in lockstep
+ * (run_tracking, tracker.cpp:73-90, for n_seq sequences at once): every
+ * frame kernel runs once for the whole batch, the sequence index in
+ * blockIdx.y, so a frame of the batch is one CUDA graph whatever n_seq is.
+ * Each sequence has its own TrackerState (theta, phi) and frame; the frame
+ * index and mode schedule are shared. The per-frame calls above return
+ * WT_EINVAL on a batch context; wt_gpu_set_state / wt_gpu_get_state act on
+ * sequence 0 and the shared frame index. */
+int wt_gpu_create_batch(int device, const wt_model_desc* model, const wt_intrinsics* intr, int32_t n_seq,
+                        wt_gpu_ctx** out);
+int32_t wt_gpu_batch_size(const wt_gpu_ctx* ctx);
+/* theta [L] / phi [V*3] of sequence seq (either may be NULL). */
+int wt_gpu_batch_set_state(wt_gpu_ctx* ctx, int32_t seq, const double* theta, const double* phi);
+int wt_gpu_batch_get_state(wt_gpu_ctx* ctx, int32_t seq, double* theta, double* phi);
+/* depth [n_seq][H][W] (host or device), one frame per sequence. */
+int wt_gpu_batch_load_depth(wt_gpu_ctx* ctx, const float* depth, double depth_scale);
+/* track_frame for every sequence on the loaded frames, without waiting. */
+int wt_gpu_batch_track_async(wt_gpu_ctx* ctx, const wt_track_config* cfg);
+/* stats[n_seq] of the last batch frame (waits for it). */
+int wt_gpu_batch_stats(wt_gpu_ctx* ctx, wt_frame_stats* stats);
+/* load + track + (stats may be NULL) + wait. */
+int wt_gpu_batch_track(wt_gpu_ctx* ctx, const float* depth, double depth_scale, const wt_track_config* cfg,
+                       wt_frame_stats* stats);
 
 /* ---- stage hooks (parity / tests) --------------------------------------- */
 /* skin(mesh, link_offsets(theta)) with phi override (NULL = state phi).

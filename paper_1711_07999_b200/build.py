@@ -21,6 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                  "-I", str(ROOT / "include"), "-I", str(CSRC), "--expt-relaxed-constexpr"]
+COMMON += os.environ.get("WT_NVCC_FLAGS", "").split()  # experiments only (e.g. -DWT_...)
 
 UNITS = [
     ("wt_gpu.cu", []),

@@ -15,21 +15,24 @@ namespace wt {
 void raster_launch(cudaStream_t st, int T, const double* vpos, const int* tri, double fx, double fy, double cx,
                    double cy, int W, int H, unsigned long long* zbits, int* owner);
 
-void launch_skin(cudaStream_t st, int grid, int L, const DevModel& m, const DevState& s, const double4* phi) {
-  launch_pdl(k_skin, dim3(grid), dim3(kVThreads), sizeof(double) * 8 * L, st, m, s, phi);
+// nseq: sequences of a batch (gridDim.y), see seq_state in wt_kernels.cuh
+void launch_skin(cudaStream_t st, int grid, int nseq, int L, const DevModel& m, const DevState& s,
+                 const double4* phi) {
+  launch_pdl(nseq > 1 ? k_skin<true> : k_skin<false>, dim3(grid, nseq), dim3(kVThreads), sizeof(double) * 8 * L, st,
+             m, s, phi);
 }
 
-void launch_normals(cudaStream_t st, int grid, const DevModel& m, const DevState& s, const DevIntr& in,
+void launch_normals(cudaStream_t st, int grid, int nseq, const DevModel& m, const DevState& s, const DevIntr& in,
                     int do_bucket, int zero_acc, int compute) {
-  launch_pdl(k_normals, dim3(grid), dim3(kVThreads), 0, st, m, s, in, do_bucket, zero_acc, compute);
+  launch_pdl(nseq > 1 ? k_normals<true> : k_normals<false>, dim3(grid, nseq), dim3(kVThreads), 0, st, m, s, in, do_bucket, zero_acc, compute);
 }
 
-void launch_fk(cudaStream_t st, const DevModel& m, const DevState& s) {
-  launch_pdl(k_fk, dim3(1), dim3(128), 0, st, m, s);
+void launch_fk(cudaStream_t st, int nseq, const DevModel& m, const DevState& s) {
+  launch_pdl(nseq > 1 ? k_fk<true> : k_fk<false>, dim3(1, nseq), dim3(128), 0, st, m, s);
 }
 
-void launch_pose_solve(cudaStream_t st, int L, const DevModel& m, const DevState& s, const PoseArgs& a) {
-  launch_pdl(k_pose_solve, dim3(1), dim3(256), pose_solve_smem_bytes(L), st, m, s, a);
+void launch_pose_solve(cudaStream_t st, int nseq, int L, const DevModel& m, const DevState& s, const PoseArgs& a) {
+  launch_pdl(nseq > 1 ? k_pose_solve<true> : k_pose_solve<false>, dim3(1, nseq), dim3(256), pose_solve_smem_bytes(L), st, m, s, a);
 }
 
 }  // namespace wt

@@ -21,14 +21,15 @@
 
 namespace wt {
 // wt_exact.cu (compiled without FMA contraction)
-void launch_skin(cudaStream_t st, int grid, int L, const DevModel& m, const DevState& s, const double4* phi);
-void launch_normals(cudaStream_t st, int grid, const DevModel& m, const DevState& s, const DevIntr& in,
+void launch_skin(cudaStream_t st, int grid, int nseq, int L, const DevModel& m, const DevState& s,
+                 const double4* phi);
+void launch_normals(cudaStream_t st, int grid, int nseq, const DevModel& m, const DevState& s, const DevIntr& in,
                     int do_bucket, int zero_acc, int compute);
-void launch_fk(cudaStream_t st, const DevModel& m, const DevState& s);
+void launch_fk(cudaStream_t st, int nseq, const DevModel& m, const DevState& s);
 void recon_launch(cudaStream_t st, const DevModel& m, const DevState& s, const DevIntr& in, int T, const int* tri,
                   double* v3, unsigned long long* zbits, int* owner, const uint8_t* pvalid, const double* pts,
                   double* ox, double* oy, double* oz, int* vis_list, int* counters, double* dist);
-void launch_pose_solve(cudaStream_t st, int L, const DevModel& m, const DevState& s, const PoseArgs& a);
+void launch_pose_solve(cudaStream_t st, int nseq, int L, const DevModel& m, const DevState& s, const PoseArgs& a);
 void render_launch(cudaStream_t st, int V, int L, int T, const double* offsets, const double* v0,
                    const double* phi, const double* wgt, const int* wlink, const int* wcount,
                    const int* tri, const int* dom, double fx, double fy, double cx, double cy,
@@ -117,6 +118,12 @@ struct wt_gpu_ctx {
   double4* phi[2] = {nullptr, nullptr};
   double4* phi_scratch = nullptr;
   int cur = 0;
+  // batch: nseq sequences in lockstep, each with its own arena of per-sequence
+  // buffers (ds, phi, frame, stats), bstride bytes apart (wt_kernels.cuh seq_state)
+  int nseq = 1;
+  long long bstride = 0;
+  void* arena = nullptr;
+  int last_nk = 0, last_ns = 0;  // iterations recorded by the last batch frame
   int frame_index = 0;
   bool fk_valid = false;  // ds.fk / offsets / dchain are the FK of ds.theta (skips k_fk at frame start)
 
@@ -191,6 +198,7 @@ struct wt_gpu_ctx {
     if (h_kin) cudaFreeHost(h_kin);
     if (h_shape) cudaFreeHost(h_shape);
     if (stream) cudaStreamDestroy(stream);
+    if (arena) cudaFree(arena);
   }
 };
 
@@ -233,6 +241,9 @@ void mark(wt_gpu_ctx* c, int kind) {
 }
 
 int vgrid(int n) { return std::max(1, (n + wt::kVThreads - 1) / wt::kVThreads); }
+
+// per-sequence CTAs of a one-wave grid of `ctas` CTAs shared by a batch
+int wave(const wt_gpu_ctx* c, int ctas) { return std::max(1, ctas / c->nseq); }
 
 // ---- validation (Skeleton::build, skeleton.cpp:7-50; bundle invariants) ----
 
@@ -294,34 +305,95 @@ void validate_model(const wt_model_desc* d) {
   }
 }
 
-void alloc_state(wt_gpu_ctx* c, wt::DevState& s, bool hook) {
+// stage-hook state: own theta / fk / offsets / dchain, sequence 0's per-vertex buffers
+void alloc_hook_state(wt_gpu_ctx* c, wt::DevState& s) {
   s.theta = c->mem.alloc<double>(c->L);
   s.fk = c->mem.alloc<double>(8 * c->L);
   s.offsets = c->mem.alloc<double>(8 * c->L);
   s.dchain = c->mem.alloc<double>(8 * std::max(1, c->NP));
-  if (!hook) {
-    s.pv = c->mem.alloc<double4>(c->V);
-    s.pn = c->mem.alloc<float4>(c->V);
-    s.vpix = c->mem.alloc<int>(c->V);
-    s.cursor = c->mem.alloc<int>(c->P);
-    s.pix_cnt = c->mem.alloc<int>(c->P);
-    s.row_cnt = c->mem.alloc<int>(c->din.H);
-    s.poff = c->mem.alloc<int>(c->P + 1);
-    s.items = c->mem.alloc<double4>(c->V);
-    s.acc = c->mem.alloc<unsigned long long>(4 * static_cast<size_t>(std::max(1, c->V)));
-    const int NE = wt::kRedCopies * (c->L * (c->L + 1) / 2 + c->L + 2) + 8;
-    s.red = c->mem.alloc<unsigned long long>(NE);
-    s.tickets = c->mem.alloc<unsigned>(8);
-    s.sys_out = c->mem.alloc<double>(c->L * c->L + c->L);
-    WT_CUDA(cudaMemsetAsync(s.pix_cnt, 0, sizeof(int) * c->P, c->stream));
-    WT_CUDA(cudaMemsetAsync(s.row_cnt, 0, sizeof(int) * c->din.H, c->stream));
-    WT_CUDA(cudaMemsetAsync(s.acc, 0, sizeof(unsigned long long) * 4 * std::max(1, c->V), c->stream));
-    WT_CUDA(cudaMemsetAsync(s.red, 0, sizeof(unsigned long long) * NE, c->stream));
-    WT_CUDA(cudaMemsetAsync(s.tickets, 0, sizeof(unsigned) * 8, c->stream));
+  s.bstride = 0;
+}
+
+// Bump allocator over one sequence's arena (a dry run with base = nullptr
+// only measures it).
+struct Carve {
+  char* base = nullptr;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~static_cast<size_t>(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += sizeof(T) * std::max<size_t>(n, 1);
+    return p;
   }
+};
+
+constexpr int kArenaKin = 64, kArenaShape = 32;  // stats slots per sequence arena
+
+// Every per-sequence buffer, in arena order. Zero-initialised arenas are a
+// valid initial state (theta = 0; the self-cleaning counters and slots 0).
+void layout_seq(wt_gpu_ctx* c, Carve& a) {
+  const int L = c->L, V = c->V, P = c->P, H = c->din.H;
+  wt::DevState& s = c->ds;
+  s.theta = a.take<double>(L);
+  s.fk = a.take<double>(8 * L);
+  s.offsets = a.take<double>(8 * L);
+  s.dchain = a.take<double>(8 * std::max(1, c->NP));
+  s.pv = a.take<double4>(V);
+  s.pn = a.take<float4>(V);
+  s.vpix = a.take<int>(V);
+  s.cursor = a.take<int>(P);
+  s.pix_cnt = a.take<int>(P);
+  s.row_cnt = a.take<int>(H);
+  s.poff = a.take<int>(P + 1);
+  s.items = a.take<double4>(V);
+  s.acc = a.take<unsigned long long>(4 * static_cast<size_t>(std::max(1, V)));
+  s.red = a.take<unsigned long long>(wt::kRedCopies * (L * (L + 1) / 2 + L + 2) + 8);
+  s.tickets = a.take<unsigned>(8);
+  s.sys_out = a.take<double>(L * L + L);
+  s.kin_stats = a.take<wt::KinStat>(kArenaKin);
+  s.shape_stats = a.take<wt::ShapeStat>(kArenaShape);
+  c->phi[0] = a.take<double4>(V);
+  c->phi[1] = a.take<double4>(V);
+  c->d_depth = a.take<float>(P);
+  c->d_valid = a.take<uint8_t>(P);
+  c->d_pts_hi = a.take<double>(3 * static_cast<size_t>(P));
+  // valid-pixel list: one run of 32 entries per 32-column row segment
+  c->d_vlist = a.take<int>(32 * H * ((c->din.W + 31) / 32));
+  c->d_nvalid = a.take<int>(1);
+  c->d_winners = a.take<int>(P);
+}
+
+void alloc_arenas(wt_gpu_ctx* c) {
+  Carve dry;
+  layout_seq(c, dry);
+  const size_t S = (dry.off + 4095) & ~static_cast<size_t>(4095);
+  WT_CUDA(cudaMalloc(&c->arena, S * static_cast<size_t>(c->nseq)));
+  WT_CUDA(cudaMemsetAsync(c->arena, 0, S * static_cast<size_t>(c->nseq), c->stream));
+  Carve real;
+  real.base = static_cast<char*>(c->arena);
+  layout_seq(c, real);
+  c->bstride = c->nseq > 1 ? static_cast<long long>(S) : 0;
+  c->ds.bstride = c->bstride;
+  c->cap_kin = kArenaKin;
+  c->cap_shape = kArenaShape;
+  WT_CUDA(cudaMallocHost(&c->h_kin, sizeof(wt::KinStat) * c->cap_kin * c->nseq));
+  WT_CUDA(cudaMallocHost(&c->h_shape, sizeof(wt::ShapeStat) * c->cap_shape * c->nseq));
+}
+
+template <class T>
+T* seq_at(T* p, const wt_gpu_ctx* c, int seq) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(p) + static_cast<long long>(seq) * c->bstride);
+}
+
+void require_single(const wt_gpu_ctx* c) {
+  if (c->nseq != 1) fail(WT_EINVAL, "not available on a batch context (use the wt_gpu_batch_* calls)");
 }
 
 void ensure_stats(wt_gpu_ctx* c, int nk, int ns) {
+  if ((nk > c->cap_kin || ns > c->cap_shape) && c->nseq > 1)
+    fail(WT_EINVAL, "a batch records at most " + std::to_string(kArenaKin) + " pose / " +
+                        std::to_string(kArenaShape) + " surface iterations per frame");
   if (nk > c->cap_kin) {
     c->cap_kin = std::max(nk, 16);
     c->ds.kin_stats = c->mem.alloc<wt::KinStat>(c->cap_kin);
@@ -343,32 +415,33 @@ void ensure_stats(wt_gpu_ctx* c, int nk, int ns) {
 // ---- kernel launch helpers (all on ctx->stream) ------------------------------
 
 void enq_fk(wt_gpu_ctx* c, const wt::DevState& s) {
-  wt::launch_fk(c->stream, c->dm, s);
+  wt::launch_fk(c->stream, c->nseq, c->dm, s);
   mark(c, K_FK);
 }
 
 void enq_skin(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi) {
-  wt::launch_skin(c->stream, vgrid(c->V), c->L, c->dm, s, phi);
+  wt::launch_skin(c->stream, vgrid(c->V), c->nseq, c->L, c->dm, s, phi);
   mark(c, K_SKIN);
 }
 
 void enq_normals(wt_gpu_ctx* c, const wt::DevState& s, bool bucket, bool zero_acc,
                  bool compute = true) {
-  wt::launch_normals(c->stream, vgrid(c->V), c->dm, s, c->din, bucket ? 1 : 0, zero_acc ? 1 : 0, compute ? 1 : 0);
+  wt::launch_normals(c->stream, vgrid(c->V), c->nseq, c->dm, s, c->din, bucket ? 1 : 0, zero_acc ? 1 : 0,
+                     compute ? 1 : 0);
   mark(c, K_NORMALS);
 }
 
 void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
-  WT_CUDA(wt::launch_pdl(wt::k_pixoff, dim3((c->din.H + 7) / 8), dim3(wt::kVThreads), 0, c->stream, s, c->din.W,
-                         c->din.H));
+  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_pixoff<true> : wt::k_pixoff<false>, dim3((c->din.H + 7) / 8, c->nseq), dim3(wt::kVThreads), 0, c->stream, s,
+                         c->din.W, c->din.H));
   mark(c, K_SCATTER);
-  WT_CUDA(wt::launch_pdl(wt::k_scatter, dim3(vgrid(std::max(c->V, c->din.H))), dim3(wt::kVThreads), 0, c->stream,
-                         c->dm, s, c->din.H));
+  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_scatter<true> : wt::k_scatter<false>, dim3(vgrid(std::max(c->V, c->din.H)), c->nseq), dim3(wt::kVThreads), 0,
+                         c->stream, c->dm, s, c->din.H));
   mark(c, K_SCATTER);
 }
 
 void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, int* winners) {
-  wt::DevFrame f{c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid};
+  wt::DevFrame f{c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid, c->bstride};
   wt::SearchArgs sa;
   sa.fx = c->din.fx;
   sa.fy = c->din.fy;
@@ -383,8 +456,9 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   sa.winners = winners;
   // 8 lanes per valid pixel; at most P pixels (the list is padded per 32 columns)
   // one wave (5 CTAs per SM fit the registers); warps stride over the 4-pixel groups
-  const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, 5 * 148));
-  WT_CUDA(wt::launch_pdl(wt::k_search, dim3(grid), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
+  // (a batch shares the wave between its sequences)
+  const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, wave(c, 5 * 148)));
+  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_search<true> : wt::k_search<false>, dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
   mark(c, K_SEARCH);
 }
 
@@ -400,7 +474,7 @@ int pose_threads(const wt_gpu_ctx*) { return 128; }
 
 int pose_grid(const wt_gpu_ctx* c) {
   const int warps = pose_threads(c) / 32;
-  return std::max(1, std::min((c->V + 32 * warps - 1) / (32 * warps), 4 * 148));
+  return std::max(1, std::min((c->V + 32 * warps - 1) / (32 * warps), wave(c, 4 * 148)));
 }
 
 // JtJ entries per lane (upper triangle + Jtr) held in registers
@@ -411,14 +485,15 @@ int pose_q(int L) {
 
 template <int Q, int TPL>
 void launch_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt::PoseArgs& pa) {
-  WT_CUDA(wt::launch_pdl(wt::k_pose_system<Q, TPL>, dim3(pose_grid(c)), dim3(pose_threads(c)),
+  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_pose_system<Q, TPL, true> : wt::k_pose_system<Q, TPL, false>, dim3(pose_grid(c), c->nseq), dim3(pose_threads(c)),
                          wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32), c->stream, c->dm, s, phi, pa));
 }
 
 template <int Q, int TPL>
 void pose_attr(wt_gpu_ctx* c) {
-  WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system<Q, TPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32))));
+  const int bytes = static_cast<int>(wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32));
+  WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system<Q, TPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system<Q, TPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt_kin_config* k,
@@ -446,11 +521,11 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
     }
   }
   mark(c, K_POSE);
-  wt::launch_pose_solve(c->stream, c->L, c->dm, s, pa);
+  wt::launch_pose_solve(c->stream, c->nseq, c->L, c->dm, s, pa);
   mark(c, K_POSE_SOLVE);
 }
 
-int shape_grid(const wt_gpu_ctx* c) { return std::max(1, std::min(vgrid(c->V), 4 * 148)); }
+int shape_grid(const wt_gpu_ctx* c) { return std::max(1, std::min(vgrid(c->V), wave(c, 4 * 148))); }
 
 void enq_shape(wt_gpu_ctx* c, const wt_shape_config* sc, int it, const double4* in, double4* out) {
   wt::ShapeArgs sa;
@@ -460,7 +535,7 @@ void enq_shape(wt_gpu_ctx* c, const wt_shape_config* sc, int it, const double4* 
   sa.diag_floor = sc->diag_floor;
   sa.iteration = it;
   sa.pad = 0;
-  WT_CUDA(wt::launch_pdl(wt::k_shape, dim3(shape_grid(c)), dim3(wt::kVThreads), sizeof(double) * 8 * c->L, c->stream,
+  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_shape<true> : wt::k_shape<false>, dim3(shape_grid(c), c->nseq), dim3(wt::kVThreads), sizeof(double) * 8 * c->L, c->stream,
                          c->dm, c->ds, in, out, sa));
   mark(c, K_SHAPE);
 }
@@ -494,7 +569,8 @@ int enq_optimize_shape(wt_gpu_ctx* c, int cur, const wt_shape_config* sc, const 
   if (stats_pass && sc->iterations > 0) {
     enq_skin(c, c->ds, c->phi[cur]);
     enq_associate(c, c->ds, a, nullptr);
-    WT_CUDA(wt::launch_pdl(wt::k_shape_after, dim3(shape_grid(c)), dim3(wt::kVThreads), 0, c->stream, c->dm, c->ds,
+    WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_shape_after<true> : wt::k_shape_after<false>, dim3(shape_grid(c), c->nseq), dim3(wt::kVThreads), 0, c->stream, c->dm,
+                           c->ds,
                            sc->iterations));
     mark(c, K_SHAPE_AFTER);
   }
@@ -532,25 +608,48 @@ void run_graph(wt_gpu_ctx* c, const GraphKey& key, const std::function<void()>& 
   WT_CUDA(cudaGraphLaunch(it->second, c->stream));
 }
 
-void put_kin(const wt_gpu_ctx* c, int n, wt_kin_iter_stats* out, int cap) {
+void put_kin(const wt_gpu_ctx* c, int n, wt_kin_iter_stats* out, int cap, int seq = 0) {
+  const wt::KinStat* h = c->h_kin + static_cast<size_t>(seq) * c->cap_kin;
   for (int k = 0; k < n && k < cap; ++k) {
     out[k].iteration = k;
-    out[k].associated = c->h_kin[k].associated;
-    out[k].residual_sum = c->h_kin[k].residual_sum;
-    out[k].step_norm = c->h_kin[k].step_norm;
-    out[k].solver_skipped = c->h_kin[k].skipped;
+    out[k].associated = h[k].associated;
+    out[k].residual_sum = h[k].residual_sum;
+    out[k].step_norm = h[k].step_norm;
+    out[k].solver_skipped = h[k].skipped;
     out[k].pad_ = 0;
   }
 }
 
-void put_shape(const wt_gpu_ctx* c, int n, wt_shape_iter_stats* out, int cap) {
+void put_shape(const wt_gpu_ctx* c, int n, wt_shape_iter_stats* out, int cap, int seq = 0) {
+  const wt::ShapeStat* h = c->h_shape + static_cast<size_t>(seq) * c->cap_shape;
   for (int k = 0; k < n && k < cap; ++k) {
     out[k].iteration = k;
-    out[k].singular = c->h_shape[k].singular;
-    out[k].mean_phi = c->h_shape[k].mean_phi;
-    out[k].max_phi = c->h_shape[k].max_phi;
-    out[k].mean_abs_r_before = c->h_shape[k].mean_abs_r_before;
-    out[k].mean_abs_r_after = c->h_shape[k].mean_abs_r_after;
+    out[k].singular = h[k].singular;
+    out[k].mean_phi = h[k].mean_phi;
+    out[k].max_phi = h[k].max_phi;
+    out[k].mean_abs_r_before = h[k].mean_abs_r_before;
+    out[k].mean_abs_r_after = h[k].mean_abs_r_after;
+  }
+}
+
+// rows of `width` bytes, one per sequence arena, to / from a packed host array
+void copy_from_seqs(const wt_gpu_ctx* c, void* dst, size_t dpitch, const void* src, size_t width) {
+  if (width == 0) return;
+  if (c->nseq == 1) {
+    WT_CUDA(cudaMemcpyAsync(dst, src, width, cudaMemcpyDefault, c->stream));
+  } else {
+    WT_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, static_cast<size_t>(c->bstride), width, c->nseq, cudaMemcpyDefault,
+                              c->stream));
+  }
+}
+
+void copy_to_seqs(const wt_gpu_ctx* c, void* dst, const void* src, size_t spitch, size_t width) {
+  if (width == 0) return;
+  if (c->nseq == 1) {
+    WT_CUDA(cudaMemcpyAsync(dst, src, width, cudaMemcpyDefault, c->stream));
+  } else {
+    WT_CUDA(cudaMemcpy2DAsync(dst, static_cast<size_t>(c->bstride), src, spitch, width, c->nseq, cudaMemcpyDefault,
+                              c->stream));
   }
 }
 
@@ -603,7 +702,10 @@ int wt_gpu_device_count(void) {
 const char* wt_gpu_global_last_error(void) { return g_err.c_str(); }
 const char* wt_gpu_last_error(const wt_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
-int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr, wt_gpu_ctx** out) {
+}  // extern "C"
+
+namespace {
+int create_ctx(int device, const wt_model_desc* d, const wt_intrinsics* intr, int nseq, wt_gpu_ctx** out) {
   if (!out) {
     g_err = "out is NULL";
     return WT_EINVAL;
@@ -611,6 +713,8 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
   *out = nullptr;
   auto* c = new wt_gpu_ctx();
   const int rc = guarded(nullptr, [&] {
+    if (nseq < 1 || nseq > 4096) fail(WT_EINVAL, "batch size must be in 1..4096");
+    c->nseq = nseq;
     validate_model(d);
     if (!intr || intr->width <= 0 || intr->height <= 0) fail(WT_EINVAL, "bad intrinsics");
     if (intr->width > 32 * wt::kRowChunks) fail(WT_EINVAL, "image rows wider than 2048 pixels are not supported");
@@ -792,23 +896,11 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
     c->dm = wt::DevModel{V, L, c->NP, K, d_v0, d_wg, d_wl, d_roff, d_ring, d_ring8, d_nbr,
                          d_links, d_poff, d_pth, d_plk, d_pow, d_s, d_depth, max_depth, d_pe};
 
-    alloc_state(c, c->ds, false);
-    c->hs = c->ds;  // hooks share the per-vertex buffers, own theta/fk/offsets/dchain
-    alloc_state(c, c->hs, true);
-    c->phi[0] = c->mem.alloc<double4>(V);
-    c->phi[1] = c->mem.alloc<double4>(V);
+    alloc_arenas(c);
+    c->hs = c->ds;  // hooks share sequence 0's per-vertex buffers, own theta/fk/offsets/dchain
+    alloc_hook_state(c, c->hs);
     c->phi_scratch = c->mem.alloc<double4>(V);
-    upload(c->phi[0], ph.data(), V, c->stream);
-    WT_CUDA(cudaMemsetAsync(c->ds.theta, 0, sizeof(double) * L, c->stream));
-
-    c->d_depth = c->mem.alloc<float>(c->P);
-    c->d_valid = c->mem.alloc<uint8_t>(c->P);
-    c->d_pts_hi = c->mem.alloc<double>(3 * static_cast<size_t>(c->P));
-    // valid-pixel list: one run of 32 entries per 32-column row segment
-    c->d_vlist = c->mem.alloc<int>(32 * c->din.H * ((c->din.W + 31) / 32));
-    c->d_nvalid = c->mem.alloc<int>(1);
-    c->d_winners = c->mem.alloc<int>(c->P);
-    ensure_stats(c, 16, 8);
+    for (int b = 0; b < c->nseq; ++b) upload(seq_at(c->phi[0], c, b), ph.data(), V, c->stream);
     if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8 + 4 * 296 + 8);
     if (wt::pose_smem_bytes(L, c->NP, pose_threads(c) / 32) > 227 * 1024)
       fail(WT_EINVAL, "skeleton too large for the pose kernel's shared memory");
@@ -831,6 +923,20 @@ int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr,
   *out = c;
   return WT_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int wt_gpu_create(int device, const wt_model_desc* d, const wt_intrinsics* intr, wt_gpu_ctx** out) {
+  return create_ctx(device, d, intr, 1, out);
+}
+
+int wt_gpu_create_batch(int device, const wt_model_desc* d, const wt_intrinsics* intr, int32_t n_seq,
+                        wt_gpu_ctx** out) {
+  return create_ctx(device, d, intr, n_seq, out);
+}
+
+int32_t wt_gpu_batch_size(const wt_gpu_ctx* c) { return c ? c->nseq : 0; }
 
 void wt_gpu_destroy(wt_gpu_ctx* ctx) {
   if (!ctx) return;
@@ -882,10 +988,12 @@ int wt_gpu_get_state(wt_gpu_ctx* c, double* theta, double* phi, int32_t* frame_i
 
 static void ingest(wt_gpu_ctx* c, const float* depth_dev, double scale, const double* cloud_dev,
                    const uint8_t* valid_dev) {
-  WT_CUDA(cudaMemsetAsync(c->d_nvalid, 0, sizeof(int), c->stream));
+  // batch: depth_dev / cloud_dev / valid_dev are the arena buffers (same stride)
+  if (c->nseq == 1) WT_CUDA(cudaMemsetAsync(c->d_nvalid, 0, sizeof(int), c->stream));
+  else WT_CUDA(cudaMemset2DAsync(c->d_nvalid, static_cast<size_t>(c->bstride), 0, sizeof(int), c->nseq, c->stream));
   const int segs = (c->din.W + wt::kIngestSeg - 1) / wt::kIngestSeg;
-  wt::k_ingest<<<segs * c->din.H, wt::kIngestSeg, 0, c->stream>>>(c->din, depth_dev, scale, cloud_dev, valid_dev,
-                                                                   c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid);
+  (c->nseq > 1 ? wt::k_ingest<true> : wt::k_ingest<false>)<<<dim3(segs * c->din.H, c->nseq), wt::kIngestSeg, 0, c->stream>>>(
+      c->din, depth_dev, scale, cloud_dev, valid_dev, c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid, c->bstride);
   check_launch();
 }
 
@@ -893,6 +1001,7 @@ int wt_gpu_load_depth(wt_gpu_ctx* c, const float* depth, double depth_scale) {
   if (!c || !depth) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     WT_CUDA(cudaMemcpyAsync(c->d_depth, depth, sizeof(float) * c->P, cudaMemcpyDefault, c->stream));
     ingest(c, c->d_depth, depth_scale, nullptr, nullptr);
     c->frame_loaded = true;
@@ -904,6 +1013,7 @@ int wt_gpu_load_cloud(wt_gpu_ctx* c, const double* points, const uint8_t* valid)
   if (!c || !points || !valid) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     WT_CUDA(cudaMemcpyAsync(c->d_pts_hi, points, sizeof(double) * 3 * c->P, cudaMemcpyDefault, c->stream));
     WT_CUDA(cudaMemcpyAsync(c->d_valid, valid, c->P, cudaMemcpyDefault, c->stream));
     ingest(c, nullptr, 1.0, c->d_pts_hi, c->d_valid);
@@ -916,6 +1026,7 @@ int wt_gpu_track_loaded(wt_gpu_ctx* c, const wt_track_config* cfg, wt_frame_stat
   if (!c || !cfg) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     require_frame(c);
     check_assoc(&cfg->assoc);
     if (cfg->kin.iterations < 0 || cfg->shape.iterations < 0) fail(WT_EINVAL, "negative iteration count");
@@ -993,6 +1104,7 @@ int wt_gpu_track_async(wt_gpu_ctx* c, const wt_track_config* cfg) {
   if (!c || !cfg) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     require_frame(c);
     check_assoc(&cfg->assoc);
     const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
@@ -1011,6 +1123,7 @@ int wt_gpu_profile_frame(wt_gpu_ctx* c, const wt_track_config* cfg, int32_t* kin
   if (!c || !cfg) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     require_frame(c);
     check_assoc(&cfg->assoc);
     const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
@@ -1090,6 +1203,7 @@ int wt_gpu_track_sequence(wt_gpu_ctx* c, const float* frames, int32_t n_frames, 
   if (!c || !cfg || (n_frames > 0 && !frames) || n_frames < 0) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     check_assoc(&cfg->assoc);
     if (cfg->kin.iterations < 0 || cfg->shape.iterations < 0) fail(WT_EINVAL, "negative iteration count");
     if (n_frames == 0) return;
@@ -1145,10 +1259,11 @@ int wt_gpu_joint_positions(wt_gpu_ctx* c, double* joints_out) {
   if (!c || !joints_out) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     ensure_seq(c, 1);
     // FK of the current theta into the hook state, then the origins
     WT_CUDA(cudaMemcpyAsync(c->hs.theta, c->ds.theta, sizeof(double) * c->L, cudaMemcpyDeviceToDevice, c->stream));
-    wt::launch_fk(c->stream, c->dm, c->hs);
+    wt::launch_fk(c->stream, 1, c->dm, c->hs);
     wt::k_record<<<1, 64, 0, c->stream>>>(c->dm, c->hs, nullptr, c->rec_buf);
     check_launch();
     WT_CUDA(cudaMemcpyAsync(joints_out, c->rec_buf, sizeof(double) * c->L * 3, cudaMemcpyDeviceToHost,
@@ -1176,6 +1291,7 @@ int wt_gpu_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* kin, const wt_assoc
   if (!c || !kin) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     require_frame(c);
     check_assoc(assoc);
     if (kin->iterations < 0) fail(WT_EINVAL, "negative iteration count");
@@ -1202,6 +1318,7 @@ int wt_gpu_optimize_shape(wt_gpu_ctx* c, const wt_shape_config* shape, const wt_
   if (!c || !shape) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     require_frame(c);
     check_assoc(assoc);
     if (shape->iterations < 0) fail(WT_EINVAL, "negative iteration count");
@@ -1231,6 +1348,7 @@ int wt_gpu_skin(wt_gpu_ctx* c, const double* theta, const double* phi, double* v
   if (!c || !theta) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     upload(c->hs.theta, theta, c->L, c->stream);
     const double4* ph = c->phi[c->cur];
     if (phi) {
@@ -1270,6 +1388,7 @@ int wt_gpu_recon_error(wt_gpu_ctx* c, double* dist, int32_t* n_visible) {
   if (!c || !dist) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     require_frame(c);
     ensure_render(c);
     if (!c->rc_obs) {
@@ -1334,6 +1453,7 @@ int wt_gpu_associate(wt_gpu_ctx* c, int32_t window_radius, double cutoff, int32_
   if (!c) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     require_frame(c);
     wt_assoc_config a{window_radius, 0, cutoff};
     check_assoc(&a);
@@ -1414,6 +1534,7 @@ int wt_gpu_normal_system(wt_gpu_ctx* c, const double* theta, const wt_kin_config
   if (!c || !theta || !kin || !count || !residual) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
+    require_single(c);
     const int V = c->V, L = c->L;
     if (!c->hook_cnt) {
       c->hook_cnt = c->mem.alloc<int>(V);
@@ -1492,6 +1613,112 @@ int wt_gpu_solve_vertices(int device, int32_t n, const double* dr_dphi, const do
     WT_CUDA(cudaMemcpy(delta, d_delta, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
     WT_CUDA(cudaMemcpy(singular, d_sing, n, cudaMemcpyDeviceToHost));
   });
+}
+
+// ---- batched sequences (C5) -------------------------------------------------------
+// n_seq independent sequences of one model, tracked in lockstep: every frame
+// kernel runs once for the whole batch with the sequence in blockIdx.y.
+
+int wt_gpu_batch_set_state(wt_gpu_ctx* c, int32_t seq, const double* theta, const double* phi) {
+  if (!c) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    if (seq < 0 || seq >= c->nseq) fail(WT_EINVAL, "sequence index out of range");
+    if (theta) {
+      upload(seq_at(c->ds.theta, c, seq), theta, c->L, c->stream);
+      c->fk_valid = false;
+    }
+    if (phi) {
+      std::vector<double4> ph(static_cast<size_t>(c->V));
+      for (int i = 0; i < c->V; ++i) ph[i] = make_double4(phi[3 * i], phi[3 * i + 1], phi[3 * i + 2], 0.0);
+      upload(seq_at(c->phi[c->cur], c, seq), ph.data(), c->V, c->stream);
+    }
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int wt_gpu_batch_get_state(wt_gpu_ctx* c, int32_t seq, double* theta, double* phi) {
+  if (!c) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    if (seq < 0 || seq >= c->nseq) fail(WT_EINVAL, "sequence index out of range");
+    if (theta)
+      WT_CUDA(cudaMemcpyAsync(theta, seq_at(c->ds.theta, c, seq), sizeof(double) * c->L, cudaMemcpyDeviceToHost,
+                              c->stream));
+    std::vector<double4> ph;
+    if (phi) {
+      ph.resize(static_cast<size_t>(c->V));
+      WT_CUDA(cudaMemcpyAsync(ph.data(), seq_at(c->phi[c->cur], c, seq), sizeof(double4) * c->V,
+                              cudaMemcpyDeviceToHost, c->stream));
+    }
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < ph.size(); ++i) {
+      phi[3 * i] = ph[i].x;
+      phi[3 * i + 1] = ph[i].y;
+      phi[3 * i + 2] = ph[i].z;
+    }
+  });
+}
+
+int wt_gpu_batch_load_depth(wt_gpu_ctx* c, const float* depth, double depth_scale) {
+  if (!c || !depth) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    const size_t row = sizeof(float) * static_cast<size_t>(c->P);
+    copy_to_seqs(c, c->d_depth, depth, row, row);
+    ingest(c, c->d_depth, depth_scale, nullptr, nullptr);
+    c->frame_loaded = true;
+    c->frame_on_rays = true;
+  });
+}
+
+int wt_gpu_batch_track_async(wt_gpu_ctx* c, const wt_track_config* cfg) {
+  if (!c || !cfg) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    require_frame(c);
+    check_assoc(&cfg->assoc);
+    if (cfg->kin.iterations < 0 || cfg->shape.iterations < 0) fail(WT_EINVAL, "negative iteration count");
+    const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
+                           (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
+    ensure_stats(c, cfg->kin.iterations, cfg->shape.iterations);
+    const int start = c->cur;
+    run_graph(c, track_key(c, cfg, shape_now, 1.0), [&] { enq_track(c, cfg, shape_now); });
+    c->fk_valid = true;
+    c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
+    c->last_nk = cfg->kin.iterations;
+    c->last_ns = shape_now ? cfg->shape.iterations : 0;
+    ++c->frame_index;
+  });
+}
+
+int wt_gpu_batch_stats(wt_gpu_ctx* c, wt_frame_stats* stats) {
+  if (!c || !stats) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    const int nk = c->last_nk, ns = c->last_ns;
+    copy_from_seqs(c, c->h_kin, sizeof(wt::KinStat) * c->cap_kin, c->ds.kin_stats, sizeof(wt::KinStat) * nk);
+    copy_from_seqs(c, c->h_shape, sizeof(wt::ShapeStat) * c->cap_shape, c->ds.shape_stats,
+                   sizeof(wt::ShapeStat) * ns);
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+    for (int b = 0; b < c->nseq; ++b) {
+      wt_frame_stats& st = stats[b];
+      st.frame = c->frame_index - 1;
+      st.n_kin = nk;
+      st.n_shape = ns;
+      if (st.kin) put_kin(c, nk, st.kin, st.cap_kin, b);
+      if (st.shape) put_shape(c, ns, st.shape, st.cap_shape, b);
+    }
+  });
+}
+
+int wt_gpu_batch_track(wt_gpu_ctx* c, const float* depth, double depth_scale, const wt_track_config* cfg,
+                       wt_frame_stats* stats) {
+  int rc = wt_gpu_batch_load_depth(c, depth, depth_scale);
+  if (rc == WT_OK) rc = wt_gpu_batch_track_async(c, cfg);
+  if (rc == WT_OK && stats) rc = wt_gpu_batch_stats(c, stats);
+  if (rc == WT_OK) rc = wt_gpu_sync(c);
+  return rc;
 }
 
 int wt_gpu_render_depth(wt_gpu_ctx* c, const double* theta, const double* phi, const wt_noise* noise,

@@ -84,6 +84,7 @@ struct DevState {
   KinStat* kin_stats;
   ShapeStat* shape_stats;
   double* sys_out;           // optional JtJ/Jtr dump [L*L + L]
+  long long bstride;         // bytes between the arenas of consecutive sequences of a batch
 };
 
 struct DevFrame {
@@ -91,7 +92,60 @@ struct DevFrame {
   const double* pts_hi;  // per pixel fp64 point (valid pixels only)
   const int* vlist;      // valid pixel indices
   const int* n_valid;
+  long long bstride;
 };
+
+// ---------------------------------------------------------------------------
+// Batched sequences. Every per-sequence buffer (state, phi, frame) of a
+// batch of B independent sequences lives in one arena per sequence, all
+// arenas the same layout and `bstride` bytes apart, so sequence b's buffers
+// are sequence 0's pointers + b * bstride. A batched launch puts the
+// sequence in blockIdx.y (gridDim.y = B) and every frame kernel rebases its
+// pointers on entry; the model (DevModel) is shared. Every frame kernel is
+// instantiated twice: B = false (one sequence, no rebasing -- the pointers
+// stay in the constant bank) and B = true (batched launches).
+template <class T>
+__device__ __forceinline__ T* seq_ptr(T* p, long long off) {
+  return p ? reinterpret_cast<T*>(reinterpret_cast<unsigned long long>(p) + off) : p;
+}
+
+__device__ __forceinline__ long long seq_off(long long bstride) {
+  return static_cast<long long>(blockIdx.y) * bstride;
+}
+
+__device__ inline DevState seq_state(DevState s) {
+  const long long o = seq_off(s.bstride);
+  if (o == 0) return s;
+  s.theta = seq_ptr(s.theta, o);
+  s.fk = seq_ptr(s.fk, o);
+  s.offsets = seq_ptr(s.offsets, o);
+  s.dchain = seq_ptr(s.dchain, o);
+  s.pv = seq_ptr(s.pv, o);
+  s.pn = seq_ptr(s.pn, o);
+  s.vpix = seq_ptr(s.vpix, o);
+  s.cursor = seq_ptr(s.cursor, o);
+  s.pix_cnt = seq_ptr(s.pix_cnt, o);
+  s.row_cnt = seq_ptr(s.row_cnt, o);
+  s.poff = seq_ptr(s.poff, o);
+  s.items = seq_ptr(s.items, o);
+  s.acc = seq_ptr(s.acc, o);
+  s.red = seq_ptr(s.red, o);
+  s.tickets = seq_ptr(s.tickets, o);
+  s.kin_stats = seq_ptr(s.kin_stats, o);
+  s.shape_stats = seq_ptr(s.shape_stats, o);
+  s.sys_out = seq_ptr(s.sys_out, o);
+  return s;
+}
+
+__device__ inline DevFrame seq_frame(DevFrame f) {
+  const long long o = seq_off(f.bstride);
+  if (o == 0) return f;
+  f.valid = seq_ptr(f.valid, o);
+  f.pts_hi = seq_ptr(f.pts_hi, o);
+  f.vlist = seq_ptr(f.vlist, o);
+  f.n_valid = seq_ptr(f.n_valid, o);
+  return f;
+}
 
 // ---------------------------------------------------------------------------
 // Programmatic dependent launch: the frame graph's kernels are launched with
@@ -144,7 +198,7 @@ __device__ __forceinline__ bool last_block(unsigned* ticket) {
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned t = atomicAdd(ticket, 1u);
-    is_last = (t == gridDim.x * gridDim.y - 1);
+    is_last = (t == gridDim.x - 1);  // per sequence (blockIdx.y)
     if (is_last) *ticket = 0u;
   }
   __syncthreads();
@@ -332,7 +386,12 @@ __device__ inline void block_fk(const DevModel& m, const DevState& s, const doub
   fk_run(m, s, theta_in, t);
 }
 
-static __global__ void k_fk(DevModel m, DevState s) { pdl_entry(); block_fk(m, s, s.theta); }
+template <bool B>
+static __global__ void k_fk(DevModel m, DevState s) {
+  pdl_entry();
+  if constexpr (B) s = seq_state(s);
+  block_fk(m, s, s.theta);
+}
 
 
 // ---------------------------------------------------------------------------
@@ -345,10 +404,21 @@ static __global__ void k_fk(DevModel m, DevState s) { pdl_entry(); block_fk(m, s
 constexpr int kIngestSeg = 256;
 constexpr int kRunAlign = 4;  // = pixels per search warp (32 / kSearchGroup)
 
+template <bool B>
 static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const float* depth, double scale,
                                                       const double* cloud, const uint8_t* cloud_valid,
                                                       uint8_t* pvalid, double* pts_hi, int* vlist,
-                                                      int* n_valid) {
+                                                      int* n_valid, long long bstride) {
+  if constexpr (B) {  // sequence blockIdx.y of a batch (see seq_state)
+    const long long o = seq_off(bstride);
+    depth = seq_ptr(depth, o);
+    cloud = seq_ptr(cloud, o);
+    cloud_valid = seq_ptr(cloud_valid, o);
+    pvalid = seq_ptr(pvalid, o);
+    pts_hi = seq_ptr(pts_hi, o);
+    vlist = seq_ptr(vlist, o);
+    n_valid = seq_ptr(n_valid, o);
+  }
   const int segs = (in.W + kIngestSeg - 1) / kIngestSeg;
   const int v = blockIdx.x / segs;
   const int u = (blockIdx.x % segs) * kIngestSeg + threadIdx.x;
@@ -396,8 +466,11 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
 // ---------------------------------------------------------------------------
 // K1 skinning: v = normalize(blend)(v0 + phi) (skinmesh.cpp:112-121).
 
+template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, const double4* phi) {
   pdl_entry();
+  if constexpr (B) s = seq_state(s);
+  if constexpr (B) phi = seq_ptr(phi, seq_off(s.bstride));
   extern __shared__ double s_off[];
   load_offsets(m, s, s_off);
   __syncthreads();
@@ -483,9 +556,11 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
 // K2 normals (skinmesh.cpp:125-139) fused with K3a: back-face cull, projection
 // with lround semantics (association.cpp:29-37,49-51) and the bin histogram.
 
+template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, DevIntr in,
                                                        int do_bucket, int zero_acc, int compute) {
   pdl_entry();
+  if constexpr (B) s = seq_state(s);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m.V) {
     const double4 v = s.pv[i];
@@ -538,8 +613,10 @@ static __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevSta
 
 constexpr int kRowChunks = 64;  // rows up to 2048 pixels
 
+template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, int H) {
   pdl_entry();
+  if constexpr (B) s = seq_state(s);
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= H) return;
@@ -593,8 +670,10 @@ static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, 
 // K3c: scatter into pixel order (association.cpp:60-66; unordered within a
 // pixel -- the winner rule is a lexicographic (d^2, index) minimum, so bucket
 // order never changes a result). Clears the row counts for the next pass.
+template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevState s, int H) {
   pdl_entry();
+  if constexpr (B) s = seq_state(s);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < H) s.row_cnt[i] = 0;
   if (i >= m.V) return;
@@ -705,8 +784,12 @@ __device__ __forceinline__ void group_min(double& bx, int& bi) {
   }
 }
 
+template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
   pdl_entry();
+  if constexpr (B) s = seq_state(s);
+  if constexpr (B) f = seq_frame(f);
+  if constexpr (B) a.winners = seq_ptr(a.winners, seq_off(s.bstride));
   const int nv = *f.n_valid;
   const int w = a.window;
   const int K1 = min(kNearRings, w);
@@ -962,9 +1045,11 @@ __host__ __device__ inline int pose_tiles(int L) {
 // TPL = 1: every lane owns one 4x4 tile of [JtJ | Jtr] (needs pose_tiles(L)
 // <= 32, i.e. L <= 27): per row 8 shared loads feed 16 FMAs. TPL = 0: lane-
 // owned entries e = lane + 32 q (Q of them), any L <= 64.
-template <int Q, int TPL>
+template <int Q, int TPL, bool B>
 static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
   pdl_entry();
+  if constexpr (B) s = seq_state(s);
+  if constexpr (B) phi = seq_ptr(phi, seq_off(s.bstride));
   extern __shared__ __align__(16) double psm[];
   const int L = m.L;
   const int Lr = (L + 1) | 1;  // row stride: L Jacobian entries + the residual, odd
@@ -1265,8 +1350,10 @@ __host__ __device__ inline size_t pose_solve_smem_bytes(int L) {
   return sizeof(double) * L * (L | 1) + sizeof(unsigned short) * 2 * NE + 16;
 }
 
+template <bool B>
 static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevState s, PoseArgs a) {
   pdl_entry();
+  if constexpr (B) s = seq_state(s);
   __shared__ FkTables fkt;
   extern __shared__ __align__(16) double solve_sm[];  // pose_solve_smem_bytes(L)
   __shared__ double jtr[64];
@@ -1516,9 +1603,13 @@ struct ShapeArgs {
   int pad;
 };
 
+template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState s, const double4* phi_in,
                                                      double4* phi_out, ShapeArgs a) {
   pdl_entry();
+  if constexpr (B) s = seq_state(s);
+  if constexpr (B) phi_in = seq_ptr(phi_in, seq_off(s.bstride));
+  if constexpr (B) phi_out = seq_ptr(phi_out, seq_off(s.bstride));
   extern __shared__ double s_off[];
   load_offsets(m, s, s_off);
   __syncthreads();
@@ -1610,8 +1701,10 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
 
 // Closing measurement pass of optimize_shape (shapeopt.cpp:112-129): mean
 // |r| over observed vertices of a fresh association; fills mean_abs_r_after.
+template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, DevState s, int n_its) {
   pdl_entry();
+  if constexpr (B) s = seq_state(s);
   double abs_r = 0.0;
   long long observed = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {

@@ -329,6 +329,97 @@ class Tracker:
         return depth, vis
 
 
+class BatchTracker:
+    """B independent tracking sequences of one model, tracked in lockstep on
+    one GPU (run_tracking, tracker.cpp:70-100, for B sequences at once).
+
+    Each sequence has its own TrackerState (theta, Phi) and frame; a frame of
+    the whole batch is one CUDA graph whose kernels carry the sequence index
+    in blockIdx.y, so every launch covers B x the per-vertex / per-pixel
+    work. The frame index and mode schedule are shared."""
+
+    def __init__(self, bundle: ModelBundle, intr: Intrinsics, n_seq: int, init_theta=None,
+                 device: int = 0):
+        self.bundle = bundle
+        self.intr = intr
+        self.n_seq = n_seq
+        self._ctx = C.c_void_p()
+        desc, keep = bundle.to_desc()
+        check(lib().wt_gpu_create_batch(device, C.byref(desc), C.byref(intr.c()), n_seq,
+                                        C.byref(self._ctx)))
+        del keep
+        if init_theta is not None:
+            th = np.asarray(init_theta, dtype=np.float64)
+            for b in range(n_seq):
+                self.set_state(b, theta=th if th.ndim == 1 else th[b])
+        self._kin = [(_lib.KinIterStats * 64)() for _ in range(n_seq)]
+        self._shape = [(_lib.ShapeIterStats * 32)() for _ in range(n_seq)]
+
+    def close(self) -> None:
+        if self._ctx:
+            lib().wt_gpu_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_state(self, seq: int, theta=None, phi=None) -> None:
+        th = None if theta is None else _f64(theta, (self.bundle.link_count,))
+        ph = None if phi is None else _f64(phi, (self.bundle.vertex_count, 3))
+        check(lib().wt_gpu_batch_set_state(self._ctx, seq, ptr(th), ptr(ph)), self._ctx)
+
+    def get_state(self, seq: int, with_phi: bool = True):
+        th = np.zeros(self.bundle.link_count)
+        ph = np.zeros((self.bundle.vertex_count, 3)) if with_phi else None
+        check(lib().wt_gpu_batch_get_state(self._ctx, seq, ptr(th), ptr(ph)), self._ctx)
+        return th, ph
+
+    def thetas(self) -> np.ndarray:
+        return np.stack([self.get_state(b, with_phi=False)[0] for b in range(self.n_seq)])
+
+    def load_depth(self, depth, depth_scale: float = 1.0) -> None:
+        """depth [B, H, W] (host array) or (device address,) of the same layout."""
+        if isinstance(depth, tuple):
+            addr = depth[0]
+        else:
+            d = np.ascontiguousarray(depth, dtype=np.float32)
+            if d.size != self.n_seq * self.intr.width * self.intr.height:
+                raise _lib.LengthMismatch(_lib.WT_ELENGTH, "depth batch differs from B x intrinsics grid")
+            addr = ptr(d)
+        check(lib().wt_gpu_batch_load_depth(self._ctx, addr, depth_scale), self._ctx)
+
+    def track_async(self, cfg: TrackConfig) -> None:
+        check(lib().wt_gpu_batch_track_async(self._ctx, C.byref(cfg.c())), self._ctx)
+
+    def sync(self) -> None:
+        check(lib().wt_gpu_sync(self._ctx), self._ctx)
+
+    def stats(self) -> list:
+        arr = (_lib.FrameStatsC * self.n_seq)()
+        for b in range(self.n_seq):
+            arr[b] = _lib.FrameStatsC(0, 0, 0, 64, 32, 0, self._kin[b], self._shape[b])
+        check(lib().wt_gpu_batch_stats(self._ctx, arr), self._ctx)
+        return [FrameStats(arr[b].frame, _kin_list(self._kin[b], arr[b].n_kin),
+                           _shape_list(self._shape[b], arr[b].n_shape)) for b in range(self.n_seq)]
+
+    def track_frame(self, cfg: TrackConfig, depth=None, depth_scale: float = 1.0,
+                    stats: bool = True) -> list | None:
+        """track_frame (tracker.cpp:54-68) of every sequence on its own frame."""
+        if depth is not None:
+            self.load_depth(depth, depth_scale)
+        self.track_async(cfg)
+        out = self.stats() if stats else None
+        self.sync()
+        return out
+
+    @property
+    def stream(self) -> int:
+        return lib().wt_gpu_stream(self._ctx) or 0
+
+
 # ---- context-free stage functions ------------------------------------------------
 
 def solve_step(jtj, jtr, cfg: KinSolverConfig, device: int = 0) -> np.ndarray:
