@@ -1123,7 +1123,6 @@ int wt_gpu_profile_frame(wt_gpu_ctx* c, const wt_track_config* cfg, int32_t* kin
   if (!c || !cfg) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
-    require_single(c);
     require_frame(c);
     check_assoc(&cfg->assoc);
     const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||

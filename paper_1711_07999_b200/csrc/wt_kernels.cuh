@@ -496,6 +496,14 @@ static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState 
 // triangle (f0, f1, f2) in CSR order, acc += (v1 - v0) x (v2 - v0), then
 // acc / |acc|; returns the PosedMesh valid flag (blend ok and |acc| > 1e-20).
 // Bitwise the reference's when compiled without FMA contraction (wt_exact.cu).
+#ifndef WT_NORM_GATHER
+#define WT_NORM_GATHER 4
+#endif
+#ifndef WT_NORM_MINB
+#define WT_NORM_MINB 2
+#endif
+constexpr int kNormGather = WT_NORM_GATHER;  // incident triangles gathered per round (divides 8)
+
 __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* pv, int i, const double4& v,
                                               double& nx, double& ny, double& nz) {
   double ax = 0, ay = 0, az = 0;
@@ -521,26 +529,32 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
       for (int q = 0; q < 8; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(-1, -1);
     }
     const int nq = packed ? 8 : min(8, r1 - r);
-    double4 pb[8], pc[8];
+    // two rounds of four triangles: 8 vertex gathers in flight per round
+    // (16 would need ~170 registers and one CTA per SM)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const bool ok = bc[q].x != -1;  // -1 / -2 are sentinels (position bits 3: never a real entry)
-      pb[q] = pv[ok ? (bc[q].x & 0x3FFFFFFF) : i];
-      pc[q] = pv[ok ? bc[q].y : i];
-    }
+    for (int h = 0; h < 8; h += kNormGather) {
+      if (h >= nq || bc[h].x == -1) break;
+      double4 pb[kNormGather], pc[kNormGather];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (q >= nq || bc[q].x == -1) break;
-      // ring entry: b, c follow i cyclically; bits 30-31 of .x = position of i
-      const int rot = static_cast<int>(static_cast<unsigned>(bc[q].x) >> 30);
-      const double4& f0 = rot == 0 ? v : (rot == 1 ? pc[q] : pb[q]);
-      const double4& f1 = rot == 0 ? pb[q] : (rot == 1 ? v : pc[q]);
-      const double4& f2 = rot == 0 ? pc[q] : (rot == 1 ? pb[q] : v);
-      const double ex = f1.x - f0.x, ey = f1.y - f0.y, ez = f1.z - f0.z;
-      const double fx = f2.x - f0.x, fy = f2.y - f0.y, fz = f2.z - f0.z;
-      ax += ey * fz - ez * fy;
-      ay += ez * fx - ex * fz;
-      az += ex * fy - ey * fx;
+      for (int q = 0; q < kNormGather; ++q) {
+        const bool ok = bc[h + q].x != -1;  // -1 / -2 are sentinels (position bits 3: never a real entry)
+        pb[q] = pv[ok ? (bc[h + q].x & 0x3FFFFFFF) : i];
+        pc[q] = pv[ok ? bc[h + q].y : i];
+      }
+#pragma unroll
+      for (int q = 0; q < kNormGather; ++q) {
+        if (h + q >= nq || bc[h + q].x == -1) break;
+        // ring entry: b, c follow i cyclically; bits 30-31 of .x = position of i
+        const int rot = static_cast<int>(static_cast<unsigned>(bc[h + q].x) >> 30);
+        const double4& f0 = rot == 0 ? v : (rot == 1 ? pc[q] : pb[q]);
+        const double4& f1 = rot == 0 ? pb[q] : (rot == 1 ? v : pc[q]);
+        const double4& f2 = rot == 0 ? pc[q] : (rot == 1 ? pb[q] : v);
+        const double ex = f1.x - f0.x, ey = f1.y - f0.y, ez = f1.z - f0.z;
+        const double fx = f2.x - f0.x, fy = f2.y - f0.y, fz = f2.z - f0.z;
+        ax += ey * fz - ez * fy;
+        ay += ez * fx - ex * fz;
+        az += ex * fy - ey * fx;
+      }
     }
   }
   const double len = sqrt(ax * ax + ay * ay + az * az);
@@ -557,7 +571,7 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
 // with lround semantics (association.cpp:29-37,49-51) and the bin histogram.
 
 template <bool B>
-static __global__ void __launch_bounds__(kVThreads) k_normals(DevModel m, DevState s, DevIntr in,
+static __global__ void __launch_bounds__(kVThreads, WT_NORM_MINB) k_normals(DevModel m, DevState s, DevIntr in,
                                                        int do_bucket, int zero_acc, int compute) {
   pdl_entry();
   if constexpr (B) s = seq_state(s);
