@@ -2,7 +2,7 @@
 """Per-frame tracking throughput of the warptrack hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c1|c2|c3|c4] [--sequences S]
+                    [--config c1|c2|c3|c4|c5] [--sequences S] [--streams]
 
 A step is one track_frame (tracker.cpp:54-68) on one synthetic depth frame:
 5 pose Gauss-Newton iterations + 2 surface iterations + optimize_shape's
@@ -45,8 +45,9 @@ CONFIGS = {
     "c2": (640, 480, 25_000, "dynamic", 5, 2),
     "c3": (640, 480, 100_000, "dynamic", 5, 2),
     "c4": (1920, 1080, 400_000, "dynamic", 5, 2),
-    # C5: 64 independent C3 sequences per job, sharded over the GPUs (one
-    # CUDA stream + frame graph per sequence, concurrently on each GPU)
+    # C5: 64 independent C3 sequences per job, sharded over the GPUs; the
+    # sequences of a rank are one batch (BatchTracker: one frame graph whose
+    # kernels carry the sequence in blockIdx.y)
     "c5": (640, 480, 100_000, "dynamic", 5, 2),
 }
 METRIC = "frames/s at 640×480 depth, pose+surface, 100k-vert mesh; % of HBM roofline"
@@ -448,6 +449,163 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         t_.close()
 
 
+def run_batched(args, rank: int, world: int, local_rank: int) -> None:
+    """C5: the rank's sequences tracked as one batch (wt_gpu_create_batch)."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1711_07999_b200 import _lib as W
+    from paper_1711_07999_b200.tracker import BatchTracker, Tracker
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    bundle, intr, cfg = make_workload(args.config)
+    S = args.sequences
+    seqs = [rank * S + s for s in range(S)]
+    th0 = np.stack([trajectory(bundle, 0, q) for q in seqs])
+    bt = BatchTracker(bundle, intr, S, init_theta=th0, device=local_rank)
+    L = W.lib()
+    ccfg = cfg.c()
+    P = intr.width * intr.height
+    nframes = args.warmup + args.steps + 2
+    renderer = Tracker(bundle, intr, device=local_rank)
+    frames_dev = torch.empty((nframes, S, intr.height, intr.width), dtype=torch.float32, device=dev)
+    for f in range(nframes):
+        for s, q in enumerate(seqs):
+            renderer.render_depth(trajectory(bundle, f, q), frame=f, out_ptr=frames_dev[f, s].data_ptr())
+    torch.cuda.synchronize()
+    frames_host = frames_dev.cpu().pin_memory()
+    valid_px = float((frames_dev[1:] > 0).float().sum().item() / ((nframes - 1) * S))
+    st0 = torch.cuda.ExternalStream(bt.stream, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def reset():
+        for s in range(S):
+            bt.set_state(s, theta=th0[s], phi=np.zeros((bundle.vertex_count, 3)))
+
+    def frame_dev(f):
+        W.check(L.wt_gpu_batch_load_depth(bt._ctx, frames_dev[f].data_ptr(), 1.0), bt._ctx)
+        W.check(L.wt_gpu_batch_track_async(bt._ctx, C.byref(ccfg)), bt._ctx)
+
+    # ---- device-resident timing (value) ----
+    reset()
+    for f in range(1, args.warmup + 1):
+        frame_dev(f)
+    bt.sync()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(st0):
+                flush.zero_()
+                starts[k].record(st0)
+            frame_dev(args.warmup + 1 + k)
+            ends[k].record(st0)
+        torch.cuda.synchronize()
+    dev_ms = sum(starts[k].elapsed_time(ends[k]) for k in range(args.steps))
+    if world > 1:
+        dist.barrier()
+
+    # ---- end to end: pinned host frames in, stats + every theta out ----
+    reset()
+    kin = [(W.KinIterStats * 64)() for _ in range(S)]
+    shp = [(W.ShapeIterStats * 32)() for _ in range(S)]
+    stats = (W.FrameStatsC * S)(*[W.FrameStatsC(0, 0, 0, 64, 32, 0, kin[s], shp[s]) for s in range(S)])
+    theta = np.zeros(bundle.link_count)
+
+    def frame_e2e(f):
+        W.check(L.wt_gpu_batch_track(bt._ctx, frames_host[f].data_ptr(), 1.0, C.byref(ccfg), stats), bt._ctx)
+        for s in range(S):
+            W.check(L.wt_gpu_batch_get_state(bt._ctx, s, theta.ctypes.data, None), bt._ctx)
+
+    for f in range(1, args.warmup + 1):
+        frame_e2e(f)
+    e_st = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_en = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        with torch.cuda.stream(st0):
+            flush.zero_()
+        e_st[k].record(st0)
+        frame_e2e(args.warmup + 1 + k)
+        e_en[k].record(st0)
+        torch.cuda.synchronize()
+    e2e_ms = sum(e_st[k].elapsed_time(e_en[k]) for k in range(args.steps))
+
+    # ---- per-kernel device times of one batch frame (events between kernels) ----
+    kinds = (C.c_int32 * 512)()
+    ms = (C.c_float * 512)()
+    n = C.c_int32()
+    W.check(L.wt_gpu_batch_load_depth(bt._ctx, frames_dev[args.warmup + args.steps + 1].data_ptr(), 1.0), bt._ctx)
+    W.check(L.wt_gpu_profile_frame(bt._ctx, C.byref(ccfg), kinds, ms, 512, C.byref(n)), bt._ctx)
+    per_kind = {}
+    for k in range(n.value):
+        d = per_kind.setdefault(W.KERNEL_KINDS[kinds[k]], [0.0, 0])
+        d[0] += ms[k]
+        d[1] += 1
+    A = int(np.mean([stats[s].n_kin and kin[s][stats[s].n_kin - 1].associated for s in range(S)]))
+    Vvis = bundle.vertex_count // 2
+    kernels = {}
+    for name, (tot, cnt) in per_kind.items():
+        avg_ms = tot / cnt
+        b = alg_bytes(name, bundle.vertex_count, P, A, Vvis) * S
+        kernels[name] = {"launches_per_frame": cnt, "avg_us": 1e3 * avg_ms, "us_per_frame": 1e3 * tot,
+                         "alg_bytes": b, "achieved_gbs": b / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else None}
+    dominant = max((k for k in kernels if kernels[k]["alg_bytes"] > 0), key=lambda k: kernels[k]["us_per_frame"])
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms = t.tolist()
+    total_frames = args.steps * S * world
+    value = total_frames / (dev_ms * 1e-3)
+    e2e = total_frames / (e2e_ms * 1e-3)
+    if rank != 0:
+        bt.close()
+        renderer.close()
+        return
+    frame_bytes = sum(kernels[nm]["alg_bytes"] * kernels[nm]["launches_per_frame"] for nm in kernels)
+    frame_us = sum(kernels[nm]["us_per_frame"] for nm in kernels)
+    dk = kernels[dominant]
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64 (geometry, distances, normal equations; normals stored f32)",
+        "data": "synthetic (GPU synthesize_frame renders of sinusoidal joint trajectories, one phase per sequence)",
+        "config": {**workload_config(args, bundle, intr, cfg), "valid_pixels_mean": valid_px,
+                   "associated_vertices": A, "batched": True,
+                   "step": f"one frame of every sequence of the rank's batch ({S} frames per rank per step)"},
+        "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": 4 * P * S,
+                "d2h_bytes_per_step": S * (8 * bundle.link_count + 32 * 64 + 40 * 32),
+                "api": "wt_gpu_batch_track (pinned host frames of the batch, stats) + wt_gpu_batch_get_state "
+                       "theta of every sequence"},
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dk["achieved_gbs"], "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
+                     "traffic": None, "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"]},
+        "frame_roofline": {"alg_bytes_per_frame": frame_bytes, "kernel_us_per_frame": frame_us,
+                           "achieved": frame_bytes / (frame_us * 1e-6) / 1e9,
+                           "frac": frame_bytes / (frame_us * 1e-6) / 1e9 / peak,
+                           "note": "one batch frame of the rank's sequences, events between kernels"},
+        "kernels": kernels,
+        "gpu_launches": args.steps * (n.value + 1),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    bt.close()
+    renderer.close()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -458,6 +616,8 @@ def main() -> None:
     ap.add_argument("--sequences", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", action="store_true",
+                    help="c5: one Tracker + stream per sequence instead of one batch")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
@@ -470,6 +630,8 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.config == "c5" and not args.streams:
+        run_batched(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
     if world > 1 and args.impl == "ours":
