@@ -242,8 +242,15 @@ void mark(wt_gpu_ctx* c, int kind) {
 
 int vgrid(int n) { return std::max(1, (n + wt::kVThreads - 1) / wt::kVThreads); }
 
-// per-sequence CTAs of a one-wave grid of `ctas` CTAs shared by a batch
-int wave(const wt_gpu_ctx* c, int ctas) { return std::max(1, ctas / c->nseq); }
+// per-sequence CTAs of a one-wave grid of `ctas` CTAs shared by a batch,
+// times batch_mult waves for a batch (WT_WAVE_<kind> overrides it, experiments)
+int wave(const wt_gpu_ctx* c, int ctas, const char* kind, double batch_mult = 1.0) {
+  if (c->nseq == 1) return ctas;
+  double mult = batch_mult;
+  const char* e = getenv((std::string("WT_WAVE_") + kind).c_str());
+  if (e) mult = atof(e);
+  return std::max(1, static_cast<int>(ctas * mult / c->nseq));
+}
 
 // ---- validation (Skeleton::build, skeleton.cpp:7-50; bundle invariants) ----
 
@@ -457,7 +464,7 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   // 8 lanes per valid pixel; at most P pixels (the list is padded per 32 columns)
   // one wave (5 CTAs per SM fit the registers); warps stride over the 4-pixel groups
   // (a batch shares the wave between its sequences)
-  const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, wave(c, 5 * 148)));
+  const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, wave(c, 5 * 148, "SEARCH", 8.0)));
   WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_search<true> : wt::k_search<false>, dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
   mark(c, K_SEARCH);
 }
@@ -474,7 +481,7 @@ int pose_threads(const wt_gpu_ctx*) { return 128; }
 
 int pose_grid(const wt_gpu_ctx* c) {
   const int warps = pose_threads(c) / 32;
-  return std::max(1, std::min((c->V + 32 * warps - 1) / (32 * warps), wave(c, 4 * 148)));
+  return std::max(1, std::min((c->V + 32 * warps - 1) / (32 * warps), wave(c, 4 * 148, "POSE")));
 }
 
 // JtJ entries per lane (upper triangle + Jtr) held in registers
@@ -525,7 +532,7 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
   mark(c, K_POSE_SOLVE);
 }
 
-int shape_grid(const wt_gpu_ctx* c) { return std::max(1, std::min(vgrid(c->V), wave(c, 4 * 148))); }
+int shape_grid(const wt_gpu_ctx* c) { return std::max(1, std::min(vgrid(c->V), wave(c, 4 * 148, "SHAPE"))); }
 
 void enq_shape(wt_gpu_ctx* c, const wt_shape_config* sc, int it, const double4* in, double4* out) {
   wt::ShapeArgs sa;

@@ -1617,6 +1617,8 @@ struct ShapeArgs {
   int pad;
 };
 
+constexpr int kNbrAhead = 4;  // neighbour gathers issued together in k_shape (kNN k = 4)
+
 template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState s, const double4* phi_in,
                                                      double4* phi_out, ShapeArgs a) {
@@ -1634,7 +1636,27 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
     const double ph[3] = {f.x, f.y, f.z};
     double nd[3] = {0.0, 0.0, 0.0};
     int ncount = 0;
-    for (int k = 0; k < m.K; ++k) {
+    // the first kNbrAhead neighbour indices, then their phi, all in flight at
+    // once; summed in list order up to the first -1 (as the loop below)
+    int jn[kNbrAhead];
+    double4 fn[kNbrAhead];
+#pragma unroll
+    for (int k = 0; k < kNbrAhead; ++k) jn[k] = k < m.K ? m.nbr[k * m.V + i] : -1;
+#pragma unroll
+    for (int k = 0; k < kNbrAhead; ++k) fn[k] = phi_in[jn[k] >= 0 ? jn[k] : i];
+    bool more = true;
+#pragma unroll
+    for (int k = 0; k < kNbrAhead; ++k) {
+      if (!more || jn[k] < 0) {
+        more = false;
+        continue;
+      }
+      nd[0] += ph[0] - fn[k].x;
+      nd[1] += ph[1] - fn[k].y;
+      nd[2] += ph[2] - fn[k].z;
+      ++ncount;
+    }
+    for (int k = kNbrAhead; more && k < m.K; ++k) {
       const int j = m.nbr[k * m.V + i];
       if (j < 0) break;
       const double4 fj = phi_in[j];

@@ -10,8 +10,8 @@ import csv
 import sys
 
 SCALE = {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3}
-TRACK = ("k_fk", "k_ingest", "k_skin(", "k_normals", "k_pixoff", "k_scatter", "k_search", "k_pose_system", "k_pose_solve",
-         "k_shape(", "k_shape_after", "k_record")
+TRACK = ("k_fk", "k_ingest", "k_skin<", "k_skin(", "k_normals", "k_pixoff", "k_scatter", "k_search", "k_pose_system",
+         "k_pose_solve", "k_shape<", "k_shape(", "k_shape_after", "k_record")
 
 
 def main(path):

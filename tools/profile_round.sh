@@ -16,4 +16,11 @@ for k in k_search k_pose_system k_pose_solve k_normals k_shape k_scatter k_pixof
   ncu --set full --clock-control none --import-source on -k regex:"${k}" -s 6 -c 2 -o $out/full_$k $pcmd \
     > $out/ncu_full_$k.log 2>&1
 done
+# C5 as one batch of 64 sequences: bench line + full captures of its two hottest kernels
+python bench.py --config c5 --steps 10 --warmup 3 > $out/bench_c5.json 2> $out/bench_c5.err || exit 3
+python tools/batch_timing.py 64 > $out/plain_batch.log 2>&1 || exit 4
+for k in k_normals k_search; do
+  ncu --set full --clock-control none --import-source on -k regex:"${k}" -s 20 -c 1 -o $out/batch_$k \
+    python tools/batch_timing.py 64 > $out/ncu_batch_$k.log 2>&1
+done
 echo done
