@@ -469,8 +469,11 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   mark(c, K_SEARCH);
 }
 
-void enq_associate(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, int* winners) {
-  enq_normals(c, s, true, true);
+// zero_acc: clear the observation sums first (stage hooks); the frame graphs
+// rely on their consumers leaving them clean (clear_acc, wt_kernels.cuh)
+void enq_associate(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, int* winners,
+                   bool zero_acc = false) {
+  enq_normals(c, s, true, zero_acc);
   enq_scatter(c, s);
   enq_search(c, s, a, winners);
 }
@@ -504,7 +507,7 @@ void pose_attr(wt_gpu_ctx* c) {
 }
 
 void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt_kin_config* k,
-              int it, bool solve, const int* count_in, const double* res_in) {
+              int it, bool solve, const int* count_in, const double* res_in, bool clean_acc = false) {
   wt::PoseArgs pa;
   pa.lambda_k = k->lambda_k;
   pa.lambda_s = k->lambda_s;
@@ -513,7 +516,7 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
   pa.clamp = k->clamp_limits;
   pa.iteration = it;
   pa.solve = solve ? 1 : 0;
-  pa.pad = 0;
+  pa.clean_acc = clean_acc ? 1 : 0;
   pa.count_in = count_in;
   pa.res_in = res_in;
   pa.dbg = c->pose_dbg;
@@ -535,13 +538,14 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
 int shape_grid(const wt_gpu_ctx* c) { return std::max(1, std::min(vgrid(c->V), wave(c, 4 * 148, "SHAPE"))); }
 
 void enq_shape(wt_gpu_ctx* c, const wt_shape_config* sc, int it, const double4* in, double4* out) {
+  // the shape step is the association's only consumer: it leaves the sums clean
   wt::ShapeArgs sa;
   sa.lambda_phi = sc->lambda_phi;
   sa.lambda_nbr = sc->lambda_nbr;
   sa.lambda_w = sc->lambda_w;
   sa.diag_floor = sc->diag_floor;
   sa.iteration = it;
-  sa.pad = 0;
+  sa.clean_acc = 1;
   WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_shape<true> : wt::k_shape<false>, dim3(shape_grid(c), c->nseq), dim3(wt::kVThreads), sizeof(double) * 8 * c->L, c->stream,
                          c->dm, c->ds, in, out, sa));
   mark(c, K_SHAPE);
@@ -559,7 +563,9 @@ void enq_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* k, const wt_assoc_con
       // correspondences kept, residuals follow the moved surface (:145-150)
       enq_normals(c, c->ds, false, false);
     }
-    enq_pose(c, c->ds, c->phi[c->cur], k, it, true, nullptr, nullptr);
+    // the last pose system before a re-association (or the end) cleans the sums
+    const bool last_use = (it + 1) % refresh == 0 || it + 1 == k->iterations;
+    enq_pose(c, c->ds, c->phi[c->cur], k, it, true, nullptr, nullptr, last_use);
   }
 }
 
@@ -577,8 +583,7 @@ int enq_optimize_shape(wt_gpu_ctx* c, int cur, const wt_shape_config* sc, const 
     enq_skin(c, c->ds, c->phi[cur]);
     enq_associate(c, c->ds, a, nullptr);
     WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_shape_after<true> : wt::k_shape_after<false>, dim3(shape_grid(c), c->nseq), dim3(wt::kVThreads), 0, c->stream, c->dm,
-                           c->ds,
-                           sc->iterations));
+                           c->ds, sc->iterations, 1));
     mark(c, K_SHAPE_AFTER);
   }
   return cur;
@@ -1464,10 +1469,13 @@ int wt_gpu_associate(wt_gpu_ctx* c, int32_t window_radius, double cutoff, int32_
     wt_assoc_config a{window_radius, 0, cutoff};
     check_assoc(&a);
     if (winners) WT_CUDA(cudaMemsetAsync(c->d_winners, 0xFF, sizeof(int) * c->P, c->stream));
-    enq_associate(c, c->hs, &a, winners ? c->d_winners : nullptr);
+    enq_associate(c, c->hs, &a, winners ? c->d_winners : nullptr, /*zero_acc=*/true);
     if (winners)
       WT_CUDA(cudaMemcpyAsync(winners, c->d_winners, sizeof(int) * c->P, cudaMemcpyDeviceToHost, c->stream));
     read_association(c->stream, c->V, c->hs, p_tilde, count, residual);
+    // leave the sums clean for the frame graphs (their consumers clean up)
+    WT_CUDA(cudaMemsetAsync(c->hs.acc, 0, sizeof(unsigned long long) * 4 * std::max(1, c->V), c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

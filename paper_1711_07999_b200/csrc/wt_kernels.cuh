@@ -147,6 +147,15 @@ __device__ inline DevFrame seq_frame(DevFrame f) {
   return f;
 }
 
+// The observation sums are self-cleaning: the kernel that consumes an
+// association last (the pose system before the next re-association, the
+// shape step, the stats pass) zeroes the sums it read, so k_normals need not
+// clear all V of them before every search.
+__device__ __forceinline__ void clear_acc(unsigned long long* acc, int i) {
+  reinterpret_cast<ulonglong2*>(acc)[2 * i] = make_ulonglong2(0ull, 0ull);
+  reinterpret_cast<ulonglong2*>(acc)[2 * i + 1] = make_ulonglong2(0ull, 0ull);
+}
+
 // ---------------------------------------------------------------------------
 // Programmatic dependent launch: the frame graph's kernels are launched with
 // programmatic stream serialisation, so kernel N+1's CTAs become resident
@@ -592,10 +601,7 @@ static __global__ void __launch_bounds__(kVThreads, WT_NORM_MINB) k_normals(DevM
       nz = n.z;
       valid = n.w != 0.0f;
     }
-    if (zero_acc) {
-      reinterpret_cast<ulonglong2*>(s.acc)[2 * i] = make_ulonglong2(0ull, 0ull);
-      reinterpret_cast<ulonglong2*>(s.acc)[2 * i + 1] = make_ulonglong2(0ull, 0ull);
-    }
+    if (zero_acc) clear_acc(s.acc, i);
     if (do_bucket) {
       // bucket_occupancy (association.cpp:39-56): per-pixel and per-row
       // counts as fire-and-forget reductions (no value comes back, so no
@@ -1031,7 +1037,7 @@ struct PoseArgs {
   int clamp;
   int iteration;
   int solve;             // 0: only dump JtJ/Jtr (+prior) to s.sys_out (stage hook)
-  int pad;
+  int clean_acc;        // zero the sums read (last consumer of this association)
   const int* count_in;   // optional association override (stage hook)
   const double* res_in;
   long long* dbg;        // optional timing record of the last CTA (WT_DEBUG_POSE)
@@ -1192,6 +1198,7 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
           const long long c = static_cast<long long>(a23.y);
           have = c > 0;
           if (have) {
+            if (a.clean_acc) clear_acc(s.acc, i);
             const double inv = 1.0 / static_cast<double>(c);
             const double px = unfix(a01.x, kFixPoint) * inv, py = unfix(a01.y, kFixPoint) * inv,
                          pz = unfix(a23.x, kFixPoint) * inv;
@@ -1614,7 +1621,7 @@ __device__ __forceinline__ bool solve_vertex3(const double g[3], double r, const
 struct ShapeArgs {
   double lambda_phi, lambda_nbr, lambda_w, diag_floor;
   int iteration;
-  int pad;
+  int clean_acc;  // zero the observation sums read
 };
 
 constexpr int kNbrAhead = 4;  // neighbour gathers issued together in k_shape (kNN k = 4)
@@ -1670,6 +1677,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
     double pt[3];
     long long cnt = 0;
     if (observed_mean(s.acc, i, pt, &cnt)) {
+      if (a.clean_acc) clear_acc(s.acc, i);
       const double4 v = s.pv[i];
       const float4 n = s.pn[i];
       const double ro = static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
@@ -1738,7 +1746,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
 // Closing measurement pass of optimize_shape (shapeopt.cpp:112-129): mean
 // |r| over observed vertices of a fresh association; fills mean_abs_r_after.
 template <bool B>
-static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, DevState s, int n_its) {
+static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, DevState s, int n_its, int clean_acc) {
   pdl_entry();
   if constexpr (B) s = seq_state(s);
   double abs_r = 0.0;
@@ -1747,6 +1755,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, De
     double pt[3];
     long long cnt = 0;
     if (observed_mean(s.acc, i, pt, &cnt)) {
+      if (clean_acc) clear_acc(s.acc, i);
       const double4 v = s.pv[i];
       const float4 n = s.pn[i];
       abs_r += fabs(static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
