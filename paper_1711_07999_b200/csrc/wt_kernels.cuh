@@ -147,13 +147,41 @@ __device__ inline DevFrame seq_frame(DevFrame f) {
   return f;
 }
 
+// ---------------------------------------------------------------------------
+// 256-bit global accesses. sm_100 has 32-byte vector loads and stores
+// (LDG/STG.E.ENL2.256): a double4 record (posed vertex, bucket item, phi,
+// skin weights, observation sums) moves in ONE L1 wavefront instead of the two
+// 128-bit halves the compiler emits for a double4, which halves the L1 work
+// of the gather-heavy kernels (normals, search, shape). Every buffer these
+// touch is 32-byte aligned (256-byte carve, wt_gpu.cu). The loads go through
+// the non-coherent path: nothing a kernel reads this way is written by the
+// same kernel. They are volatile so they stay behind the PDL wait
+// (pdl_entry) like every other access.
+__device__ __forceinline__ double4 ld256(const double4* p) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ ulonglong4 ld256(const ulonglong4* p) {
+  ulonglong4 v;
+  asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(v.x), "=l"(v.y), "=l"(v.z), "=l"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st256(double4* p, double4 v) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st256(ulonglong4* p, ulonglong4 v) {
+  asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v.x), "l"(v.y), "l"(v.z), "l"(v.w)
+               : "memory");
+}
+
 // The observation sums are self-cleaning: the kernel that consumes an
 // association last (the pose system before the next re-association, the
 // shape step, the stats pass) zeroes the sums it read, so k_normals need not
 // clear all V of them before every search.
 __device__ __forceinline__ void clear_acc(unsigned long long* acc, int i) {
-  reinterpret_cast<ulonglong2*>(acc)[2 * i] = make_ulonglong2(0ull, 0ull);
-  reinterpret_cast<ulonglong2*>(acc)[2 * i + 1] = make_ulonglong2(0ull, 0ull);
+  st256(reinterpret_cast<ulonglong4*>(acc) + i, make_ulonglong4(0ull, 0ull, 0ull, 0ull));
 }
 
 // ---------------------------------------------------------------------------
@@ -485,20 +513,20 @@ static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState 
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m.V) return;
-  const double4 a = m.v0[i];
-  const double4 f = phi[i];
+  const double4 a = ld256(m.v0 + i);
+  const double4 f = ld256(phi + i);
   const double rest[3] = {a.x + f.x, a.y + f.y, a.z + f.z};
   DQ raw;
   double sign[4];
   double4 out;
-  if (blend_vertex(s_off, m.wgt[i], m.wlink[i], raw, sign)) {
+  if (blend_vertex(s_off, ld256(m.wgt + i), m.wlink[i], raw, sign)) {
     double p[3];
     dq_transform_point(dq_normalize(raw), rest, p);
     out = make_double4(p[0], p[1], p[2], 1.0);
   } else {
     out = make_double4(rest[0], rest[1], rest[2], 0.0);  // placeholder, excluded downstream
   }
-  s.pv[i] = out;
+  st256(s.pv + i, out);
 }
 
 // Vertex normal exactly as skin() (skinmesh.cpp:125-139): per incident
@@ -547,8 +575,8 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
 #pragma unroll
       for (int q = 0; q < kNormGather; ++q) {
         const bool ok = bc[h + q].x != -1;  // -1 / -2 are sentinels (position bits 3: never a real entry)
-        pb[q] = pv[ok ? (bc[h + q].x & 0x3FFFFFFF) : i];
-        pc[q] = pv[ok ? bc[h + q].y : i];
+        pb[q] = ld256(pv + (ok ? (bc[h + q].x & 0x3FFFFFFF) : i));
+        pc[q] = ld256(pv + (ok ? bc[h + q].y : i));
       }
 #pragma unroll
       for (int q = 0; q < kNormGather; ++q) {
@@ -586,7 +614,7 @@ static __global__ void __launch_bounds__(kVThreads, WT_NORM_MINB) k_normals(DevM
   if constexpr (B) s = seq_state(s);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m.V) {
-    const double4 v = s.pv[i];
+    const double4 v = ld256(s.pv + i);
     const double vx = v.x, vy = v.y, vz = v.z;
     double nx = 0, ny = 0, nz = 0;
     bool valid;
@@ -698,11 +726,11 @@ static __global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevSta
   if (i < H) s.row_cnt[i] = 0;
   if (i >= m.V) return;
   const int pix = s.vpix[i];
-  const double4 v = s.pv[i];
   if (pix < 0) return;
+  const double4 v = ld256(s.pv + i);
   // k_pixoff left cursor[pix] = poff[pix]: the returned value is the slot
-  s.items[atomicAdd(&s.cursor[pix], 1)] =
-      make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(i)));
+  st256(s.items + atomicAdd(&s.cursor[pix], 1),
+        make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(i))));
 }
 
 // ---------------------------------------------------------------------------
@@ -754,10 +782,9 @@ __device__ __forceinline__ void scan_span(const DevState& s, int e0, int e1, dou
   const long long ck = d2_key(cut2);
   long long bk = best_i < 0 ? LLONG_MAX : d2_key(best_x);
   for (int e = e0; e < e1; ++e) {
-    const double2* q = reinterpret_cast<const double2*>(s.items + e);
-    const double2 a01 = __ldg(q), a23 = __ldg(q + 1);
-    const long long xk = d2_key(exact_d2(make_double4(a01.x, a01.y, a23.x, 0.0), px, py, pz));
-    const int vi = static_cast<int>(__double_as_longlong(a23.y));
+    const double4 it = ld256(s.items + e);
+    const long long xk = d2_key(exact_d2(it, px, py, pz));
+    const int vi = static_cast<int>(__double_as_longlong(it.w));
     if (xk <= ck && (xk < bk || (xk == bk && vi < best_i))) {
       bk = xk;
       best_i = vi;
@@ -892,8 +919,8 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
 // p~_i = mean of the observations won by vertex i; count in *cnt.
 __device__ __forceinline__ bool observed_mean(const unsigned long long* acc, int i, double* pt,
                                               long long* cnt) {
-  const ulonglong2 a01 = reinterpret_cast<const ulonglong2*>(acc)[2 * i];
-  const ulonglong2 a23 = reinterpret_cast<const ulonglong2*>(acc)[2 * i + 1];
+  const ulonglong4 q = ld256(reinterpret_cast<const ulonglong4*>(acc) + i);
+  const ulonglong2 a01 = make_ulonglong2(q.x, q.y), a23 = make_ulonglong2(q.z, q.w);
   const long long c = static_cast<long long>(a23.y);
   *cnt = c;
   if (c <= 0) return false;
@@ -1191,9 +1218,9 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
           have = a.count_in[i] > 0;
           r = have ? a.res_in[i] : 0.0;
         } else {
-          const ulonglong2 a01 = reinterpret_cast<const ulonglong2*>(s.acc)[2 * i];
-          const ulonglong2 a23 = reinterpret_cast<const ulonglong2*>(s.acc)[2 * i + 1];
-          const double4 v = s.pv[i];
+          const ulonglong4 q = ld256(reinterpret_cast<const ulonglong4*>(s.acc) + i);
+          const ulonglong2 a01 = make_ulonglong2(q.x, q.y), a23 = make_ulonglong2(q.z, q.w);
+          const double4 v = ld256(s.pv + i);
           const float4 n = s.pn[i];
           const long long c = static_cast<long long>(a23.y);
           have = c > 0;
@@ -1230,10 +1257,10 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
         const float4 n = s.pn[i];
         DQ raw;
         double sign[4];
-        const double4 wv = m.wgt[i];
+        const double4 wv = ld256(m.wgt + i);
         const uchar4 lk = m.wlink[i];
-        const double4 a0 = m.v0[i];
-        const double4 f = phi[i];
+        const double4 a0 = ld256(m.v0 + i);
+        const double4 f = ld256(phi + i);
         if (n.w != 0.0f && blend_vertex(s_off, wv, lk, raw, sign)) {
           const double rest[3] = {a0.x + f.x, a0.y + f.y, a0.z + f.z};
           const double nn[3] = {n.x, n.y, n.z};
@@ -1639,7 +1666,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
   double abs_r = 0.0, sum_phi = 0.0, max_phi = 0.0;
   long long observed = 0, singular = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
-    const double4 f = phi_in[i];
+    const double4 f = ld256(phi_in + i);
     const double ph[3] = {f.x, f.y, f.z};
     double nd[3] = {0.0, 0.0, 0.0};
     int ncount = 0;
@@ -1650,7 +1677,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
 #pragma unroll
     for (int k = 0; k < kNbrAhead; ++k) jn[k] = k < m.K ? m.nbr[k * m.V + i] : -1;
 #pragma unroll
-    for (int k = 0; k < kNbrAhead; ++k) fn[k] = phi_in[jn[k] >= 0 ? jn[k] : i];
+    for (int k = 0; k < kNbrAhead; ++k) fn[k] = ld256(phi_in + (jn[k] >= 0 ? jn[k] : i));
     bool more = true;
 #pragma unroll
     for (int k = 0; k < kNbrAhead; ++k) {
@@ -1666,7 +1693,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
     for (int k = kNbrAhead; more && k < m.K; ++k) {
       const int j = m.nbr[k * m.V + i];
       if (j < 0) break;
-      const double4 fj = phi_in[j];
+      const double4 fj = ld256(phi_in + j);
       nd[0] += ph[0] - fj.x;
       nd[1] += ph[1] - fj.y;
       nd[2] += ph[2] - fj.z;
@@ -1678,7 +1705,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
     long long cnt = 0;
     if (observed_mean(s.acc, i, pt, &cnt)) {
       if (a.clean_acc) clear_acc(s.acc, i);
-      const double4 v = s.pv[i];
+      const double4 v = ld256(s.pv + i);
       const float4 n = s.pn[i];
       const double ro = static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
                         static_cast<double>(n.z) * (pt[2] - v.z);
@@ -1686,7 +1713,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
       ++observed;
       DQ raw;
       double sign[4];
-      if (n.w != 0.0f && blend_vertex(s_off, m.wgt[i], m.wlink[i], raw, sign)) {
+      if (n.w != 0.0f && blend_vertex(s_off, ld256(m.wgt + i), m.wlink[i], raw, sign)) {
         // dr/dphi = -(R^T n), R = rotation of the normalised blend
         double R[9];
         dq_rotation(dq_normalize(raw), R);
@@ -1701,7 +1728,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
                                   a.diag_floor, delta);
     singular += ok ? 0 : 1;
     const double nx = ph[0] - delta[0], ny = ph[1] - delta[1], nz = ph[2] - delta[2];
-    phi_out[i] = make_double4(nx, ny, nz, 0.0);
+    st256(phi_out + i, make_double4(nx, ny, nz, 0.0));
     const double len = sqrt(nx * nx + ny * ny + nz * nz);
     sum_phi += len;
     max_phi = fmax(max_phi, len);
@@ -1756,7 +1783,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, De
     long long cnt = 0;
     if (observed_mean(s.acc, i, pt, &cnt)) {
       if (clean_acc) clear_acc(s.acc, i);
-      const double4 v = s.pv[i];
+      const double4 v = ld256(s.pv + i);
       const float4 n = s.pn[i];
       abs_r += fabs(static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
                     static_cast<double>(n.z) * (pt[2] - v.z));
