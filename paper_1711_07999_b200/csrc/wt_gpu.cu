@@ -349,7 +349,6 @@ void layout_seq(wt_gpu_ctx* c, Carve& a) {
   s.pv = a.take<double4>(V);
   s.pn = a.take<float4>(V);
   s.vpix = a.take<int>(V);
-  s.cursor = a.take<int>(P);
   s.pix_cnt = a.take<int>(P);
   s.row_cnt = a.take<int>(H);
   s.poff = a.take<int>(P + 1);
@@ -461,10 +460,11 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   sa.cut2 = a->cutoff * a->cutoff;
   sa.write_winners = winners ? 1 : 0;
   sa.winners = winners;
-  // 8 lanes per valid pixel; at most P pixels (the list is padded per 32 columns)
+  // G lanes per valid pixel; at most P pixels (the list is padded per 32 columns)
   // one wave (5 CTAs per SM fit the registers); warps stride over the 4-pixel groups
   // (a batch shares the wave between its sequences)
-  const int grid = std::max(1, std::min(c->P * wt::kSearchGroup / wt::kVThreads + 1, wave(c, 5 * 148, "SEARCH", 8.0)));
+  const int G = c->nseq > 1 ? wt::kSearchGroupBatch : wt::kSearchGroupSolo;
+  const int grid = std::max(1, std::min(c->P * G / wt::kVThreads + 1, wave(c, 5 * 148, "SEARCH", 8.0)));
   WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_search<true> : wt::k_search<false>, dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
   mark(c, K_SEARCH);
 }

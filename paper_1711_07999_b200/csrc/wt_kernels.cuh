@@ -73,8 +73,7 @@ struct DevState {
   double4* pv;        // posed vertices (x,y,z, blend ok), fp64
   float4* pn;         // normals (x,y,z, valid)
   int* vpix;          // bucket pixel (row-major) or -1
-  int* cursor;        // [P] k_scatter's fill position per pixel (set by k_pixoff)
-  int* pix_cnt;       // [P] bucket sizes (self-cleaning: cleared by k_pixoff)
+  int* pix_cnt;       // [P] bucket sizes (self-cleaning: k_scatter counts them back down to 0)
   int* row_cnt;       // [H] bucketed vertices per image row (cleared by k_scatter)
   int* poff;          // [P+1] row-major pixel offsets: the VertexBuckets CSR
   double4* items;     // bucketed vertices in pixel order (x,y,z, bits: vertex index)
@@ -123,7 +122,6 @@ __device__ inline DevState seq_state(DevState s) {
   s.pv = seq_ptr(s.pv, o);
   s.pn = seq_ptr(s.pn, o);
   s.vpix = seq_ptr(s.vpix, o);
-  s.cursor = seq_ptr(s.cursor, o);
   s.pix_cnt = seq_ptr(s.pix_cnt, o);
   s.row_cnt = seq_ptr(s.row_cnt, o);
   s.poff = seq_ptr(s.poff, o);
@@ -439,7 +437,7 @@ static __global__ void k_fk(DevModel m, DevState s) {
 // warp are row neighbours from at most two 32-column segments.
 
 constexpr int kIngestSeg = 256;
-constexpr int kRunAlign = 4;  // = pixels per search warp (32 / kSearchGroup)
+constexpr int kRunAlign = 4;  // pixels per search warp of the single-sequence search (32 / 8)
 
 template <bool B>
 static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const float* depth, double scale,
@@ -574,9 +572,11 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
       double4 pb[kNormGather], pc[kNormGather];
 #pragma unroll
       for (int q = 0; q < kNormGather; ++q) {
-        const bool ok = bc[h + q].x != -1;  // -1 / -2 are sentinels (position bits 3: never a real entry)
-        pb[q] = ld256(pv + (ok ? (bc[h + q].x & 0x3FFFFFFF) : i));
-        pc[q] = ld256(pv + (ok ? bc[h + q].y : i));
+        // -1 / -2 are sentinels (position bits 3: never a real entry); padding
+        // slots load nothing (predicated off, no L1 wavefront)
+        const bool ok = bc[h + q].x != -1;
+        pb[q] = ok ? ld256(pv + (bc[h + q].x & 0x3FFFFFFF)) : v;
+        pc[q] = ok ? ld256(pv + bc[h + q].y) : v;
       }
 #pragma unroll
       for (int q = 0; q < kNormGather; ++q) {
@@ -657,7 +657,7 @@ static __global__ void __launch_bounds__(kVThreads, WT_NORM_MINB) k_normals(DevM
 // one warp per image row, no block barriers: the row's base is the sum of
 // the preceding rows' counts (warp reduction); the row is read in coalesced
 // 32-pixel chunks, all loads first, then scanned chunk by chunk with
-// shuffles. Clears the per-pixel counts for the next association.
+// shuffles. (k_scatter counts the per-pixel sizes back down to zero.)
 
 constexpr int kRowChunks = 64;  // rows up to 2048 pixels
 
@@ -707,8 +707,6 @@ static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, 
     const int c = t * 32 + lane;
     if (c < W) {
       off[c] = run + incl - v[t];
-      s.cursor[row * W + c] = run + incl - v[t];
-      cnt[c] = 0;
     }
     run += __shfl_sync(0xffffffffu, incl, 31);
   }
@@ -728,8 +726,10 @@ static __global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevSta
   const int pix = s.vpix[i];
   if (pix < 0) return;
   const double4 v = ld256(s.pv + i);
-  // k_pixoff left cursor[pix] = poff[pix]: the returned value is the slot
-  st256(s.items + atomicAdd(&s.cursor[pix], 1),
+  // the bucket's slots are poff[pix] + (count - 1) .. poff[pix]: taken by
+  // counting the bucket size back down, which leaves the counts at zero for
+  // the next association (no cursor array, no clearing pass)
+  st256(s.items + __ldg(s.poff + pix) + atomicSub(&s.pix_cnt[pix], 1) - 1,
         make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(i))));
 }
 
@@ -806,22 +806,29 @@ __device__ __forceinline__ void search_emit(const DevState& s, const SearchArgs&
   }
 }
 
-// k_search: a group of 8 lanes per valid pixel (4 pixels per warp, taken
+// k_search: a group of G lanes per valid pixel (32 / G pixels per warp, taken
 // from the image-ordered 32-column runs of the valid-pixel list, so a warp's
 // pixels are row neighbours and share cache lines). Phase 1: lane r of the
-// group scans row r of the pixel's (2 K1 + 1)^2 core (K1 = 2) -- one span of
-// the row-major bucket CSR each, all rows in parallel -- and the group
-// reduces the lexicographic (d^2, index) minimum with shuffles. The pixel is
-// finished when the exact ring bound lb(K1 + 1) exceeds that best (or the
-// cutoff). Phase 2 (rare): the outermost ring K* that can still hold a winner
-// or a tie is fixed from the phase-1 best, and the group's lanes scan the
-// rows of the (2K*+1)^2 box outside the core, 8 rows at a time.
-constexpr int kNearRings = 2;
-constexpr int kSearchGroup = 8;
+// group scans row r of the pixel's (2 K1 + 1)^2 core -- one span of the
+// row-major bucket CSR each, all rows in parallel -- and the group reduces
+// the lexicographic (d^2, index) minimum with shuffles. The pixel is finished
+// when the exact ring bound lb(K1 + 1) exceeds that best (or the cutoff).
+// Phase 2 (rare): the outermost ring K* that can still hold a winner or a tie
+// is fixed from the phase-1 best, and the group's lanes scan the rows of the
+// (2K*+1)^2 box outside the core, G rows at a time.
+// Two instantiations (the result is the same exact minimum either way):
+//  - one sequence (latency-bound): K1 = 2, G = 8 -- a 5x5 core, five rows in
+//    flight per pixel;
+//  - a batch (L1-throughput-bound): K1 = 1, G = 4 -- a 3x3 core, which
+//    already closes most pixels (the nearest vertex is ~2 px-widths closer
+//    than lb(2)), so a pixel loads ~2.7x fewer bucket items.
+constexpr int kNearRingsSolo = 2, kSearchGroupSolo = 8;
+constexpr int kNearRingsBatch = 1, kSearchGroupBatch = 4;
 
+template <int G>
 __device__ __forceinline__ void group_min(double& bx, int& bi) {
 #pragma unroll
-  for (int o = kSearchGroup / 2; o > 0; o >>= 1) {
+  for (int o = G / 2; o > 0; o >>= 1) {
     const double ox = __shfl_xor_sync(0xffffffffu, bx, o);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (oi >= 0 && (bi < 0 || ox < bx || (ox == bx && oi < bi))) {
@@ -831,7 +838,7 @@ __device__ __forceinline__ void group_min(double& bx, int& bi) {
   }
 }
 
-template <bool B>
+template <bool B, int NR = B ? kNearRingsBatch : kNearRingsSolo, int G = B ? kSearchGroupBatch : kSearchGroupSolo>
 static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
   pdl_entry();
   if constexpr (B) s = seq_state(s);
@@ -839,14 +846,14 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
   if constexpr (B) a.winners = seq_ptr(a.winners, seq_off(s.bstride));
   const int nv = *f.n_valid;
   const int w = a.window;
-  const int K1 = min(kNearRings, w);
+  const int K1 = min(NR, w);
   const double ifx = 1.0 / a.fx, ify = 1.0 / a.fy;
-  const int lane = threadIdx.x & 31, sub = lane & (kSearchGroup - 1);
-  constexpr int PPW = 32 / kSearchGroup;  // pixels per warp
+  const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+  constexpr int PPW = 32 / G;  // pixels per warp
   const int TW = gridDim.x * (blockDim.x >> 5);
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   for (int base = gw * PPW; base < nv; base += TW * PPW) {
-    const int j = base + lane / kSearchGroup;
+    const int j = base + lane / G;
     const int pix = j < nv ? f.vlist[j] : -1;
     const bool act = pix >= 0;
     const int pu = pix % a.W, pv = pix / a.W;
@@ -866,7 +873,7 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
         scan_span(s, __ldg(s.poff + r + c0), __ldg(s.poff + r + c1 + 1), px, py, pz, a.cut2, best_x, best_i);
       }
     }
-    group_min(best_x, best_i);
+    group_min<G>(best_x, best_i);
     bool open = false;
     if (act) {
       bool done = K1 == w;
@@ -893,7 +900,7 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
           }
         }
         const int c0 = max(pu - ks, 0), c1 = min(pu + ks, a.W - 1);
-        for (int dr = sub - ks; dr <= ks; dr += kSearchGroup) {
+        for (int dr = sub - ks; dr <= ks; dr += G) {
           const int rr = pv + dr;
           if (rr < 0 || rr >= a.H) continue;
           const int r = rr * a.W;
@@ -906,7 +913,7 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
           }
         }
       }
-      group_min(bx, bi);
+      group_min<G>(bx, bi);
       if (open && bi >= 0 && (best_i < 0 || bx < best_x || (bx == best_x && bi < best_i))) {
         best_x = bx;
         best_i = bi;
