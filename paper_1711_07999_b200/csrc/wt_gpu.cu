@@ -859,18 +859,44 @@ int create_ctx(int device, const wt_model_desc* d, const wt_intrinsics* intr, in
     uchar4* d_wl = c->mem.alloc<uchar4>(V);
     int* d_roff = c->mem.alloc<int>(V + 1);
     int2* d_ring = c->mem.alloc<int2>(ring.size());
-    // padded 8-slot copy of the ring for vertices with <= 8 incident triangles
-    std::vector<int2> ring8(static_cast<size_t>(V) * 8, make_int2(-1, -1));
+    // fan table of k_normals: the distinct ring neighbours of each vertex
+    // (first-appearance order) and, per incident triangle in CSR order, the
+    // slots of its two other vertices and the position of i (rot)
+    std::vector<int> fan_nb(static_cast<size_t>(V) * 8, -1);
+    std::vector<unsigned long long> fan_code(static_cast<size_t>(V), ~0ull);
     for (int i = 0; i < V; ++i) {
       const int n = ring_off[i + 1] - ring_off[i];
-      if (n > 8) {
-        ring8[static_cast<size_t>(i) * 8] = make_int2(-2, -2);
-        continue;
+      int* nb = fan_nb.data() + static_cast<size_t>(i) * 8;
+      int cnt = 0;
+      auto slot = [&](int id) {
+        for (int k = 0; k < cnt; ++k)
+          if (nb[k] == id) return k;
+        if (cnt == 8) return -1;
+        nb[cnt] = id;
+        return cnt++;
+      };
+      unsigned long long code = ~0ull;
+      bool ok = n <= 8;
+      for (int q = 0; ok && q < n; ++q) {
+        const int2 e = ring[ring_off[i] + q];
+        const int b = slot(e.x & 0x3FFFFFFF), cc = slot(e.y);
+        if (b < 0 || cc < 0) {
+          ok = false;
+          break;
+        }
+        const unsigned long long byte = (static_cast<unsigned>(e.x) >> 30) | (b << 2) | (cc << 5);
+        code = (code & ~(0xFFull << (8 * q))) | (byte << (8 * q));
       }
-      for (int q = 0; q < n; ++q) ring8[static_cast<size_t>(i) * 8 + q] = ring[ring_off[i] + q];
+      if (!ok) {
+        std::fill(nb, nb + 8, -1);
+        nb[0] = -2;
+      }
+      fan_code[i] = code;
     }
-    int2* d_ring8 = c->mem.alloc<int2>(ring8.size());
-    upload(d_ring8, ring8.data(), ring8.size(), c->stream);
+    int* d_fan_nb = c->mem.alloc<int>(fan_nb.size());
+    unsigned long long* d_fan_code = c->mem.alloc<unsigned long long>(fan_code.size());
+    upload(d_fan_nb, fan_nb.data(), fan_nb.size(), c->stream);
+    upload(d_fan_code, fan_code.data(), fan_code.size(), c->stream);
     int* d_nbr = c->mem.alloc<int>(nbr.size());
     wt::LinkDesc* d_links = c->mem.alloc<wt::LinkDesc>(L);
     int* d_poff = c->mem.alloc<int>(L + 1);
@@ -905,7 +931,7 @@ int create_ctx(int device, const wt_model_desc* d, const wt_intrinsics* intr, in
     upload(d_plk, c->pair_link.data(), c->NP, c->stream);
     upload(d_pow, c->pair_owner.data(), c->NP, c->stream);
     upload(d_s, c->s_diag.data(), L, c->stream);
-    c->dm = wt::DevModel{V, L, c->NP, K, d_v0, d_wg, d_wl, d_roff, d_ring, d_ring8, d_nbr,
+    c->dm = wt::DevModel{V, L, c->NP, K, d_v0, d_wg, d_wl, d_roff, d_ring, d_fan_nb, d_fan_code, d_nbr,
                          d_links, d_poff, d_pth, d_plk, d_pow, d_s, d_depth, max_depth, d_pe};
 
     alloc_arenas(c);

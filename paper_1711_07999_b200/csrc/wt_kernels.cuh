@@ -33,8 +33,10 @@ struct DevModel {
   const uchar4* wlink;     // skin links, 0xFF = unused
   const int* ring_off;     // [V+1] incident triangles of each vertex (CSR order)
   const int2* ring;        // (b,c) follow i in its triangle; bits 30-31 of b: position of i
-  const int2* ring8;       // [V*8] the same for vertices with <= 8 triangles, padded with x = -1;
-                           // x = -2 in slot 0: more than 8, use the CSR
+  const int* fan_nb;       // [V*8] distinct ring neighbours of vertices with <= 8 incident triangles
+                           // and <= 8 distinct neighbours (-1 padded); -2 in slot 0: use the CSR
+  const unsigned long long* fan_code;  // [V] byte t = incident triangle t (CSR order): rot | b << 2 | c << 5
+                                       // (b, c = fan_nb slots of the ring entry); rot 3 = no more triangles
   const int* nbr;          // [K][V] neighbour ELL, -1 padded
   const LinkDesc* links;   // [L]
   const int* pair_off;     // [L+1] dchain pairs of each link
@@ -527,70 +529,87 @@ static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState 
   st256(s.pv + i, out);
 }
 
+// One of eight register values by a 3-bit slot (a select tree, no local memory).
+__device__ __forceinline__ double pick8(const double (&a)[8], unsigned k) {
+  const double l0 = (k & 1u) ? a[1] : a[0], l1 = (k & 1u) ? a[3] : a[2];
+  const double l2 = (k & 1u) ? a[5] : a[4], l3 = (k & 1u) ? a[7] : a[6];
+  const double m0 = (k & 2u) ? l1 : l0, m1 = (k & 2u) ? l3 : l2;
+  return (k & 4u) ? m1 : m0;
+}
+
+// acc += (f1 - f0) x (f2 - f0) for one incident triangle; (b, c) follow i in
+// the triangle cyclically and rot is the position of i in it.
+__device__ __forceinline__ void add_cross(unsigned rot, double vx, double vy, double vz, double bx, double by,
+                                          double bz, double cx, double cy, double cz, double& ax, double& ay,
+                                          double& az) {
+  const double f0x = rot == 0 ? vx : (rot == 1 ? cx : bx), f1x = rot == 0 ? bx : (rot == 1 ? vx : cx),
+               f2x = rot == 0 ? cx : (rot == 1 ? bx : vx);
+  const double f0y = rot == 0 ? vy : (rot == 1 ? cy : by), f1y = rot == 0 ? by : (rot == 1 ? vy : cy),
+               f2y = rot == 0 ? cy : (rot == 1 ? by : vy);
+  const double f0z = rot == 0 ? vz : (rot == 1 ? cz : bz), f1z = rot == 0 ? bz : (rot == 1 ? vz : cz),
+               f2z = rot == 0 ? cz : (rot == 1 ? bz : vz);
+  const double ex = f1x - f0x, ey = f1y - f0y, ez = f1z - f0z;
+  const double fx = f2x - f0x, fy = f2y - f0y, fz = f2z - f0z;
+  ax += ey * fz - ez * fy;
+  ay += ez * fx - ex * fz;
+  az += ex * fy - ey * fx;
+}
+
 // Vertex normal exactly as skin() (skinmesh.cpp:125-139): per incident
 // triangle (f0, f1, f2) in CSR order, acc += (v1 - v0) x (v2 - v0), then
 // acc / |acc|; returns the PosedMesh valid flag (blend ok and |acc| > 1e-20).
 // Bitwise the reference's when compiled without FMA contraction (wt_exact.cu).
-#ifndef WT_NORM_GATHER
-#define WT_NORM_GATHER 4
-#endif
-#ifndef WT_NORM_MINB
-#define WT_NORM_MINB 2
-#endif
-constexpr int kNormGather = WT_NORM_GATHER;  // incident triangles gathered per round (divides 8)
-
+//
+// Fan path (all but a handful of vertices): the ring's triangles share their
+// vertices pairwise, so a vertex with six incident triangles has six distinct
+// neighbours, not twelve. Those are gathered once, all in flight together
+// (one 256-bit load each), and every triangle picks its two from registers
+// in CSR order -- half the L1 traffic of gathering per triangle, the same
+// arithmetic in the same order.
 __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* pv, int i, const double4& v,
                                               double& nx, double& ny, double& nz) {
   double ax = 0, ay = 0, az = 0;
-  // up to eight incident triangles straight from the padded table (no offset
-  // load first), else the CSR eight at a time; all gathers of a step in flight
-  const int4* r8 = reinterpret_cast<const int4*>(m.ring8 + 8 * static_cast<size_t>(i));
-  const int4 q01 = r8[0], q23 = r8[1], q45 = r8[2], q67 = r8[3];
-  const bool packed = q01.x != -2;
-  const int r0 = packed ? 0 : m.ring_off[i], r1 = packed ? 8 : m.ring_off[i + 1];
-  for (int r = r0; r < r1; r += 8) {
-    int2 bc[8];
-    if (packed) {
-      bc[0] = make_int2(q01.x, q01.y);
-      bc[1] = make_int2(q01.z, q01.w);
-      bc[2] = make_int2(q23.x, q23.y);
-      bc[3] = make_int2(q23.z, q23.w);
-      bc[4] = make_int2(q45.x, q45.y);
-      bc[5] = make_int2(q45.z, q45.w);
-      bc[6] = make_int2(q67.x, q67.y);
-      bc[7] = make_int2(q67.z, q67.w);
-    } else {
+  const ulonglong4 q = ld256(reinterpret_cast<const ulonglong4*>(m.fan_nb + 8 * static_cast<size_t>(i)));
+  const int id[8] = {static_cast<int>(q.x), static_cast<int>(q.x >> 32), static_cast<int>(q.y),
+                     static_cast<int>(q.y >> 32), static_cast<int>(q.z), static_cast<int>(q.z >> 32),
+                     static_cast<int>(q.w), static_cast<int>(q.w >> 32)};
+  if (id[0] != -2) {
+    const unsigned long long code = __ldg(m.fan_code + i);
+    double px[8], py[8], pz[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) bc[q] = r + q < r1 ? m.ring[r + q] : make_int2(-1, -1);
+    for (int k = 0; k < 8; ++k) {
+      const double4 g = id[k] >= 0 ? ld256(pv + id[k]) : v;  // padding slots load nothing
+      px[k] = g.x;
+      py[k] = g.y;
+      pz[k] = g.z;
     }
-    const int nq = packed ? 8 : min(8, r1 - r);
-    // two rounds of four triangles: 8 vertex gathers in flight per round
-    // (16 would need ~170 registers and one CTA per SM)
 #pragma unroll
-    for (int h = 0; h < 8; h += kNormGather) {
-      if (h >= nq || bc[h].x == -1) break;
-      double4 pb[kNormGather], pc[kNormGather];
+    for (int t = 0; t < 8; ++t) {
+      const unsigned byte = static_cast<unsigned>(code >> (8 * t)) & 0xFFu;
+      const unsigned rot = byte & 3u;
+      if (rot == 3u) break;
+      const unsigned b = (byte >> 2) & 7u, c = byte >> 5;
+      add_cross(rot, v.x, v.y, v.z, pick8(px, b), pick8(py, b), pick8(pz, b), pick8(px, c), pick8(py, c),
+                pick8(pz, c), ax, ay, az);
+    }
+  } else {
+    // many-triangle vertices: the CSR, four triangles' gathers in flight at a time
+    const int r0 = m.ring_off[i], r1 = m.ring_off[i + 1];
+    for (int r = r0; r < r1; r += 4) {
+      int2 bc[4];
+      double4 pb[4], pc[4];
 #pragma unroll
-      for (int q = 0; q < kNormGather; ++q) {
-        // -1 / -2 are sentinels (position bits 3: never a real entry); padding
-        // slots load nothing (predicated off, no L1 wavefront)
-        const bool ok = bc[h + q].x != -1;
-        pb[q] = ok ? ld256(pv + (bc[h + q].x & 0x3FFFFFFF)) : v;
-        pc[q] = ok ? ld256(pv + bc[h + q].y) : v;
+      for (int k = 0; k < 4; ++k) {
+        bc[k] = r + k < r1 ? m.ring[r + k] : make_int2(-1, -1);
+        const bool ok = bc[k].x != -1;
+        pb[k] = ok ? ld256(pv + (bc[k].x & 0x3FFFFFFF)) : v;
+        pc[k] = ok ? ld256(pv + bc[k].y) : v;
       }
 #pragma unroll
-      for (int q = 0; q < kNormGather; ++q) {
-        if (h + q >= nq || bc[h + q].x == -1) break;
-        // ring entry: b, c follow i cyclically; bits 30-31 of .x = position of i
-        const int rot = static_cast<int>(static_cast<unsigned>(bc[h + q].x) >> 30);
-        const double4& f0 = rot == 0 ? v : (rot == 1 ? pc[q] : pb[q]);
-        const double4& f1 = rot == 0 ? pb[q] : (rot == 1 ? v : pc[q]);
-        const double4& f2 = rot == 0 ? pc[q] : (rot == 1 ? pb[q] : v);
-        const double ex = f1.x - f0.x, ey = f1.y - f0.y, ez = f1.z - f0.z;
-        const double fx = f2.x - f0.x, fy = f2.y - f0.y, fz = f2.z - f0.z;
-        ax += ey * fz - ez * fy;
-        ay += ez * fx - ex * fz;
-        az += ex * fy - ey * fx;
+      for (int k = 0; k < 4; ++k) {
+        if (r + k >= r1) break;
+        add_cross(static_cast<unsigned>(bc[k].x) >> 30, v.x, v.y, v.z, pb[k].x, pb[k].y, pb[k].z, pc[k].x,
+                  pc[k].y, pc[k].z, ax, ay, az);
       }
     }
   }
@@ -607,6 +626,9 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
 // K2 normals (skinmesh.cpp:125-139) fused with K3a: back-face cull, projection
 // with lround semantics (association.cpp:29-37,49-51) and the bin histogram.
 
+#ifndef WT_NORM_MINB
+#define WT_NORM_MINB 2
+#endif
 template <bool B>
 static __global__ void __launch_bounds__(kVThreads, WT_NORM_MINB) k_normals(DevModel m, DevState s, DevIntr in,
                                                        int do_bucket, int zero_acc, int compute) {
