@@ -513,13 +513,15 @@ static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState 
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m.V) return;
+  const double4 wv = ld256(m.wgt + i);  // all loads first (the 256-bit loads keep program order)
   const double4 a = ld256(m.v0 + i);
   const double4 f = ld256(phi + i);
+  const uchar4 lk = m.wlink[i];
   const double rest[3] = {a.x + f.x, a.y + f.y, a.z + f.z};
   DQ raw;
   double sign[4];
   double4 out;
-  if (blend_vertex(s_off, ld256(m.wgt + i), m.wlink[i], raw, sign)) {
+  if (blend_vertex(s_off, wv, lk, raw, sign)) {
     double p[3];
     dq_transform_point(dq_normalize(raw), rest, p);
     out = make_double4(p[0], p[1], p[2], 1.0);
@@ -946,9 +948,11 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
 }
 
 // p~_i = mean of the observations won by vertex i; count in *cnt.
-__device__ __forceinline__ bool observed_mean(const unsigned long long* acc, int i, double* pt,
-                                              long long* cnt) {
-  const ulonglong4 q = ld256(reinterpret_cast<const ulonglong4*>(acc) + i);
+__device__ __forceinline__ ulonglong4 load_obs(const unsigned long long* acc, int i) {
+  return ld256(reinterpret_cast<const ulonglong4*>(acc) + i);
+}
+
+__device__ __forceinline__ bool observed_mean(const ulonglong4& q, double* pt, long long* cnt) {
   const ulonglong2 a01 = make_ulonglong2(q.x, q.y), a23 = make_ulonglong2(q.z, q.w);
   const long long c = static_cast<long long>(a23.y);
   *cnt = c;
@@ -1695,7 +1699,9 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
   double abs_r = 0.0, sum_phi = 0.0, max_phi = 0.0;
   long long observed = 0, singular = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
+    // every load of the vertex up front (the 256-bit loads keep program order)
     const double4 f = ld256(phi_in + i);
+    const ulonglong4 obs = load_obs(s.acc, i);
     const double ph[3] = {f.x, f.y, f.z};
     double nd[3] = {0.0, 0.0, 0.0};
     int ncount = 0;
@@ -1732,7 +1738,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
     double r = 0.0;
     double pt[3];
     long long cnt = 0;
-    if (observed_mean(s.acc, i, pt, &cnt)) {
+    if (observed_mean(obs, pt, &cnt)) {
       if (a.clean_acc) clear_acc(s.acc, i);
       const double4 v = ld256(s.pv + i);
       const float4 n = s.pn[i];
@@ -1810,7 +1816,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, De
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
     double pt[3];
     long long cnt = 0;
-    if (observed_mean(s.acc, i, pt, &cnt)) {
+    if (observed_mean(load_obs(s.acc, i), pt, &cnt)) {
       if (clean_acc) clear_acc(s.acc, i);
       const double4 v = ld256(s.pv + i);
       const float4 n = s.pn[i];
