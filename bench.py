@@ -68,6 +68,16 @@ def alg_bytes(kind: str, V: int, P: int, A: int, Vvis: int) -> float:
     }[kind]
 
 
+def ncu_traffic(config: str, kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` capture summarised in profiles/traffic.json (None if absent)."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text())[config][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -76,32 +86,61 @@ def env_int(name, default):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML
+    every 2 ms (nvidia-smi every 0.2 s where NVML is unavailable)."""
+
+    REASONS = {  # NVML clocks-event bit -> name
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, [reasons])
         self._stop = threading.Event()
         self._t = None
 
-    def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    def _nvml_sample(self, nv, h, mx):
+        sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+        bits = (nv.nvmlDeviceGetCurrentClocksEventReasons(h) if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons")
+                else nv.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+        self.samples.append((sm, mx, [n for b, n in self.REASONS.items() if bits & b]))
+
+    def _run_nvml(self, nv, h, mx):
+        while not self._stop.is_set():
+            try:
+                self._nvml_sample(nv, h, mx)
+            except Exception:
+                pass
+            self._stop.wait(0.002)
+
+    def _run_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                f = [x.strip() for x in out.split(",")]
+                if len(f) >= 6 and f[0].replace(".", "").isdigit():
+                    self.samples.append((float(f[0]), float(f[1]),
+                                         [names[k] for k in range(4) if f[2 + k].lower() == "active"]))
+            except Exception:
+                pass
+            self._stop.wait(0.2)
 
-        def run():
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-
-        self._t = threading.Thread(target=run, daemon=True)
+    def __enter__(self):
+        try:  # NVML initialised and sampled once before the timed region starts
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._nvml_sample(nv, h, mx)
+            target = lambda: self._run_nvml(nv, h, mx)  # noqa: E731
+        except Exception:
+            target = self._run_smi
+        self._t = threading.Thread(target=target, daemon=True)
         self._t.start()
         return self
 
@@ -112,13 +151,9 @@ class ClockSampler:
     def summary(self) -> dict:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 3 + k and s[3 + k].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted({r for s in self.samples for r in s[2]}), "samples": len(self.samples)}
 
 
 def make_workload(cfg_name: str):
@@ -425,7 +460,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                          "d2h_bytes_per_step": 32 * bundle.link_count, "l2": "not flushed inside the sequence"},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dk["achieved_gbs"], "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
-                     "traffic": None, "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"]},
+                     "traffic": ncu_traffic(args.config, dominant), "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"]},
         "frame_roofline": {"alg_bytes_per_frame": frame_bytes, "kernel_us_per_frame": frame_us,
                            "achieved": frame_bytes / (frame_us * 1e-6) / 1e9,
                            "frac": frame_bytes / (frame_us * 1e-6) / 1e9 / peak,
@@ -592,7 +627,7 @@ def run_batched(args, rank: int, world: int, local_rank: int) -> None:
                        "theta of every sequence"},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dk["achieved_gbs"], "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
-                     "traffic": None, "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"]},
+                     "traffic": ncu_traffic(args.config, dominant), "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"]},
         "frame_roofline": {"alg_bytes_per_frame": frame_bytes, "kernel_us_per_frame": frame_us,
                            "achieved": frame_bytes / (frame_us * 1e-6) / 1e9,
                            "frac": frame_bytes / (frame_us * 1e-6) / 1e9 / peak,
