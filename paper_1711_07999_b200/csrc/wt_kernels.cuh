@@ -33,10 +33,10 @@ struct DevModel {
   const uchar4* wlink;     // skin links, 0xFF = unused
   const int* ring_off;     // [V+1] incident triangles of each vertex (CSR order)
   const int2* ring;        // (b,c) follow i in its triangle; bits 30-31 of b: position of i
-  const int* fan_nb;       // [V*8] distinct ring neighbours of vertices with <= 8 incident triangles
-                           // and <= 8 distinct neighbours (-1 padded); -2 in slot 0: use the CSR
-  const unsigned long long* fan_code;  // [V] byte t = incident triangle t (CSR order): rot | b << 2 | c << 5
-                                       // (b, c = fan_nb slots of the ring entry); rot 3 = no more triangles
+  const int* fan_nb;       // [V*8] ring neighbours in fan order n_0..n_{k-1}, then n_0 again (k < 8),
+                           // -1 padded; -2 in slot 0: not a closed fan of <= 8 triangles, use the CSR
+  const unsigned long long* fan_code;  // [V] bits 2j..2j+1: rot of fan triangle j = (i, n_j, n_j+1);
+                                       // bits 16+3t..: fan position of CSR triangle t; bits 40..43: k
   const int* nbr;          // [K][V] neighbour ELL, -1 padded
   const LinkDesc* links;   // [L]
   const int* pair_off;     // [L+1] dchain pairs of each link
@@ -557,17 +557,36 @@ __device__ __forceinline__ void add_cross(unsigned rot, double vx, double vy, do
   az += ex * fy - ey * fx;
 }
 
+// The cross product (f1 - f0) x (f2 - f0) of one incident triangle, as add_cross.
+__device__ __forceinline__ void fan_cross(unsigned rot, double vx, double vy, double vz, double bx, double by,
+                                          double bz, double cx, double cy, double cz, double& ox, double& oy,
+                                          double& oz) {
+  const double f0x = rot == 0 ? vx : (rot == 1 ? cx : bx), f1x = rot == 0 ? bx : (rot == 1 ? vx : cx),
+               f2x = rot == 0 ? cx : (rot == 1 ? bx : vx);
+  const double f0y = rot == 0 ? vy : (rot == 1 ? cy : by), f1y = rot == 0 ? by : (rot == 1 ? vy : cy),
+               f2y = rot == 0 ? cy : (rot == 1 ? by : vy);
+  const double f0z = rot == 0 ? vz : (rot == 1 ? cz : bz), f1z = rot == 0 ? bz : (rot == 1 ? vz : cz),
+               f2z = rot == 0 ? cz : (rot == 1 ? bz : vz);
+  const double ex = f1x - f0x, ey = f1y - f0y, ez = f1z - f0z;
+  const double fx = f2x - f0x, fy = f2y - f0y, fz = f2z - f0z;
+  ox = ey * fz - ez * fy;
+  oy = ez * fx - ex * fz;
+  oz = ex * fy - ey * fx;
+}
+
 // Vertex normal exactly as skin() (skinmesh.cpp:125-139): per incident
 // triangle (f0, f1, f2) in CSR order, acc += (v1 - v0) x (v2 - v0), then
 // acc / |acc|; returns the PosedMesh valid flag (blend ok and |acc| > 1e-20).
 // Bitwise the reference's when compiled without FMA contraction (wt_exact.cu).
 //
-// Fan path (all but a handful of vertices): the ring's triangles share their
-// vertices pairwise, so a vertex with six incident triangles has six distinct
-// neighbours, not twelve. Those are gathered once, all in flight together
-// (one 256-bit load each), and every triangle picks its two from registers
-// in CSR order -- half the L1 traffic of gathering per triangle, the same
-// arithmetic in the same order.
+// Fan path (closed fans of <= 8 triangles: every vertex of the meshes here):
+// the k incident triangles of a closed, consistently wound fan are
+// (i, n_j, n_j+1) around the ring, so the k distinct neighbours are gathered
+// once, all in flight, one 256-bit load each (6 for 97 % of the vertices, not
+// the 12 a per-triangle gather makes). Each fan triangle's cross product is
+// formed from registers with static indices; only the CSR-order summation
+// picks them by fan position (a select tree), so the arithmetic and its order
+// are the reference's.
 __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* pv, int i, const double4& v,
                                               double& nx, double& ny, double& nz) {
   double ax = 0, ay = 0, az = 0;
@@ -577,22 +596,32 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
                      static_cast<int>(q.w), static_cast<int>(q.w >> 32)};
   if (id[0] != -2) {
     const unsigned long long code = __ldg(m.fan_code + i);
+    const int k = static_cast<int>(code >> 40) & 15;
     double px[8], py[8], pz[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const double4 g = id[k] >= 0 ? ld256(pv + id[k]) : v;  // padding slots load nothing
-      px[k] = g.x;
-      py[k] = g.y;
-      pz[k] = g.z;
+    for (int j = 0; j < 8; ++j) {
+      const double4 g = id[j] >= 0 ? ld256(pv + id[j]) : v;  // padding slots load nothing
+      px[j] = g.x;
+      py[j] = g.y;
+      pz[j] = g.z;
+    }
+    double cx[8], cy[8], cz[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int j1 = (j + 1) & 7;  // slot k holds n_0 again (k < 8); k = 8 wraps to slot 0
+      cx[j] = cy[j] = cz[j] = 0.0;
+      if (j < k) {
+        const unsigned rot = static_cast<unsigned>(code >> (2 * j)) & 3u;
+        fan_cross(rot, v.x, v.y, v.z, px[j], py[j], pz[j], px[j1], py[j1], pz[j1], cx[j], cy[j], cz[j]);
+      }
     }
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const unsigned byte = static_cast<unsigned>(code >> (8 * t)) & 0xFFu;
-      const unsigned rot = byte & 3u;
-      if (rot == 3u) break;
-      const unsigned b = (byte >> 2) & 7u, c = byte >> 5;
-      add_cross(rot, v.x, v.y, v.z, pick8(px, b), pick8(py, b), pick8(pz, b), pick8(px, c), pick8(py, c),
-                pick8(pz, c), ax, ay, az);
+      if (t >= k) break;
+      const unsigned f = static_cast<unsigned>(code >> (16 + 3 * t)) & 7u;
+      ax += pick8(cx, f);
+      ay += pick8(cy, f);
+      az += pick8(cz, f);
     }
   } else {
     // many-triangle vertices: the CSR, four triangles' gathers in flight at a time
@@ -628,11 +657,11 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
 // K2 normals (skinmesh.cpp:125-139) fused with K3a: back-face cull, projection
 // with lround semantics (association.cpp:29-37,49-51) and the bin histogram.
 
-#ifndef WT_NORM_MINB
-#define WT_NORM_MINB 2
-#endif
+// A batch is throughput-bound: three CTAs per SM (the register cap spills a
+// little, which costs less than the lost occupancy). A lone sequence is
+// latency-bound: two CTAs per SM, no spills.
 template <bool B>
-static __global__ void __launch_bounds__(kVThreads, WT_NORM_MINB) k_normals(DevModel m, DevState s, DevIntr in,
+static __global__ void __launch_bounds__(kVThreads, B ? 3 : 2) k_normals(DevModel m, DevState s, DevIntr in,
                                                        int do_bucket, int zero_acc, int compute) {
   pdl_entry();
   if constexpr (B) s = seq_state(s);
