@@ -118,3 +118,29 @@ def test_track_frames_match_reference(setup, mode):
         assert np.abs(th - rth).max() <= 1e-4, (f, np.abs(th - rth).max())
         assert np.abs(ph - rph).max() <= 2e-5, (f, np.abs(ph - rph).max())
         assert st.kin[-1].associated == pytest.approx(rst.kin[rst.n_kin - 1].associated, rel=2e-3)
+
+
+def test_associate_1080p_matches_reference():
+    """The C4 frame size (1920x1080, a 2M-pixel bucket CSR, 32-column
+    valid-pixel runs across 60 segments per row): the winner map and the
+    per-vertex counts are the reference's, pixel for pixel."""
+    from paper_1711_07999_b200.tracker import Intrinsics
+    b = humanoid(7000)
+    intr = Intrinsics.scaled(1920, 1080)
+    rm = ref.RefModel.from_bundle(b)
+    trk = Tracker(b, intr)
+    try:
+        depth, _ = rm.render_depth(theta_at(b, 5), intr.c())
+        th = theta_at(b, 4)
+        trk.load_depth(depth)
+        trk.skin(th)
+        g = trk.associate(5, 0.10)
+        rv, rn, rvalid = rm.skin(th)
+        pts, pvalid = ref.depth_to_cloud(intr.c(), depth)
+        r = ref.associate(intr.c(), rv, rn, rvalid, pts, pvalid, 5, 0.10)
+        valid_px = pvalid.astype(bool)
+        assert valid_px.sum() > 50_000
+        assert np.array_equal(g["winners"][valid_px], r["winners"][valid_px])
+        assert np.array_equal(g["count"], r["count"])
+    finally:
+        trk.close()
