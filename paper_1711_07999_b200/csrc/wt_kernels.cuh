@@ -1075,31 +1075,31 @@ __device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b
   double bi = row ? b[lane] : 0.0;
   double dinv = 1.0;
   int ok = 1;
-#pragma unroll 1
+  // Fully unrolled over the pivots: a[j] is this lane's entry of column j
+  // (static register indices, no shifting), and pivot k shuffles and updates
+  // only the trailing columns k+1..N-1 -- half the work of a rolled loop, the
+  // same operations on every entry that is read.
+#pragma unroll
   for (int k = 0; k < N; ++k) {
-    // a[t] holds this lane's entry of column k + t
-    const double dk = __shfl_sync(0xffffffffu, a[0], k);
+    const double dk = __shfl_sync(0xffffffffu, a[k], k);
     ok &= dk > 0.0 ? 1 : 0;  // uniform; padded pivots are 1
     const double inv = __drcp_rn(dk);
     const double zk = __shfl_sync(0xffffffffu, bi, k);
     const bool act = lane > k;
-    const double lik = a[0] * inv;
+    const double lik = a[k] * inv;
     if (lane == k) dinv = inv;
-    // Unpredicated: entries with k + t > lane (or lane <= k) are upper-
-    // triangle values no later pivot reads, so updating them is harmless;
-    // every entry that is read gets exactly the FMA the predicated form did.
+    // Unpredicated: entries with t > lane (or lane <= k) are upper-triangle
+    // values no later pivot reads, so updating them is harmless; every entry
+    // that is read gets exactly the FMA the predicated form did.
     double cj[N];
 #pragma unroll
-    for (int t = 1; t < N; ++t) cj[t] = __shfl_sync(0xffffffffu, a[0], k + t);  // A[k+t][k], unscaled
+    for (int t = k + 1; t < N; ++t) cj[t] = __shfl_sync(0xffffffffu, a[k], t);  // A[t][k], unscaled
 #pragma unroll
-    for (int t = 1; t < N; ++t) a[t] = __fma_rn(-lik, cj[t], a[t]);  // explicit FMA (exact unit)
+    for (int t = k + 1; t < N; ++t) a[t] = __fma_rn(-lik, cj[t], a[t]);  // explicit FMA (exact unit)
     if (act) {
       bi = __fma_rn(-lik, zk, bi);
       if (row) A[lane * lda + k] = lik;
     }
-#pragma unroll
-    for (int t = 0; t + 1 < N; ++t) a[t] = a[t + 1];
-    a[N - 1] = 0.0;
   }
   if (!ok) return 0;
   __syncwarp();
