@@ -476,6 +476,21 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "gpu_launches": args.steps * S * (nker + 1),
         "clocks": clk.summary(),
     }
+    if world == 1 and args.config == "c3" and not args.no_batch:
+        # the same workload as 64 concurrent sequences on this GPU (C5's
+        # per-GPU batch): where the per-vertex / per-pixel kernels become
+        # HBM-bound, so their roofline fraction is meaningful
+        bargs = argparse.Namespace(**{**vars(args), "config": "c5", "sequences": 64, "steps": 10, "warmup": 3})
+        b = run_batched(bargs, rank, world, local_rank, emit=False)
+        line["batch_c5"] = {
+            "workload": b["config"]["workload"], "value": b["value"], "unit": "frames/s",
+            "ms_per_step": b["ms_per_step"], "steps": bargs.steps, "step": b["config"]["step"],
+            "e2e": b["e2e"], "roofline": b["roofline"], "frame_roofline": b["frame_roofline"],
+            "kernels": {k: {"avg_us": v["avg_us"], "us_per_frame": v["us_per_frame"],
+                            "achieved_gbs": v["achieved_gbs"],
+                            "frac": (v["achieved_gbs"] or 0.0) / b["roofline"]["peak"]}
+                        for k, v in b["kernels"].items()},
+            "gpu_launches": b["gpu_launches"], "clocks": b["clocks"]}
     if world == 1 and not args.no_cpu_baseline:
         # a bounded CPU sample of the same workload: enough frames of the same
         # trajectory for ~cpu_seconds of reference work (rendered on the GPU)
@@ -488,8 +503,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         t_.close()
 
 
-def run_batched(args, rank: int, world: int, local_rank: int) -> None:
-    """C5: the rank's sequences tracked as one batch (wt_gpu_create_batch)."""
+def run_batched(args, rank: int, world: int, local_rank: int, emit: bool = True):
+    """C5: the rank's sequences tracked as one batch (wt_gpu_create_batch).
+    Prints the JSON line (emit) or returns it."""
     import ctypes as C
 
     import torch
@@ -641,9 +657,11 @@ def run_batched(args, rank: int, world: int, local_rank: int) -> None:
         "gpu_launches": args.steps * (n.value + 1),
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
     bt.close()
     renderer.close()
+    if emit:
+        print(json.dumps(line), flush=True)
+    return line
 
 
 def main() -> None:
@@ -656,6 +674,8 @@ def main() -> None:
     ap.add_argument("--sequences", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-batch", action="store_true",
+                    help="c3: skip the 64-sequence batch sub-measurement (batch_c5)")
     ap.add_argument("--streams", action="store_true",
                     help="c5: one Tracker + stream per sequence instead of one batch")
     args = ap.parse_args()

@@ -7,7 +7,7 @@ tag=${1:-r01}
 out=gpurun_out/$tag
 mkdir -p $out
 python bench.py --steps 30 --warmup 5 > $out/bench.json 2> $out/bench.err || exit 1
-cmd="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
+cmd="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-batch"
 $cmd > $out/plain.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv $cmd > $out/ncu_launches.log 2>&1
 pcmd="python tools/profile_frame.py c3 3"
