@@ -439,7 +439,7 @@ static __global__ void k_fk(DevModel m, DevState s) {
 // warp are row neighbours from at most two 32-column segments.
 
 constexpr int kIngestSeg = 256;
-constexpr int kRunAlign = 4;  // pixels per search warp of the single-sequence search (32 / 8)
+constexpr int kRunAlign = 4;  // valid-pixel runs padded to 4 entries (a batch search warp's pixels)
 
 template <bool B>
 static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const float* depth, double scale,
@@ -831,10 +831,10 @@ __device__ __forceinline__ double ring_lb2(int k, double atx, double aty, double
 __device__ __forceinline__ long long d2_key(double x) { return __double_as_longlong(x); }
 
 __device__ __forceinline__ void scan_span(const DevState& s, int e0, int e1, double px, double py, double pz,
-                                          double cut2, double& best_x, int& best_i) {
+                                          double cut2, double& best_x, int& best_i, int step = 1) {
   const long long ck = d2_key(cut2);
   long long bk = best_i < 0 ? LLONG_MAX : d2_key(best_x);
-  for (int e = e0; e < e1; ++e) {
+  for (int e = e0; e < e1; e += step) {
     const double4 it = ld256(s.items + e);
     const long long xk = d2_key(exact_d2(it, px, py, pz));
     const int vi = static_cast<int>(__double_as_longlong(it.w));
@@ -870,13 +870,22 @@ __device__ __forceinline__ void search_emit(const DevState& s, const SearchArgs&
 // is fixed from the phase-1 best, and the group's lanes scan the rows of the
 // (2K*+1)^2 box outside the core, G rows at a time.
 // Two instantiations (the result is the same exact minimum either way):
-//  - one sequence (latency-bound): K1 = 2, G = 8 -- a 5x5 core, five rows in
-//    flight per pixel;
-//  - a batch (L1-throughput-bound): K1 = 1, G = 4 -- a 3x3 core, which
-//    already closes most pixels (the nearest vertex is ~2 px-widths closer
-//    than lb(2)), so a pixel loads ~2.7x fewer bucket items.
-constexpr int kNearRingsSolo = 2, kSearchGroupSolo = 8;
-constexpr int kNearRingsBatch = 1, kSearchGroupBatch = 4;
+//  - one sequence (latency-bound): K1 = 2, G = 16, SPL = 3 -- a 5x5 core,
+//    three lanes per core row each taking every third item of the row's
+//    span, so a lane's dependent load chain is a third of the row (measured:
+//    C3 1747 -> 1937 frames/s against one lane per row, G = 8);
+//  - a batch (L1-throughput-bound): K1 = 1, G = 4, SPL = 1 -- a 3x3 core,
+//    which already closes ~89 % of the pixels (the nearest vertex is usually
+//    well inside lb(2)), so a pixel loads ~2.7x fewer bucket items; splitting
+//    rows there only costs issue slots (G = 8 / SPL = 2: -4 %).
+#ifndef WT_SEARCH_SOLO_G
+#define WT_SEARCH_SOLO_G 16
+#endif
+#ifndef WT_SEARCH_SOLO_SPL
+#define WT_SEARCH_SOLO_SPL 3
+#endif
+constexpr int kNearRingsSolo = 2, kSearchGroupSolo = WT_SEARCH_SOLO_G, kSearchSplitSolo = WT_SEARCH_SOLO_SPL;
+constexpr int kNearRingsBatch = 1, kSearchGroupBatch = 4, kSearchSplitBatch = 1;
 
 template <int G>
 __device__ __forceinline__ void group_min(double& bx, int& bi) {
@@ -891,7 +900,8 @@ __device__ __forceinline__ void group_min(double& bx, int& bi) {
   }
 }
 
-template <bool B, int NR = B ? kNearRingsBatch : kNearRingsSolo, int G = B ? kSearchGroupBatch : kSearchGroupSolo>
+template <bool B, int NR = B ? kNearRingsBatch : kNearRingsSolo, int G = B ? kSearchGroupBatch : kSearchGroupSolo,
+          int SPL = B ? kSearchSplitBatch : kSearchSplitSolo>
 static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
   pdl_entry();
   if constexpr (B) s = seq_state(s);
@@ -918,12 +928,14 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
     }
     double best_x = INFINITY;
     int best_i = -1;
-    if (act && sub <= 2 * K1) {
-      const int rr = pv - K1 + sub;
+    if (act && sub < (2 * K1 + 1) * SPL) {
+      // SPL lanes per core row, each scanning every SPL-th item of its span
+      const int rr = pv - K1 + sub / SPL;
       if (rr >= 0 && rr < a.H) {
         const int r = rr * a.W;
         const int c0 = max(pu - K1, 0), c1 = min(pu + K1, a.W - 1);
-        scan_span(s, __ldg(s.poff + r + c0), __ldg(s.poff + r + c1 + 1), px, py, pz, a.cut2, best_x, best_i);
+        scan_span(s, __ldg(s.poff + r + c0) + sub % SPL, __ldg(s.poff + r + c1 + 1), px, py, pz, a.cut2, best_x,
+                  best_i, SPL);
       }
     }
     group_min<G>(best_x, best_i);
