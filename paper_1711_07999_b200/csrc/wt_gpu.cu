@@ -141,6 +141,10 @@ struct wt_gpu_ctx {
   int cap_kin = 0, cap_shape = 0;
   wt::KinStat* h_kin = nullptr;
   wt::ShapeStat* h_shape = nullptr;
+  // host mirror of theta, read back with a tracked frame's stats (one round
+  // trip per frame); valid until the next API call on the context
+  double* h_theta = nullptr;
+  bool theta_mirror = false;
 
   // renderer (fp64 copies, lazily built)
   double* r_v0 = nullptr;
@@ -196,6 +200,7 @@ struct wt_gpu_ctx {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
     if (h_kin) cudaFreeHost(h_kin);
+    if (h_theta) cudaFreeHost(h_theta);
     if (h_shape) cudaFreeHost(h_shape);
     if (stream) cudaStreamDestroy(stream);
     if (arena) cudaFree(arena);
@@ -205,7 +210,8 @@ struct wt_gpu_ctx {
 namespace {
 
 template <class F>
-int guarded(wt_gpu_ctx* ctx, F&& f) {
+int guarded(wt_gpu_ctx* ctx, F&& f, bool keep_mirror = false) {
+  if (ctx && !keep_mirror) ctx->theta_mirror = false;  // any other call may move theta
   try {
     f();
     return WT_OK;
@@ -385,6 +391,7 @@ void alloc_arenas(wt_gpu_ctx* c) {
   c->cap_shape = kArenaShape;
   WT_CUDA(cudaMallocHost(&c->h_kin, sizeof(wt::KinStat) * c->cap_kin * c->nseq));
   WT_CUDA(cudaMallocHost(&c->h_shape, sizeof(wt::ShapeStat) * c->cap_shape * c->nseq));
+  WT_CUDA(cudaMallocHost(&c->h_theta, sizeof(double) * c->L));
 }
 
 template <class T>
@@ -1016,6 +1023,11 @@ int wt_gpu_set_state(wt_gpu_ctx* c, const double* theta, const double* phi, int3
 
 int wt_gpu_get_state(wt_gpu_ctx* c, double* theta, double* phi, int32_t* frame_index) {
   if (!c) return WT_EINVAL;
+  if (c->theta_mirror && !phi) {  // right after a tracked frame: theta came back with its stats
+    if (theta) std::memcpy(theta, c->h_theta, sizeof(double) * c->L);
+    if (frame_index) *frame_index = c->frame_index;
+    return WT_OK;
+  }
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
     if (theta)
@@ -1106,7 +1118,9 @@ int wt_gpu_track_loaded(wt_gpu_ctx* c, const wt_track_config* cfg, wt_frame_stat
       if (ns) WT_CUDA(cudaMemcpyAsync(c->h_shape, c->ds.shape_stats, sizeof(wt::ShapeStat) * ns,
                                       cudaMemcpyDeviceToHost, c->stream));
     }
+    WT_CUDA(cudaMemcpyAsync(c->h_theta, c->ds.theta, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
     WT_CUDA(cudaStreamSynchronize(c->stream));
+    c->theta_mirror = true;
     if (stats) {
       stats->frame = c->frame_index;
       stats->n_kin = nk;
