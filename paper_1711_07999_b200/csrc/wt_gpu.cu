@@ -190,6 +190,19 @@ struct wt_gpu_ctx {
   double* rec_buf = nullptr;                       // [cap_rec * L * 4] theta + joints
   int cap_rec = 0;
 
+  // per-frame API with a pinned host frame: the upload and ingest are forked
+  // onto up_stream inside the frame graph and joined before the first
+  // search, so they overlap the first skin / normals / bucket build
+  struct H2DGraph {
+    cudaGraph_t graph;       // kept: its memcpy node is re-pointed per launch
+    cudaGraphExec_t exec;
+    cudaGraphNode_t copy;
+  };
+  std::map<GraphKey, H2DGraph> h2d_graphs;
+  cudaStream_t up_stream = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  std::function<void()> before_search;  // the join, run once by the next enq_search
+
   ~wt_gpu_ctx() {
     for (int b = 0; b < 2; ++b) {
       if (seq_pinned[b]) cudaFreeHost(seq_pinned[b]);
@@ -197,6 +210,13 @@ struct wt_gpu_ctx {
       if (seq_ingest[b]) cudaEventDestroy(seq_ingest[b]);
     }
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (auto& kv : h2d_graphs) {
+      cudaGraphExecDestroy(kv.second.exec);
+      cudaGraphDestroy(kv.second.graph);
+    }
+    if (up_stream) cudaStreamDestroy(up_stream);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
     if (h_kin) cudaFreeHost(h_kin);
@@ -454,6 +474,11 @@ void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
 }
 
 void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, int* winners) {
+  if (c->before_search) {  // the frame's upload + ingest, forked off earlier in this graph
+    auto join = std::move(c->before_search);
+    c->before_search = nullptr;
+    join();
+  }
   wt::DevFrame f{c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid, c->bstride};
   wt::SearchArgs sa;
   sa.fx = c->din.fx;
@@ -649,6 +674,29 @@ void put_shape(const wt_gpu_ctx* c, int n, wt_shape_iter_stats* out, int cap, in
     out[k].mean_abs_r_before = h[k].mean_abs_r_before;
     out[k].mean_abs_r_after = h[k].mean_abs_r_after;
   }
+}
+
+
+// A tracked frame's results back on the host: the stats (FrameStats) and
+// theta (the host mirror), one synchronisation; then the frame counter.
+void frame_readback(wt_gpu_ctx* c, int nk, int ns, wt_frame_stats* stats) {
+  if (stats) {
+    if (nk) WT_CUDA(cudaMemcpyAsync(c->h_kin, c->ds.kin_stats, sizeof(wt::KinStat) * nk,
+                                    cudaMemcpyDeviceToHost, c->stream));
+    if (ns) WT_CUDA(cudaMemcpyAsync(c->h_shape, c->ds.shape_stats, sizeof(wt::ShapeStat) * ns,
+                                    cudaMemcpyDeviceToHost, c->stream));
+  }
+  WT_CUDA(cudaMemcpyAsync(c->h_theta, c->ds.theta, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
+  WT_CUDA(cudaStreamSynchronize(c->stream));
+  c->theta_mirror = true;
+  if (stats) {
+    stats->frame = c->frame_index;
+    stats->n_kin = nk;
+    stats->n_shape = ns;
+    if (stats->kin) put_kin(c, nk, stats->kin, stats->cap_kin);
+    if (stats->shape) put_shape(c, ns, stats->shape, stats->cap_shape);
+  }
+  ++c->frame_index;
 }
 
 // rows of `width` bytes, one per sequence arena, to / from a packed host array
@@ -1049,12 +1097,13 @@ int wt_gpu_get_state(wt_gpu_ctx* c, double* theta, double* phi, int32_t* frame_i
 }
 
 static void ingest(wt_gpu_ctx* c, const float* depth_dev, double scale, const double* cloud_dev,
-                   const uint8_t* valid_dev) {
+                   const uint8_t* valid_dev, cudaStream_t st = nullptr) {
   // batch: depth_dev / cloud_dev / valid_dev are the arena buffers (same stride)
-  if (c->nseq == 1) WT_CUDA(cudaMemsetAsync(c->d_nvalid, 0, sizeof(int), c->stream));
-  else WT_CUDA(cudaMemset2DAsync(c->d_nvalid, static_cast<size_t>(c->bstride), 0, sizeof(int), c->nseq, c->stream));
+  if (!st) st = c->stream;
+  if (c->nseq == 1) WT_CUDA(cudaMemsetAsync(c->d_nvalid, 0, sizeof(int), st));
+  else WT_CUDA(cudaMemset2DAsync(c->d_nvalid, static_cast<size_t>(c->bstride), 0, sizeof(int), c->nseq, st));
   const int segs = (c->din.W + wt::kIngestSeg - 1) / wt::kIngestSeg;
-  (c->nseq > 1 ? wt::k_ingest<true> : wt::k_ingest<false>)<<<dim3(segs * c->din.H, c->nseq), wt::kIngestSeg, 0, c->stream>>>(
+  (c->nseq > 1 ? wt::k_ingest<true> : wt::k_ingest<false>)<<<dim3(segs * c->din.H, c->nseq), wt::kIngestSeg, 0, st>>>(
       c->din, depth_dev, scale, cloud_dev, valid_dev, c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid, c->bstride);
   check_launch();
 }
@@ -1111,24 +1160,7 @@ int wt_gpu_track_loaded(wt_gpu_ctx* c, const wt_track_config* cfg, wt_frame_stat
     });
     c->fk_valid = true;
     c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
-    const int nk = cfg->kin.iterations, ns = shape_now ? cfg->shape.iterations : 0;
-    if (stats) {
-      if (nk) WT_CUDA(cudaMemcpyAsync(c->h_kin, c->ds.kin_stats, sizeof(wt::KinStat) * nk,
-                                      cudaMemcpyDeviceToHost, c->stream));
-      if (ns) WT_CUDA(cudaMemcpyAsync(c->h_shape, c->ds.shape_stats, sizeof(wt::ShapeStat) * ns,
-                                      cudaMemcpyDeviceToHost, c->stream));
-    }
-    WT_CUDA(cudaMemcpyAsync(c->h_theta, c->ds.theta, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
-    WT_CUDA(cudaStreamSynchronize(c->stream));
-    c->theta_mirror = true;
-    if (stats) {
-      stats->frame = c->frame_index;
-      stats->n_kin = nk;
-      stats->n_shape = ns;
-      if (stats->kin) put_kin(c, nk, stats->kin, stats->cap_kin);
-      if (stats->shape) put_shape(c, ns, stats->shape, stats->cap_shape);
-    }
-    ++c->frame_index;
+    frame_readback(c, cfg->kin.iterations, shape_now ? cfg->shape.iterations : 0, stats);
   });
 }
 
@@ -1335,11 +1367,94 @@ int wt_gpu_joint_positions(wt_gpu_ctx* c, double* joints_out) {
   });
 }
 
+namespace {
+bool pinned_host(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// One frame from a pinned host depth image: the frame graph forks the upload
+// and ingest onto copy_stream at its start and joins them before the first
+// search; only the search and what follows need the frame.
+void track_frame_overlapped(wt_gpu_ctx* c, const float* depth, double scale, const wt_track_config* cfg,
+                            bool shape_now) {
+  if (!c->up_stream) WT_CUDA(cudaStreamCreateWithFlags(&c->up_stream, cudaStreamNonBlocking));
+  if (!c->fork_ev) WT_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+  if (!c->join_ev) WT_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+  GraphKey key = track_key(c, cfg, shape_now, 4.0);
+  key.v.push_back(scale);
+  const size_t bytes = sizeof(float) * c->P;
+  auto it = c->h2d_graphs.find(key);
+  if (it == c->h2d_graphs.end()) {
+    cudaGraph_t g;
+    WT_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      WT_CUDA(cudaEventRecord(c->fork_ev, c->stream));
+      WT_CUDA(cudaStreamWaitEvent(c->up_stream, c->fork_ev, 0));
+      WT_CUDA(cudaMemcpyAsync(c->d_depth, depth, bytes, cudaMemcpyHostToDevice, c->up_stream));
+      ingest(c, c->d_depth, scale, nullptr, nullptr, c->up_stream);
+      WT_CUDA(cudaEventRecord(c->join_ev, c->up_stream));
+      c->before_search = [c] { WT_CUDA(cudaStreamWaitEvent(c->stream, c->join_ev, 0)); };
+      enq_track(c, cfg, shape_now);
+      if (c->before_search) {  // no search in this frame: join at the end
+        c->before_search = nullptr;
+        WT_CUDA(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
+      }
+    } catch (...) {
+      c->before_search = nullptr;
+      cudaStreamEndCapture(c->stream, &g);
+      throw;
+    }
+    WT_CUDA(cudaStreamEndCapture(c->stream, &g));
+    size_t n = 0;
+    WT_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    WT_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+    cudaGraphNode_t cp = nullptr;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      WT_CUDA(cudaGraphNodeGetType(nd, &t));
+      if (t == cudaGraphNodeTypeMemcpy) cp = nd;
+    }
+    if (!cp) fail(WT_ECUDA, "frame graph: upload node not found");
+    cudaGraphExec_t ex;
+    WT_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    it = c->h2d_graphs.emplace(key, wt_gpu_ctx::H2DGraph{g, ex, cp}).first;
+  } else {
+    WT_CUDA(cudaGraphExecMemcpyNodeSetParams1D(it->second.exec, it->second.copy, c->d_depth, depth, bytes,
+                                               cudaMemcpyHostToDevice));
+  }
+  WT_CUDA(cudaGraphLaunch(it->second.exec, c->stream));
+}
+}  // namespace
+
 int wt_gpu_track_frame(wt_gpu_ctx* c, const float* depth, double depth_scale,
                        const wt_track_config* cfg, wt_frame_stats* stats) {
-  const int rc = wt_gpu_load_depth(c, depth, depth_scale);
-  if (rc != WT_OK) return rc;
-  return wt_gpu_track_loaded(c, cfg, stats);
+  if (!c || !depth || !cfg) return WT_EINVAL;
+  if (c->nseq != 1 || getenv("WT_NO_H2D_OVERLAP") || !pinned_host(depth)) {
+    const int rc = wt_gpu_load_depth(c, depth, depth_scale);
+    if (rc != WT_OK) return rc;
+    return wt_gpu_track_loaded(c, cfg, stats);
+  }
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    check_assoc(&cfg->assoc);
+    if (cfg->kin.iterations < 0 || cfg->shape.iterations < 0) fail(WT_EINVAL, "negative iteration count");
+    const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
+                           (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
+    ensure_stats(c, cfg->kin.iterations, cfg->shape.iterations);
+    const int start = c->cur;
+    c->frame_loaded = true;
+    c->frame_on_rays = true;
+    track_frame_overlapped(c, depth, depth_scale, cfg, shape_now);
+    c->fk_valid = true;
+    c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
+    frame_readback(c, cfg->kin.iterations, shape_now ? cfg->shape.iterations : 0, stats);
+  });
 }
 
 int wt_gpu_track_frame_cloud(wt_gpu_ctx* c, const double* points, const uint8_t* valid,
