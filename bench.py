@@ -64,7 +64,7 @@ def alg_bytes(kind: str, V: int, P: int, A: int, Vvis: int) -> float:
         "pose_system": 4 * V + 61 * A,        # K6
         "pose_solve": 0,                      # K7 (+K0 FK): one CTA, latency only
         "shape_step": 81 * V,                 # K8
-        "shape_stats": 72 * V,
+        "shape_stats": 32 * V + 24 * A,       # sums of every vertex + (v, n) of the observed ones
         "fk": 0,
     }[kind]
 

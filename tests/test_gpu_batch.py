@@ -120,3 +120,32 @@ def test_batch_rejects_per_frame_calls():
     desc, keep = b.to_desc()
     assert lib.wt_gpu_create_batch(0, C.byref(desc), C.byref(intr.c()), 0, C.byref(bad)) == W.WT_EINVAL
     bt.close()
+
+
+def test_batch_vga_equals_independent_sequences():
+    """640x480 frames of the 25k-vertex humanoid, two sequences: the batched
+    search's fp32 prefilter (k_search<true>, float4 bucket items) must pick
+    exactly the exact search's winners -- theta, Phi and the statistics
+    stay bitwise those of the lone sequences."""
+    from .helpers import cfg as mkcfg, humanoid, intr640, theta_at
+    b = humanoid(25000)
+    intr = intr640()
+    c = mkcfg("dynamic")
+    th0 = np.stack([theta_at(b, 0), theta_at(b, 0, phase=0.7)])
+    bt = BatchTracker(b, intr, 2, init_theta=th0)
+    solo = [Tracker(b, intr, th0[s]) for s in range(2)]
+    try:
+        for f in range(1, 4):
+            frames = np.stack([solo[s].render_depth(theta_at(b, f, phase=0.7 * s), frame=f)[0] for s in range(2)])
+            bst = bt.track_frame(c, depth=frames)
+            for s in range(2):
+                st = solo[s].track_frame(c, depth=frames[s])
+                th_b, ph_b = bt.get_state(s)
+                th_s, ph_s, _ = solo[s].get_state()
+                assert np.array_equal(th_b, th_s), (f, s)
+                assert np.array_equal(ph_b, ph_s), (f, s)
+                assert [k.associated for k in bst[s].kin] == [k.associated for k in st.kin]
+    finally:
+        bt.close()
+        for t in solo:
+            t.close()
