@@ -198,7 +198,11 @@ int wt_gpu_load_cloud(wt_gpu_ctx* ctx, const double* points, const uint8_t* vali
 /* ---- the hot path ---------------------------------------------------------- */
 /* track_frame (tracker.cpp:54-68) on the loaded frame. stats may be NULL. */
 int wt_gpu_track_loaded(wt_gpu_ctx* ctx, const wt_track_config* cfg, wt_frame_stats* stats);
-/* load_depth + track_loaded. */
+/* load_depth + track_loaded. With a pinned host frame the upload and its
+ * unprojection run on a side stream inside the frame graph and are joined
+ * before the first correspondence search, so they overlap the first skin /
+ * normals / bucket build; theta comes back with the stats, so a
+ * wt_gpu_get_state(theta only) right after costs no device round trip. */
 int wt_gpu_track_frame(wt_gpu_ctx* ctx, const float* depth, double depth_scale,
                        const wt_track_config* cfg, wt_frame_stats* stats);
 /* load_cloud + track_loaded. */
