@@ -495,9 +495,17 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   // G lanes per valid pixel; at most P pixels (the list is padded per 32 columns)
   // one wave (5 CTAs per SM fit the registers); warps stride over the 4-pixel groups
   // (a batch shares the wave between its sequences)
-  const int G = c->nseq > 1 ? wt::kSearchGroupBatch : wt::kSearchGroupSolo;
+  // the narrow 3x3-core form pays once the batch makes the search
+  // throughput-bound; small batches stay latency-bound and keep the solo form
+  static const int narrow_from = getenv("WT_NARROW_SEARCH_FROM") ? atoi(getenv("WT_NARROW_SEARCH_FROM")) : 8;
+  const bool narrow = c->nseq > 1 && c->nseq >= narrow_from;
+  const int G = narrow ? wt::kSearchGroupBatch : wt::kSearchGroupSolo;
   const int grid = std::max(1, std::min(c->P * G / wt::kVThreads + 1, wave(c, 5 * 148, "SEARCH", 8.0)));
-  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_search<true> : wt::k_search<false>, dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
+  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? (narrow ? wt::k_search<true>
+                                              : wt::k_search<true, wt::kNearRingsSolo, wt::kSearchGroupSolo,
+                                                             wt::kSearchSplitSolo>)
+                                     : wt::k_search<false>,
+                         dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
   mark(c, K_SEARCH);
 }
 
