@@ -499,12 +499,16 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   // throughput-bound; small batches stay latency-bound and keep the solo form
   static const int narrow_from = getenv("WT_NARROW_SEARCH_FROM") ? atoi(getenv("WT_NARROW_SEARCH_FROM")) : 8;
   const bool narrow = c->nseq > 1 && c->nseq >= narrow_from;
-  const int G = narrow ? wt::kSearchGroupBatch : wt::kSearchGroupSolo;
+  const int G = narrow ? wt::kSearchGroupBatch : wt::kSearchGroupSolo;  // grid sizing
   const int grid = std::max(1, std::min(c->P * G / wt::kVThreads + 1, wave(c, 5 * 148, "SEARCH", 8.0)));
+  // a lone frame of more than 2^20 pixels (C4) has enough pixels in flight to
+  // be throughput-bound: one lane per core row, 8-lane groups (1080p: 572 ->
+  // 647 frames/s against the VGA form)
+  const bool big_frame = c->nseq == 1 && c->P > (1 << 20);
   WT_CUDA(wt::launch_pdl(c->nseq > 1 ? (narrow ? wt::k_search<true>
                                               : wt::k_search<true, wt::kNearRingsSolo, wt::kSearchGroupSolo,
                                                              wt::kSearchSplitSolo>)
-                                     : wt::k_search<false>,
+                                     : (big_frame ? wt::k_search<false, wt::kNearRingsSolo, 8, 1> : wt::k_search<false>),
                          dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
   mark(c, K_SEARCH);
 }
