@@ -194,9 +194,9 @@ struct wt_gpu_ctx {
   // onto up_stream inside the frame graph and joined before the first
   // search, so they overlap the first skin / normals / bucket build
   struct H2DGraph {
-    cudaGraph_t graph;       // kept: its memcpy node is re-pointed per launch
+    cudaGraph_t graph;                  // kept: its memcpy nodes are re-pointed per launch
     cudaGraphExec_t exec;
-    cudaGraphNode_t copy;
+    std::vector<cudaGraphNode_t> copy;  // the upload of sequence b's frame
   };
   std::map<GraphKey, H2DGraph> h2d_graphs;
   cudaStream_t up_stream = nullptr;
@@ -722,13 +722,14 @@ void copy_from_seqs(const wt_gpu_ctx* c, void* dst, size_t dpitch, const void* s
   }
 }
 
-void copy_to_seqs(const wt_gpu_ctx* c, void* dst, const void* src, size_t spitch, size_t width) {
+void copy_to_seqs(const wt_gpu_ctx* c, void* dst, const void* src, size_t spitch, size_t width,
+                  cudaStream_t st = nullptr, cudaMemcpyKind kind = cudaMemcpyDefault) {
   if (width == 0) return;
+  if (!st) st = c->stream;
   if (c->nseq == 1) {
-    WT_CUDA(cudaMemcpyAsync(dst, src, width, cudaMemcpyDefault, c->stream));
+    WT_CUDA(cudaMemcpyAsync(dst, src, width, kind, st));
   } else {
-    WT_CUDA(cudaMemcpy2DAsync(dst, static_cast<size_t>(c->bstride), src, spitch, width, c->nseq, cudaMemcpyDefault,
-                              c->stream));
+    WT_CUDA(cudaMemcpy2DAsync(dst, static_cast<size_t>(c->bstride), src, spitch, width, c->nseq, kind, st));
   }
 }
 
@@ -1407,7 +1408,9 @@ void track_frame_overlapped(wt_gpu_ctx* c, const float* depth, double scale, con
     try {
       WT_CUDA(cudaEventRecord(c->fork_ev, c->stream));
       WT_CUDA(cudaStreamWaitEvent(c->up_stream, c->fork_ev, 0));
-      WT_CUDA(cudaMemcpyAsync(c->d_depth, depth, bytes, cudaMemcpyHostToDevice, c->up_stream));
+      for (int b = 0; b < c->nseq; ++b)  // one 1D upload per sequence (re-pointable per launch)
+        WT_CUDA(cudaMemcpyAsync(seq_at(c->d_depth, c, b), depth + static_cast<size_t>(b) * c->P, bytes,
+                                cudaMemcpyHostToDevice, c->up_stream));
       ingest(c, c->d_depth, scale, nullptr, nullptr, c->up_stream);
       WT_CUDA(cudaEventRecord(c->join_ev, c->up_stream));
       c->before_search = [c] { WT_CUDA(cudaStreamWaitEvent(c->stream, c->join_ev, 0)); };
@@ -1426,19 +1429,27 @@ void track_frame_overlapped(wt_gpu_ctx* c, const float* depth, double scale, con
     WT_CUDA(cudaGraphGetNodes(g, nullptr, &n));
     std::vector<cudaGraphNode_t> nodes(n);
     WT_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
-    cudaGraphNode_t cp = nullptr;
+    std::vector<cudaGraphNode_t> cp(static_cast<size_t>(c->nseq), nullptr);
     for (cudaGraphNode_t nd : nodes) {
       cudaGraphNodeType t;
       WT_CUDA(cudaGraphNodeGetType(nd, &t));
-      if (t == cudaGraphNodeTypeMemcpy) cp = nd;
+      if (t != cudaGraphNodeTypeMemcpy) continue;
+      cudaMemcpy3DParms prm{};
+      WT_CUDA(cudaGraphMemcpyNodeGetParams(nd, &prm));
+      const long long off = static_cast<const char*>(prm.dstPtr.ptr) - reinterpret_cast<const char*>(c->d_depth);
+      const long long b = c->nseq > 1 ? off / c->bstride : 0;
+      if (b >= 0 && b < c->nseq) cp[static_cast<size_t>(b)] = nd;
     }
-    if (!cp) fail(WT_ECUDA, "frame graph: upload node not found");
+    for (cudaGraphNode_t nd : cp)
+      if (!nd) fail(WT_ECUDA, "frame graph: upload node not found");
     cudaGraphExec_t ex;
     WT_CUDA(cudaGraphInstantiate(&ex, g, 0));
     it = c->h2d_graphs.emplace(key, wt_gpu_ctx::H2DGraph{g, ex, cp}).first;
-  } else {
-    WT_CUDA(cudaGraphExecMemcpyNodeSetParams1D(it->second.exec, it->second.copy, c->d_depth, depth, bytes,
-                                               cudaMemcpyHostToDevice));
+  } else {  // re-point the uploads at this call's host frames
+    for (int b = 0; b < c->nseq; ++b)
+      WT_CUDA(cudaGraphExecMemcpyNodeSetParams1D(it->second.exec, it->second.copy[static_cast<size_t>(b)],
+                                                 seq_at(c->d_depth, c, b), depth + static_cast<size_t>(b) * c->P,
+                                                 bytes, cudaMemcpyHostToDevice));
   }
   WT_CUDA(cudaGraphLaunch(it->second.exec, c->stream));
 }
@@ -1907,6 +1918,30 @@ int wt_gpu_batch_stats(wt_gpu_ctx* c, wt_frame_stats* stats) {
 
 int wt_gpu_batch_track(wt_gpu_ctx* c, const float* depth, double depth_scale, const wt_track_config* cfg,
                        wt_frame_stats* stats) {
+  if (c && depth && cfg && c->nseq > 1 && !getenv("WT_NO_H2D_OVERLAP") && pinned_host(depth)) {
+    // pinned host frames: the uploads overlap the batch's first skin /
+    // normals / bucket build inside the frame graph (track_frame_overlapped)
+    int rc = guarded(c, [&] {
+      WT_CUDA(cudaSetDevice(c->device));
+      check_assoc(&cfg->assoc);
+      if (cfg->kin.iterations < 0 || cfg->shape.iterations < 0) fail(WT_EINVAL, "negative iteration count");
+      const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
+                             (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
+      ensure_stats(c, cfg->kin.iterations, cfg->shape.iterations);
+      const int start = c->cur;
+      c->frame_loaded = true;
+      c->frame_on_rays = true;
+      track_frame_overlapped(c, depth, depth_scale, cfg, shape_now);
+      c->fk_valid = true;
+      c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
+      c->last_nk = cfg->kin.iterations;
+      c->last_ns = shape_now ? cfg->shape.iterations : 0;
+      ++c->frame_index;
+    });
+    if (rc == WT_OK && stats) rc = wt_gpu_batch_stats(c, stats);
+    if (rc == WT_OK) rc = wt_gpu_sync(c);
+    return rc;
+  }
   int rc = wt_gpu_batch_load_depth(c, depth, depth_scale);
   if (rc == WT_OK) rc = wt_gpu_batch_track_async(c, cfg);
   if (rc == WT_OK && stats) rc = wt_gpu_batch_stats(c, stats);

@@ -50,3 +50,37 @@ def test_pinned_track_frame_equals_loaded(mode):
     finally:
         a.close()
         o.close()
+
+
+def test_pinned_batch_track_equals_loaded():
+    """wt_gpu_batch_track with pinned host frames (the [n][H][W] upload forked
+    inside the batch frame graph, its 2D memcpy node re-pointed per call)
+    tracks exactly like batch load_depth + track_async."""
+    import torch
+    from paper_1711_07999_b200.tracker import BatchTracker
+    b = humanoid(7000)
+    intr = intr320()
+    c = cfg("dynamic")
+    n = 3
+    th0 = np.stack([theta_at(b, 0, phase=0.5 * s) for s in range(n)])
+    ref_t = Tracker(b, intr, th0[0])
+    a = BatchTracker(b, intr, n, init_theta=th0)
+    o = BatchTracker(b, intr, n, init_theta=th0)
+    L = W.lib()
+    try:
+        for f in range(1, 4):
+            frames = np.stack([ref_t.render_depth(theta_at(b, f, phase=0.5 * s), frame=f)[0] for s in range(n)])
+            pinned = torch.from_numpy(np.ascontiguousarray(frames, dtype=np.float32)).pin_memory()
+            a.track_frame(c, depth=frames)
+            stats = (W.FrameStatsC * n)(*[W.FrameStatsC(0, 0, 0, 64, 32, 0, o._kin[s], o._shape[s]) for s in range(n)])
+            W.check(L.wt_gpu_batch_track(o._ctx, pinned.data_ptr(), 1.0, C.byref(c.c()), stats), o._ctx)
+            for s in range(n):
+                th_a, ph_a = a.get_state(s)
+                th_o, ph_o = o.get_state(s)
+                assert np.array_equal(th_a, th_o), (f, s)
+                assert np.array_equal(ph_a, ph_o), (f, s)
+                assert stats[s].n_kin == c.kin.iterations
+    finally:
+        ref_t.close()
+        a.close()
+        o.close()
