@@ -7,6 +7,9 @@
 // (device sin/cos of theta/2 may still differ from libm by an ulp).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "wt_kernels.cuh"
 
 namespace wt {
@@ -18,13 +21,22 @@ void raster_launch(cudaStream_t st, int T, const double* vpos, const int* tri, d
 // nseq: sequences of a batch (gridDim.y), see seq_state in wt_kernels.cuh
 void launch_skin(cudaStream_t st, int grid, int nseq, int L, const DevModel& m, const DevState& s,
                  const double4* phi) {
-  launch_pdl(nseq > 1 ? k_skin<true> : k_skin<false>, dim3(grid, nseq), dim3(kVThreads), sizeof(double) * 8 * L, st,
+  // a batch of 16+ sequences: several vertices per thread, so the grid is a
+  // few waves of longer-lived CTAs instead of thousands of short ones
+  // (C5: 110 -> 95 us per launch)
+  const int vpt = std::max(1, std::min(4, nseq / 16));
+  const int g = (grid + vpt - 1) / vpt;
+  launch_pdl(nseq > 1 ? k_skin<true> : k_skin<false>, dim3(g, nseq), dim3(kVThreads), sizeof(double) * 8 * L, st,
              m, s, phi);
 }
 
 void launch_normals(cudaStream_t st, int grid, int nseq, const DevModel& m, const DevState& s, const DevIntr& in,
                     int do_bucket, int zero_acc, int compute) {
-  launch_pdl(nseq > 1 ? k_normals<true> : k_normals<false>, dim3(grid, nseq), dim3(kVThreads), 0, st, m, s, in, do_bucket, zero_acc, compute);
+  // a batch of 16+ sequences: up to 8 vertices per thread (C5: 366 -> 311 us)
+  const int vpt = std::max(1, std::min(8, nseq / 8));
+  const int g = (grid + vpt - 1) / vpt;
+  launch_pdl(nseq > 1 ? k_normals<true> : k_normals<false>, dim3(g, nseq), dim3(kVThreads), 0, st, m, s, in,
+             do_bucket, zero_acc, compute);
 }
 
 void launch_fk(cudaStream_t st, int nseq, const DevModel& m, const DevState& s) {

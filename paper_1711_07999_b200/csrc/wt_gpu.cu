@@ -468,8 +468,9 @@ void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
   WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_pixoff<true> : wt::k_pixoff<false>, dim3((c->din.H + 7) / 8, c->nseq), dim3(wt::kVThreads), 0, c->stream, s,
                          c->din.W, c->din.H));
   mark(c, K_SCATTER);
-  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_scatter<true> : wt::k_scatter<false>, dim3(vgrid(std::max(c->V, c->din.H)), c->nseq), dim3(wt::kVThreads), 0,
-                         c->stream, c->dm, s, c->din.H));
+  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_scatter<true> : wt::k_scatter<false>,
+                         dim3(vgrid(std::max(c->V, c->din.H)), c->nseq), dim3(wt::kVThreads), 0, c->stream, c->dm, s,
+                         c->din.H));
   mark(c, K_SCATTER);
 }
 

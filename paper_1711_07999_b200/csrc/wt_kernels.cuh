@@ -503,16 +503,9 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
 // ---------------------------------------------------------------------------
 // K1 skinning: v = normalize(blend)(v0 + phi) (skinmesh.cpp:112-121).
 
-template <bool B>
-static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, const double4* phi) {
-  pdl_entry();
-  if constexpr (B) s = seq_state(s);
-  if constexpr (B) phi = seq_ptr(phi, seq_off(s.bstride));
-  extern __shared__ double s_off[];
-  load_offsets(m, s, s_off);
-  __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m.V) return;
+// One vertex: offsets in shared memory, every load issued before the arithmetic.
+__device__ __forceinline__ void skin_vertex(const DevModel& m, const DevState& s, const double4* phi,
+                                            const double* s_off, int i) {
   const double4 wv = ld256(m.wgt + i);  // all loads first (the 256-bit loads keep program order)
   const double4 a = ld256(m.v0 + i);
   const double4 f = ld256(phi + i);
@@ -529,6 +522,19 @@ static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState 
     out = make_double4(rest[0], rest[1], rest[2], 0.0);  // placeholder, excluded downstream
   }
   st256(s.pv + i, out);
+}
+
+template <bool B>
+static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, const double4* phi) {
+  pdl_entry();
+  if constexpr (B) s = seq_state(s);
+  if constexpr (B) phi = seq_ptr(phi, seq_off(s.bstride));
+  extern __shared__ double s_off[];
+  load_offsets(m, s, s_off);
+  __syncthreads();
+  // grid-stride: a batch launches fewer, longer-lived CTAs per sequence
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x)
+    skin_vertex(m, s, phi, s_off, i);
 }
 
 // One of eight register values by a 3-bit slot (a select tree, no local memory).
@@ -665,8 +671,8 @@ static __global__ void __launch_bounds__(kVThreads, B ? 3 : 2) k_normals(DevMode
                                                        int do_bucket, int zero_acc, int compute) {
   pdl_entry();
   if constexpr (B) s = seq_state(s);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m.V) {
+  // grid-stride: a batch launches fewer, longer-lived CTAs per sequence
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
     const double4 v = ld256(s.pv + i);
     const double vx = v.x, vy = v.y, vz = v.z;
     double nx = 0, ny = 0, nz = 0;
@@ -769,11 +775,8 @@ static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, 
 // K3c: scatter into pixel order (association.cpp:60-66; unordered within a
 // pixel -- the winner rule is a lexicographic (d^2, index) minimum, so bucket
 // order never changes a result). Clears the row counts for the next pass.
-template <bool B>
-static __global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevState s, int H) {
-  pdl_entry();
-  if constexpr (B) s = seq_state(s);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// One vertex (or row counter) of the scatter.
+__device__ __forceinline__ void scatter_vertex(const DevModel& m, const DevState& s, int H, int i) {
   if (i < H) s.row_cnt[i] = 0;
   if (i >= m.V) return;
   const int pix = s.vpix[i];
@@ -785,6 +788,17 @@ static __global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevSta
   st256(s.items + __ldg(s.poff + pix) + atomicSub(&s.pix_cnt[pix], 1) - 1,
         make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(i))));
 }
+
+template <bool B>
+static __global__ void __launch_bounds__(kVThreads) k_scatter(DevModel m, DevState s, int H) {
+  pdl_entry();
+  if constexpr (B) s = seq_state(s);
+  const int n = max(m.V, H);
+  // grid-stride: a batch launches fewer, longer-lived CTAs per sequence
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    scatter_vertex(m, s, H, i);
+}
+
 
 // ---------------------------------------------------------------------------
 // K4 + K5: windowed nearest-vertex search (associate_winners,
