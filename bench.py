@@ -157,11 +157,16 @@ class ClockSampler:
                 "reasons": sorted({r for s in self.samples for r in s[2]}), "samples": len(self.samples)}
 
 
+# the humanoid 1.6 m from the camera: ~40k valid pixels per 640x480 frame
+# (acceptance.cpp:694-700 brings its biped closer the same way)
+SUBJECT_DEPTH = 1.6
+
+
 def make_workload(cfg_name: str):
     from paper_1711_07999_b200.model import make_humanoid
     from paper_1711_07999_b200.tracker import AssocConfig, Intrinsics, KinSolverConfig, ShapeSolverConfig, TrackConfig
     W, H, nv, mode, kits, sits = CONFIGS[cfg_name]
-    bundle = make_humanoid(nv)
+    bundle = make_humanoid(nv, depth=SUBJECT_DEPTH)
     intr = Intrinsics.scaled(W, H)
     cfg = TrackConfig(mode=mode, kin=KinSolverConfig(iterations=kits), shape=ShapeSolverConfig(iterations=max(sits, 1)),
                       assoc=AssocConfig())
