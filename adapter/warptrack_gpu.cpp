@@ -3,9 +3,12 @@
 // status codes back onto the reference's exception types (errors.hpp).
 #include "warptrack_gpu.hpp"
 
+#include <cstdint>
+#include <cstring>
+#include <list>
 #include <mutex>
 #include <string>
-#include <unordered_map>
+#include <type_traits>
 
 #include "warptrack/errors.hpp"
 #include "wt_gpu.h"
@@ -157,13 +160,25 @@ struct DescArrays {
   }
 };
 
-void flatten(const CloudFrame& f, std::vector<double>& pts) {
-  pts.resize(3 * f.points.size());
-  for (std::size_t i = 0; i < f.points.size(); ++i) {
-    pts[3 * i] = f.points[i].x();
-    pts[3 * i + 1] = f.points[i].y();
-    pts[3 * i + 2] = f.points[i].z();
+// The CloudFrame's points as the packed [P][3] doubles the C-ABI takes: a
+// Vec3 (Eigen::Vector3d) is three unpadded doubles, so the vector's storage
+// already is that array and nothing is copied; otherwise it is flattened.
+const double* packed_points(const CloudFrame& f, std::vector<double>& tmp) {
+  if constexpr (sizeof(Vec3) == 3 * sizeof(double) && std::is_standard_layout_v<Vec3>) {
+    if (!f.points.empty()) return f.points.data()->data();
   }
+  tmp.resize(3 * f.points.size());
+  for (std::size_t i = 0; i < f.points.size(); ++i) {
+    tmp[3 * i] = f.points[i].x();
+    tmp[3 * i + 1] = f.points[i].y();
+    tmp[3 * i + 2] = f.points[i].z();
+  }
+  return tmp.data();
+}
+
+// Does track_frame run optimize_shape this frame (tracker.cpp:63-66)?
+bool shape_runs(const TrackConfig& cfg, int frame_index) {
+  return cfg.mode == TrackMode::dynamic || (cfg.mode == TrackMode::shape_match && frame_index == 0);
 }
 
 }  // namespace
@@ -175,34 +190,45 @@ Sequence::Sequence(const Skeleton& skeleton, const SkinnedMesh& mesh, const Intr
   check(wt_gpu_create(device, &d.desc, &ci, &ctx_), nullptr, "wt_gpu_create");
 }
 
-Sequence::~Sequence() { wt_gpu_destroy(ctx_); }
+Sequence::~Sequence() {
+  wt_gpu_destroy(ctx_);
+  wt_gpu_host_free(pinned_depth_);
+}
 
 void Sequence::upload(const TrackerState& state) {
   if (state.theta.size() != links_) throw LengthMismatch("theta size differs from the skeleton");
-  std::vector<double> th(static_cast<std::size_t>(links_)), ph;
+  std::vector<double> th(static_cast<std::size_t>(links_));
   for (int k = 0; k < links_; ++k) th[static_cast<std::size_t>(k)] = state.theta[k];
   const double* php = nullptr;
-  if (state.mesh.phi.size() == static_cast<std::size_t>(vertices_)) {
-    ph.resize(3 * static_cast<std::size_t>(vertices_));
-    for (int i = 0; i < vertices_; ++i)
-      for (int c = 0; c < 3; ++c) ph[3 * static_cast<std::size_t>(i) + c] = state.mesh.phi[static_cast<std::size_t>(i)][c];
-    php = ph.data();
+  const std::size_t V = static_cast<std::size_t>(vertices_);
+  if (state.mesh.phi.size() == V) {
+    bool same = phi_known_;
+    for (std::size_t i = 0; same && i < V; ++i)
+      for (int c = 0; c < 3; ++c) same = same && phi_mirror_[3 * i + c] == state.mesh.phi[i][c];
+    if (!same) {
+      phi_mirror_.resize(3 * V);
+      for (std::size_t i = 0; i < V; ++i)
+        for (int c = 0; c < 3; ++c) phi_mirror_[3 * i + c] = state.mesh.phi[i][c];
+      php = phi_mirror_.data();
+      phi_known_ = true;
+    }
   }
   check(wt_gpu_set_state(ctx_, th.data(), php, state.frame_index), ctx_, "wt_gpu_set_state");
 }
 
-void Sequence::download(TrackerState& state, bool with_phi) const {
-  std::vector<double> th(static_cast<std::size_t>(links_)), ph(with_phi ? 3 * static_cast<std::size_t>(vertices_) : 0);
+void Sequence::download(TrackerState& state, bool with_phi) {
+  std::vector<double> th(static_cast<std::size_t>(links_));
+  const std::size_t V = static_cast<std::size_t>(vertices_);
+  if (with_phi) phi_mirror_.resize(3 * V);
   int32_t fi = 0;
-  check(wt_gpu_get_state(ctx_, th.data(), with_phi ? ph.data() : nullptr, &fi), ctx_, "wt_gpu_get_state");
+  check(wt_gpu_get_state(ctx_, th.data(), with_phi ? phi_mirror_.data() : nullptr, &fi), ctx_, "wt_gpu_get_state");
   state.theta.resize(links_);
   for (int k = 0; k < links_; ++k) state.theta[k] = th[static_cast<std::size_t>(k)];
   if (with_phi) {
-    state.mesh.phi.resize(static_cast<std::size_t>(vertices_));
-    for (int i = 0; i < vertices_; ++i)
-      state.mesh.phi[static_cast<std::size_t>(i)] =
-          Vec3(ph[3 * static_cast<std::size_t>(i)], ph[3 * static_cast<std::size_t>(i) + 1],
-               ph[3 * static_cast<std::size_t>(i) + 2]);
+    phi_known_ = true;
+    state.mesh.phi.resize(V);
+    for (std::size_t i = 0; i < V; ++i)
+      state.mesh.phi[i] = Vec3(phi_mirror_[3 * i], phi_mirror_[3 * i + 1], phi_mirror_[3 * i + 2]);
   }
   state.frame_index = fi;
 }
@@ -221,98 +247,177 @@ FrameStats collect(const wt_frame_stats& st, const std::vector<wt_kin_iter_stats
 FrameStats Sequence::track_frame(const CloudFrame& frame, const TrackConfig& cfg) {
   if (frame.width != intr_.width || frame.height != intr_.height)
     throw LengthMismatch("frame size differs from the intrinsics grid");
-  std::vector<double> pts;
-  flatten(frame, pts);
+  std::vector<double> tmp;
+  const double* pts = packed_points(frame, tmp);
   std::vector<wt_kin_iter_stats> k(static_cast<std::size_t>(std::max(cfg.kin.iterations, 1)));
   std::vector<wt_shape_iter_stats> s(static_cast<std::size_t>(std::max(cfg.shape.iterations, 1)));
   wt_frame_stats st{0, 0, 0, static_cast<int32_t>(k.size()), static_cast<int32_t>(s.size()), 0, k.data(), s.data()};
   const wt_track_config c = to_c(cfg);
-  check(wt_gpu_track_frame_cloud(ctx_, pts.data(), frame.valid.data(), &c, &st), ctx_, "wt_gpu_track_frame_cloud");
+  check(wt_gpu_track_frame_cloud(ctx_, pts, frame.valid.data(), &c, &st), ctx_, "wt_gpu_track_frame_cloud");
   return collect(st, k, s);
 }
 
 FrameStats Sequence::track_depth(const std::vector<float>& depth, double scale, const TrackConfig& cfg) {
   if (depth.size() != static_cast<std::size_t>(intr_.width) * intr_.height)
     throw LengthMismatch("depth image size differs from the intrinsics grid");
+  // staged in page-locked memory: the frame graph then uploads it on a side
+  // stream, overlapped with the first skin / normals / bucket build
+  if (!pinned_depth_) {
+    void* p = nullptr;
+    check(wt_gpu_host_alloc(sizeof(float) * depth.size(), &p), nullptr, "wt_gpu_host_alloc");
+    pinned_depth_ = static_cast<float*>(p);
+  }
+  std::memcpy(pinned_depth_, depth.data(), sizeof(float) * depth.size());
   std::vector<wt_kin_iter_stats> k(static_cast<std::size_t>(std::max(cfg.kin.iterations, 1)));
   std::vector<wt_shape_iter_stats> s(static_cast<std::size_t>(std::max(cfg.shape.iterations, 1)));
   wt_frame_stats st{0, 0, 0, static_cast<int32_t>(k.size()), static_cast<int32_t>(s.size()), 0, k.data(), s.data()};
   const wt_track_config c = to_c(cfg);
-  check(wt_gpu_track_frame(ctx_, depth.data(), scale, &c, &st), ctx_, "wt_gpu_track_frame");
+  check(wt_gpu_track_frame(ctx_, pinned_depth_, scale, &c, &st), ctx_, "wt_gpu_track_frame");
   return collect(st, k, s);
 }
 
 void Sequence::optimize_pose(const CloudFrame& frame, const KinSolverConfig& cfg, const AssocConfig& assoc,
                              std::vector<KinIterStats>* stats) {
-  std::vector<double> pts;
-  flatten(frame, pts);
-  check(wt_gpu_load_cloud(ctx_, pts.data(), frame.valid.data()), ctx_, "wt_gpu_load_cloud");
+  std::vector<double> tmp;
+  check(wt_gpu_load_cloud(ctx_, packed_points(frame, tmp), frame.valid.data()), ctx_, "wt_gpu_load_cloud");
   std::vector<wt_kin_iter_stats> k(static_cast<std::size_t>(std::max(cfg.iterations, 1)));
   int32_t n = 0;
   const wt_kin_config kc = to_c(cfg);
   const wt_assoc_config ac = to_c(assoc);
   check(wt_gpu_optimize_pose(ctx_, &kc, &ac, k.data(), static_cast<int32_t>(k.size()), &n), ctx_,
         "wt_gpu_optimize_pose");
-  if (stats) {
-    stats->clear();
+  if (stats)  // appended, as kinopt.cpp:153-169 push_back onto the caller's vector
     for (int i = 0; i < n; ++i) stats->push_back(from_c(k[static_cast<std::size_t>(i)]));
-  }
 }
 
 void Sequence::optimize_shape(const CloudFrame& frame, const ShapeSolverConfig& cfg, const AssocConfig& assoc,
                               std::vector<ShapeIterStats>* stats) {
-  std::vector<double> pts;
-  flatten(frame, pts);
-  check(wt_gpu_load_cloud(ctx_, pts.data(), frame.valid.data()), ctx_, "wt_gpu_load_cloud");
+  std::vector<double> tmp;
+  check(wt_gpu_load_cloud(ctx_, packed_points(frame, tmp), frame.valid.data()), ctx_, "wt_gpu_load_cloud");
   std::vector<wt_shape_iter_stats> s(static_cast<std::size_t>(std::max(cfg.iterations, 1)));
   int32_t n = 0;
   const wt_shape_config sc = to_c(cfg);
   const wt_assoc_config ac = to_c(assoc);
   check(wt_gpu_optimize_shape(ctx_, &sc, &ac, stats ? 1 : 0, s.data(), static_cast<int32_t>(s.size()), &n), ctx_,
         "wt_gpu_optimize_shape");
-  if (stats) {
-    stats->clear();
+  if (stats)  // appended after the caller's entries (shapeopt.cpp:56,112-129 use stats_base = size())
     for (int i = 0; i < n; ++i) stats->push_back(from_c(s[static_cast<std::size_t>(i)]));
-  }
 }
 
 // ---- free functions with the reference signatures ----------------------------------
 
 namespace {
-struct Cached {
-  std::unique_ptr<Sequence> seq;
+// What a cached device context was built from: the state's address plus the
+// identity of its model (a state at a reused address, or a different model
+// of the same size -- e.g. rigidify(bundle) -- does not match).
+struct ModelKey {
+  const TrackerState* state = nullptr;
+  const Skeleton* skeleton = nullptr;
+  const void* v0 = nullptr;
+  const void* weights = nullptr;
+  const void* triangles = nullptr;
+  const void* neighbors = nullptr;
+  std::size_t V = 0, T = 0, N = 0;
+  int L = 0;
+  std::uint64_t fingerprint = 0;
   Intrinsics intr;
+
+  bool operator==(const ModelKey& o) const {
+    return state == o.state && skeleton == o.skeleton && v0 == o.v0 && weights == o.weights &&
+           triangles == o.triangles && neighbors == o.neighbors && V == o.V && T == o.T && N == o.N && L == o.L &&
+           fingerprint == o.fingerprint && intr.fx == o.intr.fx && intr.fy == o.intr.fy && intr.cx == o.intr.cx &&
+           intr.cy == o.intr.cy && intr.width == o.intr.width && intr.height == o.intr.height;
+  }
+};
+
+// FNV-1a over the link offsets and up to 1024 evenly sampled vertices'
+// template positions and skin weights (cheap enough for every call).
+std::uint64_t fingerprint(const Skeleton& sk, const SkinnedMesh& m) {
+  std::uint64_t h = 1469598103934665603ull;
+  auto mix = [&h](const void* p, std::size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (std::size_t k = 0; k < n; ++k) h = (h ^ b[k]) * 1099511628211ull;
+  };
+  for (int j = 0; j < sk.link_count(); ++j) {
+    const Vec8 o = to_vec8(sk.link(j).parent_offset);
+    for (int c = 0; c < 8; ++c) {
+      const double x = o[c];
+      mix(&x, sizeof x);
+    }
+  }
+  const std::size_t V = m.v0.size(), step = V > 1024 ? V / 1024 : 1;
+  for (std::size_t i = 0; i < V; i += step) {
+    for (int c = 0; c < 3; ++c) {
+      const double x = m.v0[i][c];
+      mix(&x, sizeof x);
+    }
+    if (i < m.weights.size()) {
+      const VertexWeights& w = m.weights[i];
+      mix(&w.count, sizeof w.count);
+      for (int s = 0; s < w.count && s < 4; ++s) {
+        mix(&w.entry[static_cast<std::size_t>(s)].link, sizeof(int));
+        mix(&w.entry[static_cast<std::size_t>(s)].w, sizeof(double));
+      }
+    }
+  }
+  return h;
+}
+
+ModelKey key_of(const TrackerState& state, const Intrinsics& intr) {
+  ModelKey k;
+  k.state = &state;
+  k.skeleton = state.skeleton;
+  k.v0 = state.mesh.v0.data();
+  k.weights = state.mesh.weights.data();
+  k.triangles = state.mesh.triangles.data();
+  k.neighbors = state.mesh.neighbors.data();
+  k.V = state.mesh.v0.size();
+  k.T = state.mesh.triangles.size();
+  k.N = state.mesh.neighbors.size();
+  k.L = state.skeleton->link_count();
+  k.fingerprint = fingerprint(*state.skeleton, state.mesh);
+  k.intr = intr;
+  return k;
+}
+
+struct Cached {
+  ModelKey key;
+  std::unique_ptr<Sequence> seq;
 };
 std::mutex g_mu;
-std::unordered_map<const TrackerState*, Cached> g_cache;
+std::list<Cached> g_cache;  // most recently used first, at most kMaxCachedStates
 
 Sequence& sequence_for(const TrackerState& state, const Intrinsics& intr) {
   if (!state.skeleton) throw ValidationError("TrackerState has no skeleton");
+  const ModelKey key = key_of(state, intr);
   std::lock_guard<std::mutex> lock(g_mu);
-  Cached& c = g_cache[&state];
-  const bool same = c.seq && c.seq->vertex_count() == state.mesh.vertex_count() &&
-                    c.seq->link_count() == state.skeleton->link_count() && c.intr.fx == intr.fx &&
-                    c.intr.fy == intr.fy && c.intr.cx == intr.cx && c.intr.cy == intr.cy &&
-                    c.intr.width == intr.width && c.intr.height == intr.height;
-  if (!same) {
-    c.seq = std::make_unique<Sequence>(*state.skeleton, state.mesh, intr);
-    c.intr = intr;
+  for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+    if (it->key.state != &state) continue;
+    if (it->key == key) {
+      g_cache.splice(g_cache.begin(), g_cache, it);
+      return *g_cache.front().seq;
+    }
+    g_cache.erase(it);  // same address, different model: rebuild
+    break;
   }
-  return *c.seq;
+  g_cache.push_front(Cached{key, std::make_unique<Sequence>(*state.skeleton, state.mesh, intr)});
+  while (g_cache.size() > static_cast<std::size_t>(kMaxCachedStates)) g_cache.pop_back();
+  return *g_cache.front().seq;
 }
 }  // namespace
 
 void release(const TrackerState& state) {
   std::lock_guard<std::mutex> lock(g_mu);
-  g_cache.erase(&state);
+  g_cache.remove_if([&](const Cached& c) { return c.key.state == &state; });
 }
 
 FrameStats track_frame(TrackerState& state, const CloudFrame& frame, const Intrinsics& intr,
                        const TrackConfig& cfg) {
   Sequence& s = sequence_for(state, intr);
   s.upload(state);
+  const bool shape = shape_runs(cfg, state.frame_index);
   FrameStats fs = s.track_frame(frame, cfg);
-  s.download(state);
+  s.download(state, shape);  // phi only moved if optimize_shape ran
   return fs;
 }
 
@@ -342,6 +447,7 @@ TrackOutputs run_tracking(const ModelBundle& bundle, SequenceReader& reader, con
   const Intrinsics intr = reader.header().intrinsics();
   Sequence seq(bundle, intr);
   seq.upload(state);
+  const bool need_phi = static_cast<bool>(callback);
 
   TrackOutputs out;
   for (const Link& l : bundle.skeleton.links()) out.estimate.joint_names.push_back(l.name);
@@ -349,8 +455,9 @@ TrackOutputs run_tracking(const ModelBundle& bundle, SequenceReader& reader, con
   std::vector<double> joints(3 * static_cast<std::size_t>(L));
   for (int f = 0; f < reader.frame_count(); ++f) {
     const std::vector<float> depth = reader.read_depth(f);
+    const bool shape = shape_runs(cfg, state.frame_index);
     out.stats.push_back(seq.track_depth(depth, reader.header().depth_scale, cfg));
-    seq.download(state, static_cast<bool>(callback));
+    seq.download(state, need_phi && shape);
     check(wt_gpu_joint_positions(seq.handle(), joints.data()), seq.handle(), "wt_gpu_joint_positions");
     std::vector<Vec3> js(static_cast<std::size_t>(L));
     for (int j = 0; j < L; ++j)

@@ -29,9 +29,12 @@ class Sequence {
   Sequence(const Sequence&) = delete;
   Sequence& operator=(const Sequence&) = delete;
 
-  /// TrackerState <-> device (theta, mesh.phi, frame_index).
+  /// TrackerState <-> device (theta, mesh.phi, frame_index). Phi crosses
+  /// only when it differs from what the device holds (a host mirror of the
+  /// last synchronised Phi), so a caller that leaves state.mesh.phi alone
+  /// between frames pays no Phi upload.
   void upload(const TrackerState& state);
-  void download(TrackerState& state, bool with_phi = true) const;
+  void download(TrackerState& state, bool with_phi = true);
 
   FrameStats track_frame(const CloudFrame& frame, const TrackConfig& cfg);
   FrameStats track_depth(const std::vector<float>& depth, double scale, const TrackConfig& cfg);
@@ -48,13 +51,21 @@ class Sequence {
   wt_gpu_ctx* ctx_ = nullptr;
   int links_ = 0, vertices_ = 0;
   Intrinsics intr_;
+  std::vector<double> phi_mirror_;  // packed [V][3]: the device's Phi as of the last upload / download
+  bool phi_known_ = false;
+  float* pinned_depth_ = nullptr;   // page-locked staging: track_depth takes the overlapped upload path
 };
 
 /// Drop-in replacements with the reference signatures. Each call keeps a
-/// device context cached per TrackerState (keyed by its address, created
-/// from state.skeleton + state.mesh on first use) and synchronises the
-/// state's theta / phi / frame_index in and out, so the host TrackerState
-/// stays authoritative exactly as in the reference.
+/// device context cached per TrackerState, keyed by the state's address AND
+/// its model's identity (the skeleton pointer, the mesh arrays' addresses and
+/// sizes, and a fingerprint of sampled template vertices, skin weights and
+/// link offsets), so a new state at a reused address or a rigidified model
+/// gets its own upload. At most kMaxCachedStates contexts are kept (least
+/// recently used dropped). Each call synchronises theta / phi / frame_index
+/// in and out, so the host TrackerState stays authoritative exactly as in
+/// the reference (phi only moves when it changed, see Sequence::upload).
+constexpr int kMaxCachedStates = 16;
 FrameStats track_frame(TrackerState& state, const CloudFrame& frame, const Intrinsics& intr,
                        const TrackConfig& cfg);
 void optimize_pose(TrackerState& state, const CloudFrame& frame, const Intrinsics& intr,

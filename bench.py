@@ -7,19 +7,23 @@
 A step is one track_frame (tracker.cpp:54-68) on one synthetic depth frame:
 5 pose Gauss-Newton iterations + 2 surface iterations + optimize_shape's
 closing stats pass (dynamic mode), the BASELINE.json headline configuration
-C3 (640x480 depth, ~100k-vertex 20-link humanoid) unless --config says
-otherwise. Frames are rendered on the GPU (synthesize_frame semantics, no
-noise) from a sinusoidal joint trajectory before timing.
+C3 (640x480 depth, ~100k-vertex 20-link humanoid 1.6 m from the camera,
+~42k valid pixels) unless --config says otherwise. Frames are rendered on the
+GPU (synthesize_frame semantics, no noise) from a sinusoidal joint trajectory
+before timing.
 
 value: frames/s over all ranks with the depth frames already resident in
 HBM, each frame = device copy into the tracker + one graph launch, timed
 with CUDA events on the tracker's stream; L2 is flushed (256 MiB write)
 between frames, outside the timed spans. e2e: the same metric through the
-public per-frame API (Tracker.track_frame with a pinned host depth frame,
-stats read back, then theta read back), events bracketing each call.
+public per-frame C-ABI call (wt_gpu_track_frame with a pinned host depth
+frame, stats + theta read back), timed with the HOST clock around each call.
 
-Under torchrun each rank tracks its own sequence(s) on its own GPU (weak
-scaling, no collective in the loop); time = max over ranks.
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one process per GPU). Each rank tracks its own sequence (C3 weak scaling, no
+collective in the loop; time = max over ranks), and the north_star
+multi-sequence case C5 (64 sequences per job, 64/N per rank as one batch)
+is reported beside it as `batch_c5`.
 --impl reference times the unmodified reference CPU implementation
 (oracle/_ref, all host threads) on rank 0 on the same workload.
 """
@@ -28,6 +32,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -50,21 +55,27 @@ CONFIGS = {
     # kernels carry the sequence in blockIdx.y)
     "c5": (640, 480, 100_000, "dynamic", 5, 2),
 }
+C5_SEQUENCES = 64
 HOST_LEAD_CYCLES = 400_000  # ~0.2 ms spin before each device-timed frame (host enqueue lead)
 METRIC = "frames/s at 640×480 depth, pose+surface, 100k-vert mesh; % of HBM roofline"
 
-# SURVEY.md §8(d) algorithmic bytes per launch (fp32, unpadded) for each
-# kernel kind: V vertices, P pixels, A associated vertices, Vvis bucketed.
+
+# SURVEY.md §8(d) algorithmic bytes (fp32, unpadded) attributed to the kernel
+# that does the work here: V vertices, P pixels, A associated vertices, Vvis
+# bucketed (visible, front-facing, in-frame) vertices. K5's per-vertex
+# finalize (p~ = sum / count, r = n.(p~ - v), 72 B/V) runs inside each
+# consumer of an association (pose system, shape step, stats pass).
 def alg_bytes(kind: str, V: int, P: int, A: int, Vvis: int) -> float:
     return {
-        "skin": 56 * V,                       # K1
-        "normals+bucket": 77 * V + 37 * V + 16 * P,  # K2 + K3 histogram/scan
-        "scatter": 8 * Vvis,                  # K3 scatter part (items)
-        "search+average": 12 * P + 16 * Vvis + 8 * P + 72 * V,  # K4 + K5
-        "pose_system": 4 * V + 61 * A,        # K6
-        "pose_solve": 0,                      # K7 (+K0 FK): one CTA, latency only
-        "shape_step": 81 * V,                 # K8
-        "shape_stats": 32 * V + 24 * A,       # sums of every vertex + (v, n) of the observed ones
+        "skin": 56 * V,                          # K1
+        "normals+bucket": 77 * V + 37 * V,       # K2 + K3's per-vertex histogram
+        "pixoff": 16 * P,                        # K3's per-pixel CSR scan
+        "scatter": 8 * Vvis,                     # K3's scatter into pixel order
+        "search+average": 12 * P + 16 * Vvis + 8 * P,  # K4 + K5's per-pixel accumulation
+        "pose_system": 4 * V + 61 * A + 72 * V,  # K6 + K5 finalize
+        "pose_solve": 0,                         # K7 (+K0 FK): one CTA, latency only
+        "shape_step": 81 * V + 72 * V,           # K8 + K5 finalize
+        "shape_stats": 72 * V,                   # K5 finalize + mean |r|
         "fk": 0,
     }[kind]
 
@@ -84,6 +95,14 @@ def env_int(name, default):
         return int(os.environ.get(name, default))
     except ValueError:
         return default
+
+
+def peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    peaks = json.loads(p.read_text()) if p.exists() else {}
+    if "hbm_gbs" in peaks:
+        return float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -157,7 +176,7 @@ class ClockSampler:
                 "reasons": sorted({r for s in self.samples for r in s[2]}), "samples": len(self.samples)}
 
 
-# the humanoid 1.6 m from the camera: ~40k valid pixels per 640x480 frame
+# the humanoid 1.6 m from the camera: ~42k valid pixels per 640x480 frame
 # (acceptance.cpp:694-700 brings its biped closer the same way)
 SUBJECT_DEPTH = 1.6
 
@@ -178,7 +197,7 @@ def trajectory(bundle, frame: int, seq: int) -> np.ndarray:
     return humanoid_trajectory(bundle.link_count, frame, phase_offset=0.7 * seq)
 
 
-def cpu_port(bundle, intr, cfg, frames_host, seconds: float, theta0) -> dict:
+def cpu_port(bundle, intr, cfg, frames_host, seconds: float, theta0):
     """Fallback when oracle/_ref was not built: the C restatement
     (oracle/wt_oracle.c, single thread) over a bounded sample."""
     from oracle import c_oracle
@@ -186,22 +205,26 @@ def cpu_port(bundle, intr, cfg, frames_host, seconds: float, theta0) -> dict:
     c = cfg.c()
     ot.load_depth(frames_host[0])
     ot.track_loaded(c)
+    thetas = [ot.get_state()[0]]
     n, t0 = 0, time.perf_counter()
     while n + 1 < len(frames_host):
         ot.load_depth(frames_host[n + 1])
         ot.track_loaded(c)
         n += 1
+        if n < 3:
+            thetas.append(ot.get_state()[0])
         if time.perf_counter() - t0 > seconds:
             break
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": "frames/s", "cores": 1, "kind": "port",
             "sample": f"{n} frames of the same workload after 1 warm-up frame, C restatement of the reference "
-                      f"(oracle/wt_oracle.c, 1 thread), {dt:.1f} s"}
+                      f"(oracle/wt_oracle.c, 1 thread), {dt:.1f} s"}, thetas
 
 
-def cpu_reference(bundle, intr, cfg, frames_host, seconds: float, theta0) -> dict:
+def cpu_reference(bundle, intr, cfg, frames_host, seconds: float, theta0):
     """The reference's own track_frame (oracle/_ref) on all host threads over a
-    bounded sample of the same frames."""
+    bounded sample of the same frames. Also returns theta after each of the
+    first frames (for the bench line's parity check)."""
     from oracle import ref
     if not ref.available():
         return cpu_port(bundle, intr, cfg, frames_host, seconds, theta0)
@@ -210,23 +233,54 @@ def cpu_reference(bundle, intr, cfg, frames_host, seconds: float, theta0) -> dic
     c = cfg.c()
     c.threads = 0  # resolve_threads(0) = all hardware threads (parallel.hpp:17-21)
     rt.track_frame_depth(intr.c(), frames_host[0], c)  # warm-up frame
+    thetas = [rt.get_state()[0]]
     n, t0 = 0, time.perf_counter()
     while n + 1 < len(frames_host):
         rt.track_frame_depth(intr.c(), frames_host[n + 1], c)
         n += 1
+        if n < 3:
+            thetas.append(rt.get_state()[0])
         if time.perf_counter() - t0 > seconds:
             break
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": "frames/s", "cores": ref.hardware_threads(), "kind": "reference",
             "sample": f"{n} frames of the same workload after 1 warm-up frame, track_frame threads=0 "
-                      f"(oracle/_ref, reference sources compiled unmodified), {dt:.1f} s"}
+                      f"(oracle/_ref, reference sources compiled unmodified), {dt:.1f} s"}, thetas
+
+
+def parity_line(bundle, intr, cfg, frames_host, theta0, ref_thetas, device: int) -> dict:
+    """Max |theta_gpu - theta_ref| after each of the first frames the CPU
+    baseline tracked, the GPU tracking the same frames from the same start."""
+    from paper_1711_07999_b200.tracker import Tracker
+    trk = Tracker(bundle, intr, theta0, device=device)
+    worst = 0.0
+    try:
+        for f, rth in enumerate(ref_thetas):
+            trk.track_frame(cfg, depth=frames_host[f])
+            worst = max(worst, float(np.abs(trk.theta - rth).max()))
+    finally:
+        trk.close()
+    return {"max_abs_dtheta": worst, "frames": len(ref_thetas), "tolerance": 1e-6,
+            "vs": "the cpu_baseline leg (the reference on the host) on the same frames from the same start"}
+
+
+def workload_config(args, bundle, intr, cfg) -> dict:
+    """The workload only (identical on both arms): no measured statistics."""
+    W, H, nv, mode, kits, sits = CONFIGS[args.config]
+    names = {"c1": "C1", "c2": "C2", "c3": "C3 (headline)", "c4": "C4", "c5": "C5 (64 sequences per job)"}
+    return {"workload": f"{names[args.config]}: {W}x{H} depth, {bundle.vertex_count}-vertex "
+                        f"{bundle.link_count}-link humanoid at {SUBJECT_DEPTH} m, {mode} ({kits} pose + {sits} "
+                        f"surface GN iterations{' + stats pass' if sits else ''})",
+            "vertices": bundle.vertex_count, "triangles": bundle.triangle_count, "links": bundle.link_count,
+            "width": W, "height": H, "mode": mode, "pose_iterations": kits, "shape_iterations": sits,
+            "window_radius": cfg.assoc.window_radius, "cutoff": cfg.assoc.cutoff,
+            "l2": "flushed between timed frames (256 MiB write, outside the timed spans)"}
 
 
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     from oracle import ref
-    from paper_1711_07999_b200 import _lib as W
     bundle, intr, cfg = make_workload(args.config)
     rm = ref.RefModel.from_bundle(bundle)
     nframes = args.warmup + args.steps + 1
@@ -241,11 +295,13 @@ def run_reference(args, rank: int, world: int) -> None:
         rt.track_frame_depth(intr.c(), frames[args.warmup + f + 1], c)
     dt = time.perf_counter() - t0
     v = args.steps / dt
+    kits, sits = CONFIGS[args.config][4], CONFIGS[args.config][5]
     line = {"metric": METRIC, "value": v, "unit": "frames/s", "impl": "reference", "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference synthesize_frame renders of a sinusoidal trajectory, no noise)",
             "config": workload_config(args, bundle, intr, cfg),
+            "gn_iterations_per_s": v * (kits + sits),
             "cpu_baseline": {"value": v, "unit": "frames/s", "cores": ref.hardware_threads(), "kind": "reference",
                              "sample": f"{args.steps} frames after {args.warmup} warm-up frames, "
                                        "track_frame threads=0, wall clock"},
@@ -253,17 +309,53 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, bundle, intr, cfg) -> dict:
-    W, H, nv, mode, kits, sits = CONFIGS[args.config]
-    names = {"c1": "C1", "c2": "C2", "c3": "C3 (headline)", "c4": "C4", "c5": "C5 (64 sequences per job)"}
-    return {"workload": f"{names[args.config]}: {W}x{H} depth, {bundle.vertex_count}-vertex "
-                        f"{bundle.link_count}-link humanoid, {mode} ({kits} pose + {sits} surface GN iterations"
-                        f"{' + stats pass' if sits else ''}), {args.sequences} sequence(s) per GPU",
-            "vertices": bundle.vertex_count, "triangles": bundle.triangle_count, "links": bundle.link_count,
-            "width": W, "height": H, "mode": mode, "pose_iterations": kits, "shape_iterations": sits,
-            "window_radius": cfg.assoc.window_radius, "cutoff": cfg.assoc.cutoff,
-            "sequences_per_gpu": args.sequences,
-            "l2": "flushed between timed frames (256 MiB write, outside the timed spans)"}
+def profile_kernels(L, ctx, ccfg, load, nprof: int, nseq: int, bundle, P, A, Vvis, peak, config):
+    """Per-kernel device times inside the real frame graph (an event after
+    every kernel, wt_gpu_profile_frame) over nprof frames, with the §8(d)
+    algorithmic bytes (times nseq for a batch) and the DRAM-measured traffic."""
+    import ctypes as C
+
+    from paper_1711_07999_b200 import _lib as W
+    kinds = (C.c_int32 * 1024)()
+    ms = (C.c_float * 1024)()
+    n = C.c_int32()
+    per_kind = {}
+    nker = 0
+    for rep in range(nprof):
+        load(rep)
+        W.check(L.wt_gpu_profile_frame(ctx, C.byref(ccfg), kinds, ms, 1024, C.byref(n)), ctx)
+        nker = n.value
+        for k in range(n.value):
+            d = per_kind.setdefault(W.KERNEL_KINDS[kinds[k]], [0.0, 0])
+            d[0] += ms[k]
+            d[1] += 1
+    kernels = {}
+    for name, (tot, cnt) in per_kind.items():
+        avg_ms = tot / cnt
+        b = alg_bytes(name, bundle.vertex_count, P, A, Vvis) * nseq
+        gbs = b / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else None
+        tr = ncu_traffic(config, name)
+        kernels[name] = {"launches_per_frame": cnt / nprof, "avg_us": 1e3 * avg_ms,
+                         "us_per_frame": 1e3 * tot / nprof, "alg_bytes": b, "achieved_gbs": gbs,
+                         "frac": (gbs or 0.0) / peak,
+                         "dram_bytes_per_launch": tr,
+                         "dram_frac": (tr / (avg_ms * 1e-3) / 1e9 / peak) if (tr and avg_ms > 0) else None}
+    return kernels, nker
+
+
+def roofline_of(kernels, peak, peak_src, config):
+    # the dominant kernel among those that move data (the one-CTA solve is pure latency)
+    dominant = max((k for k in kernels if kernels[k]["alg_bytes"] > 0), key=lambda k: kernels[k]["us_per_frame"])
+    dk = kernels[dominant]
+    frame_bytes = sum(kernels[nm]["alg_bytes"] * kernels[nm]["launches_per_frame"] for nm in kernels)
+    frame_us = sum(kernels[nm]["us_per_frame"] for nm in kernels)
+    roof = {"bound": "hbm", "kernel": dominant, "achieved": dk["achieved_gbs"], "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
+            "traffic": ncu_traffic(config, dominant), "alg_bytes_per_launch": dk["alg_bytes"],
+            "avg_launch_us": dk["avg_us"], "dram_frac": dk["dram_frac"]}
+    frame = {"alg_bytes_per_frame": frame_bytes, "kernel_us_per_frame": frame_us,
+             "achieved": frame_bytes / (frame_us * 1e-6) / 1e9, "frac": frame_bytes / (frame_us * 1e-6) / 1e9 / peak}
+    return roof, frame
 
 
 def run_ours(args, rank: int, world: int, local_rank: int) -> None:
@@ -341,20 +433,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if world > 1:
         dist.barrier()
 
-    # ---- end-to-end through the public per-frame API (e2e) ----
+    # ---- end-to-end through the public per-frame C-ABI call (e2e), host clock ----
+    # every step: the pinned host frame goes up, the frame is tracked, the
+    # stats and theta come back (wt_gpu_track_frame + wt_gpu_get_state)
     reset()
-    stats_buf = W.FrameStatsC(0, 0, 0, 64, 64, 0, trackers[0]._kin, trackers[0]._shape)
-    theta = np.zeros(bundle.link_count)
-    e_st = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    e_en = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for f in range(1, args.warmup + 1):
         for s in range(S):
             trackers[s].track_frame(cfg, depth=frames_host[s][f].numpy())
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    # several sequences: one host thread per sequence slice (the C-ABI calls
-    # release the GIL), as a multi-sequence server would drive them
     from concurrent.futures import ThreadPoolExecutor
     nthr = min(S, 16)
     bufs = [(W.FrameStatsC(0, 0, 0, 64, 64, 0, t._kin, t._shape), np.zeros(bundle.link_count)) for t in trackers]
@@ -367,25 +452,26 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                     t._ctx)
             W.check(L.wt_gpu_get_state(t._ctx, th.ctypes.data, None, None), t._ctx)
 
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_s = 0.0
     with ThreadPoolExecutor(max_workers=nthr) as pool:
         for k in range(args.steps):
             f = args.warmup + 1 + k
             with torch.cuda.stream(st0):
                 flush.zero_()
-            e_st[k].record(st0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
             if S == 1:
                 drive(f, 0)
-            else:
+            else:  # one host thread per sequence slice (the C-ABI calls release the GIL)
                 list(pool.map(lambda lo: drive(f, lo), range(nthr)))
-            e_en[k].record(st0)
-            torch.cuda.synchronize()
-    e2e_ms = sum(e_st[k].elapsed_time(e_en[k]) for k in range(args.steps))
+            e2e_s += time.perf_counter() - t0
+    e2e_ms = 1e3 * e2e_s
 
     # ---- the sequence driver: all K frames in one call from pinned host memory ----
-    # (uploads overlap the solves; no L2 flush inside a sequence, so reported
-    # beside e2e rather than as it)
     reset()
-    # warm-up call: the driver's staging buffers, copy stream and graphs
     warm = frames_host[0][1: args.warmup + 1]
     W.check(L.wt_gpu_track_sequence(trackers[0]._ctx, warm.data_ptr(), args.warmup, 1.0, C.byref(ccfg), None,
                                     None), trackers[0]._ctx)
@@ -393,51 +479,32 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     th_out = np.zeros((args.steps, bundle.link_count))
     jt_out = np.zeros((args.steps, bundle.link_count, 3))
     trackers[0].set_state(theta=trajectory(bundle, args.warmup, rank * S), frame_index=args.warmup)
-    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    q0.record(st0)
+    t0 = time.perf_counter()
     W.check(L.wt_gpu_track_sequence(trackers[0]._ctx, seq_frames.data_ptr(), args.steps, 1.0, C.byref(ccfg),
                                     th_out.ctypes.data, jt_out.ctypes.data), trackers[0]._ctx)
-    q1.record(st0)
-    torch.cuda.synchronize()
-    seq_ms = q0.elapsed_time(q1)
+    seq_s = time.perf_counter() - t0
 
-    # ---- per-kernel device times inside the real frame (events between kernels) ----
-    kinds = (C.c_int32 * 512)()
-    ms = (C.c_float * 512)()
-    n = C.c_int32()
-    per_kind = {}
-    nker = 0
-    # profile frames that follow the tracker's state (steady tracking)
+    # ---- association statistics of the workload: bucketed and associated vertices ----
     trackers[0].set_state(theta=trajectory(bundle, args.warmup, rank * S), phi=np.zeros((bundle.vertex_count, 3)),
                           frame_index=1)
-    for rep in range(nprof):
+    st = trackers[0].track_frame(cfg, depth=frames_host[0][args.warmup + 1].numpy())
+    nb = C.c_int32()
+    W.check(L.wt_gpu_bucket_count(trackers[0]._ctx, 0, C.byref(nb)), trackers[0]._ctx)
+    A = int(np.mean([k.associated for k in st.kin]))
+    Vvis = int(nb.value)
+
+    # ---- per-kernel device times inside the real frame (events between kernels) ----
+    peak, peak_src = peak_hbm()
+    trackers[0].set_state(theta=trajectory(bundle, args.warmup, rank * S), phi=np.zeros((bundle.vertex_count, 3)),
+                          frame_index=1)
+
+    def load(rep):
         f = args.warmup + 1 + rep
         W.check(L.wt_gpu_load_depth(trackers[0]._ctx, frames_dev[0][f].data_ptr(), 1.0), trackers[0]._ctx)
-        W.check(L.wt_gpu_profile_frame(trackers[0]._ctx, C.byref(ccfg), kinds, ms, 512, C.byref(n)),
-                trackers[0]._ctx)
-        nker = n.value
-        for k in range(n.value):
-            name = W.KERNEL_KINDS[kinds[k]]
-            d = per_kind.setdefault(name, [0.0, 0])
-            d[0] += ms[k]
-            d[1] += 1
-    # association statistics for the byte model
-    st = trackers[0].track_frame(cfg, depth=frames_host[0][args.warmup + nprof + 1].numpy())
-    A = st.kin[-1].associated if st and st.kin else bundle.vertex_count // 4
-    Vvis = bundle.vertex_count // 2
-    kernels = {}
-    for name, (tot, cnt) in per_kind.items():
-        avg_ms = tot / cnt
-        b = alg_bytes(name, bundle.vertex_count, P, A, Vvis)
-        kernels[name] = {"launches_per_frame": cnt // nprof, "avg_us": 1e3 * avg_ms,
-                         "us_per_frame": 1e3 * tot / nprof, "alg_bytes": b,
-                         "achieved_gbs": b / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else None}
-    # the dominant kernel among those that move data (the one-CTA solve is pure latency)
-    dominant = max((k for k in kernels if kernels[k]["alg_bytes"] > 0), key=lambda k: kernels[k]["us_per_frame"])
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = peaks.get("hbm_gbs", 6650.0)
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    kernels, nker = profile_kernels(L, trackers[0]._ctx, ccfg, load, nprof, 1, bundle, P, A, Vvis, peak,
+                                    args.config)
 
     # ---- aggregate over ranks (max time) ----
     t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
@@ -447,62 +514,67 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     total_frames = args.steps * S * world
     value = total_frames / (dev_ms * 1e-3)
     e2e = total_frames / (e2e_ms * 1e-3)
+    batch = None
+    bargs = None
+    if args.config == "c3" and not args.no_batch:
+        # C5, the north_star multi-sequence case: 64 sequences per job, 64/N
+        # per rank as one batch -- where the per-vertex / per-pixel kernels
+        # become HBM-bound, so their roofline fraction is meaningful
+        bargs = argparse.Namespace(**{**vars(args), "config": "c5", "sequences": max(1, C5_SEQUENCES // world),
+                                      "steps": 10, "warmup": 3})
+        batch = run_batched(bargs, rank, world, local_rank, emit=False)
     if rank != 0:
+        for t_ in trackers:
+            t_.close()
         return
-    frame_bytes = sum(alg_bytes(nm, bundle.vertex_count, P, A, Vvis) * kernels[nm]["launches_per_frame"]
-                      for nm in kernels)
-    frame_us = sum(kernels[nm]["us_per_frame"] for nm in kernels)
-    dk = kernels[dominant]
+    roof, frame = roofline_of(kernels, peak, peak_src, args.config)
+    kits, sits = CONFIGS[args.config][4], CONFIGS[args.config][5]
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if args.config == "c5" else "weak", "vs_baseline": None,
+        "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 (geometry, distances, normal equations; normals stored f32)",
         "data": "synthetic (GPU synthesize_frame renders of a sinusoidal joint trajectory, no noise)",
-        "config": {**workload_config(args, bundle, intr, cfg), "valid_pixels_mean": valid_px,
-                   "associated_vertices": A},
+        "config": {**workload_config(args, bundle, intr, cfg), "sequences_per_gpu": S},
+        "workload_stats": {"valid_pixels_mean": valid_px, "bucketed_vertices": Vvis, "associated_vertices_mean": A},
+        "gn_iterations_per_s": value * (kits + sits),
         "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": 4 * P * S,
-                "d2h_bytes_per_step": S * (8 * bundle.link_count + 32 * (cfg.kin.iterations + cfg.shape.iterations))},
-        "e2e_sequence": {"value": args.steps / (seq_ms * 1e-3), "unit": "frames/s",
+                "d2h_bytes_per_step": S * (8 * bundle.link_count + 32 * (kits + sits)),
+                "api": "wt_gpu_track_frame (pinned host depth frame, FrameStats) + wt_gpu_get_state (theta), "
+                       "host clock around the calls"},
+        "e2e_sequence": {"value": args.steps / seq_s, "unit": "frames/s",
                          "api": "wt_gpu_track_sequence (one call, K pinned host frames, uploads overlapped, "
-                                "theta + joints read back)", "h2d_bytes_per_step": 4 * P,
+                                "theta + joints read back), host clock", "h2d_bytes_per_step": 4 * P,
                          "d2h_bytes_per_step": 32 * bundle.link_count, "l2": "not flushed inside the sequence"},
-        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dk["achieved_gbs"], "peak": peak,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
-                     "traffic": ncu_traffic(args.config, dominant), "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"]},
-        "frame_roofline": {"alg_bytes_per_frame": frame_bytes, "kernel_us_per_frame": frame_us,
-                           "achieved": frame_bytes / (frame_us * 1e-6) / 1e9,
-                           "frac": frame_bytes / (frame_us * 1e-6) / 1e9 / peak,
-                           "aggregate_achieved": frame_bytes * value / world / 1e9,
-                           "aggregate_frac": frame_bytes * value / world / 1e9 / peak,
+        "roofline": roof,
+        "frame_roofline": {**frame, "aggregate_achieved": frame["alg_bytes_per_frame"] * value / world / 1e9,
+                           "aggregate_frac": frame["alg_bytes_per_frame"] * value / world / 1e9 / peak,
                            "note": "per-kernel times from one sequence's frame graph (events between kernels); "
                                    "aggregate = algorithmic bytes per frame x frames/s per GPU"},
         "kernels": kernels,
         "gpu_launches": args.steps * S * (nker + 1),
         "clocks": clk.summary(),
     }
-    if world == 1 and args.config == "c3" and not args.no_batch:
-        # the same workload as 64 concurrent sequences on this GPU (C5's
-        # per-GPU batch): where the per-vertex / per-pixel kernels become
-        # HBM-bound, so their roofline fraction is meaningful
-        bargs = argparse.Namespace(**{**vars(args), "config": "c5", "sequences": 64, "steps": 10, "warmup": 3})
-        b = run_batched(bargs, rank, world, local_rank, emit=False)
+    if batch is not None:
         line["batch_c5"] = {
-            "workload": b["config"]["workload"], "value": b["value"], "unit": "frames/s",
-            "ms_per_step": b["ms_per_step"], "steps": bargs.steps, "step": b["config"]["step"],
-            "e2e": b["e2e"], "roofline": b["roofline"], "frame_roofline": b["frame_roofline"],
-            "kernels": {k: {"avg_us": v["avg_us"], "us_per_frame": v["us_per_frame"],
-                            "achieved_gbs": v["achieved_gbs"],
-                            "frac": (v["achieved_gbs"] or 0.0) / b["roofline"]["peak"]}
-                        for k, v in b["kernels"].items()},
-            "gpu_launches": b["gpu_launches"], "clocks": b["clocks"]}
+            "workload": batch["config"]["workload"], "value": batch["value"], "unit": "frames/s",
+            "n_gpus": world, "sequences_per_gpu": bargs.sequences, "scaling": "strong",
+            "ms_per_step": batch["ms_per_step"], "steps": bargs.steps, "step": batch["step"],
+            "gn_iterations_per_s": batch["gn_iterations_per_s"], "workload_stats": batch["workload_stats"],
+            "e2e": batch["e2e"], "roofline": batch["roofline"], "frame_roofline": batch["frame_roofline"],
+            "kernels": {k: {kk: v[kk] for kk in ("avg_us", "us_per_frame", "achieved_gbs", "frac",
+                                                 "dram_bytes_per_launch", "dram_frac")}
+                        for k, v in batch["kernels"].items()},
+            "gpu_launches": batch["gpu_launches"], "clocks": batch["clocks"]}
     if world == 1 and not args.no_cpu_baseline:
         # a bounded CPU sample of the same workload: enough frames of the same
         # trajectory for ~cpu_seconds of reference work (rendered on the GPU)
         ncpu = int(args.cpu_seconds * 40) + 2
         cpu_frames = [trackers[0].render_depth(trajectory(bundle, f, 0), frame=f)[0] for f in range(ncpu)]
-        line["cpu_baseline"] = cpu_reference(bundle, intr, cfg, cpu_frames, args.cpu_seconds,
-                                             trajectory(bundle, 0, 0))
+        line["cpu_baseline"], ref_thetas = cpu_reference(bundle, intr, cfg, cpu_frames, args.cpu_seconds,
+                                                         trajectory(bundle, 0, 0))
+        line["parity"] = parity_line(bundle, intr, cfg, cpu_frames, trajectory(bundle, 0, 0), ref_thetas,
+                                     local_rank)
     print(json.dumps(line), flush=True)
     for t_ in trackers:
         t_.close()
@@ -510,7 +582,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
 
 def run_batched(args, rank: int, world: int, local_rank: int, emit: bool = True):
     """C5: the rank's sequences tracked as one batch (wt_gpu_create_batch).
-    Prints the JSON line (emit) or returns it."""
+    Prints the JSON line (emit) or returns it (rank 0; None elsewhere)."""
     import ctypes as C
 
     import torch
@@ -572,7 +644,7 @@ def run_batched(args, rank: int, world: int, local_rank: int, emit: bool = True)
     if world > 1:
         dist.barrier()
 
-    # ---- end to end: pinned host frames in, stats + every theta out ----
+    # ---- end to end: pinned host frames in, stats + every theta out, host clock ----
     reset()
     kin = [(W.KinIterStats * 64)() for _ in range(S)]
     shp = [(W.ShapeIterStats * 32)() for _ in range(S)]
@@ -586,43 +658,31 @@ def run_batched(args, rank: int, world: int, local_rank: int, emit: bool = True)
 
     for f in range(1, args.warmup + 1):
         frame_e2e(f)
-    e_st = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    e_en = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    e2e_s = 0.0
     for k in range(args.steps):
         with torch.cuda.stream(st0):
             flush.zero_()
-        e_st[k].record(st0)
-        frame_e2e(args.warmup + 1 + k)
-        e_en[k].record(st0)
         torch.cuda.synchronize()
-    e2e_ms = sum(e_st[k].elapsed_time(e_en[k]) for k in range(args.steps))
+        t0 = time.perf_counter()
+        frame_e2e(args.warmup + 1 + k)
+        e2e_s += time.perf_counter() - t0
+    e2e_ms = 1e3 * e2e_s
+    A = int(np.mean([np.mean([kin[s][k].associated for k in range(stats[s].n_kin)]) for s in range(S)]))
+    nb = C.c_int32()
+    W.check(L.wt_gpu_bucket_count(bt._ctx, 0, C.byref(nb)), bt._ctx)
+    Vvis = int(nb.value)
 
     # ---- per-kernel device times of one batch frame (events between kernels) ----
-    kinds = (C.c_int32 * 512)()
-    ms = (C.c_float * 512)()
-    n = C.c_int32()
-    W.check(L.wt_gpu_batch_load_depth(bt._ctx, frames_dev[args.warmup + args.steps + 1].data_ptr(), 1.0), bt._ctx)
-    W.check(L.wt_gpu_profile_frame(bt._ctx, C.byref(ccfg), kinds, ms, 512, C.byref(n)), bt._ctx)
-    per_kind = {}
-    for k in range(n.value):
-        d = per_kind.setdefault(W.KERNEL_KINDS[kinds[k]], [0.0, 0])
-        d[0] += ms[k]
-        d[1] += 1
-    A = int(np.mean([stats[s].n_kin and kin[s][stats[s].n_kin - 1].associated for s in range(S)]))
-    Vvis = bundle.vertex_count // 2
-    kernels = {}
-    for name, (tot, cnt) in per_kind.items():
-        avg_ms = tot / cnt
-        b = alg_bytes(name, bundle.vertex_count, P, A, Vvis) * S
-        kernels[name] = {"launches_per_frame": cnt, "avg_us": 1e3 * avg_ms, "us_per_frame": 1e3 * tot,
-                         "alg_bytes": b, "achieved_gbs": b / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else None}
-    dominant = max((k for k in kernels if kernels[k]["alg_bytes"] > 0), key=lambda k: kernels[k]["us_per_frame"])
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = peaks.get("hbm_gbs", 6650.0)
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    peak, peak_src = peak_hbm()
+
+    def load(rep):
+        W.check(L.wt_gpu_batch_load_depth(bt._ctx, frames_dev[args.warmup + args.steps + 1].data_ptr(), 1.0),
+                bt._ctx)
+
+    kernels, nker = profile_kernels(L, bt._ctx, ccfg, load, 1, S, bundle, P, A, Vvis, peak, "c5")
 
     t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -631,42 +691,62 @@ def run_batched(args, rank: int, world: int, local_rank: int, emit: bool = True)
     total_frames = args.steps * S * world
     value = total_frames / (dev_ms * 1e-3)
     e2e = total_frames / (e2e_ms * 1e-3)
+    bt.close()
+    renderer.close()
     if rank != 0:
-        bt.close()
-        renderer.close()
-        return
-    frame_bytes = sum(kernels[nm]["alg_bytes"] * kernels[nm]["launches_per_frame"] for nm in kernels)
-    frame_us = sum(kernels[nm]["us_per_frame"] for nm in kernels)
-    dk = kernels[dominant]
+        return None
+    roof, frame = roofline_of(kernels, peak, peak_src, "c5")
+    kits, sits = CONFIGS[args.config][4], CONFIGS[args.config][5]
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
         "dtype": "f64 (geometry, distances, normal equations; normals stored f32)",
         "data": "synthetic (GPU synthesize_frame renders of sinusoidal joint trajectories, one phase per sequence)",
-        "config": {**workload_config(args, bundle, intr, cfg), "valid_pixels_mean": valid_px,
-                   "associated_vertices": A, "batched": True,
-                   "step": f"one frame of every sequence of the rank's batch ({S} frames per rank per step)"},
+        "config": {**workload_config(args, bundle, intr, cfg), "sequences_per_gpu": S, "batched": True},
+        "step": f"one frame of every sequence of the rank's batch ({S} frames per rank per step)",
+        "workload_stats": {"valid_pixels_mean": valid_px, "bucketed_vertices": Vvis, "associated_vertices_mean": A},
+        "gn_iterations_per_s": value * (kits + sits),
         "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": 4 * P * S,
                 "d2h_bytes_per_step": S * (8 * bundle.link_count + 32 * 64 + 40 * 32),
                 "api": "wt_gpu_batch_track (pinned host frames of the batch, stats) + wt_gpu_batch_get_state "
-                       "theta of every sequence"},
-        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dk["achieved_gbs"], "peak": peak,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
-                     "traffic": ncu_traffic(args.config, dominant), "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"]},
-        "frame_roofline": {"alg_bytes_per_frame": frame_bytes, "kernel_us_per_frame": frame_us,
-                           "achieved": frame_bytes / (frame_us * 1e-6) / 1e9,
-                           "frac": frame_bytes / (frame_us * 1e-6) / 1e9 / peak,
-                           "note": "one batch frame of the rank's sequences, events between kernels"},
+                       "theta of every sequence, host clock"},
+        "roofline": roof,
+        "frame_roofline": {**frame, "note": "one batch frame of the rank's sequences, events between kernels"},
         "kernels": kernels,
-        "gpu_launches": args.steps * (n.value + 1),
+        "gpu_launches": args.steps * (nker + 1),
         "clocks": clk.summary(),
     }
-    bt.close()
-    renderer.close()
     if emit:
         print(json.dumps(line), flush=True)
     return line
+
+
+def plumbing_check(args, rank: int, world: int) -> None:
+    """--plumbing-check (CPU, gloo): the multi-rank host path of the bench
+    without device work -- each rank's C5 shard, the barrier, the max over
+    ranks and rank 0's single JSON line."""
+    import torch.distributed as dist
+
+    from paper_1711_07999_b200 import shard
+    r = shard.Rank(rank, world, rank)
+    if world > 1:
+        dist.init_process_group("gloo")
+    mine = list(shard.shard(C5_SEQUENCES, r))
+    shard.barrier(r)
+    ms = shard.max_over_ranks([1.0 + rank], r)
+    got = shard.gather_to_root({"rank": rank, "pid": os.getpid(), "sequences": mine}, r)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "n_gpus": world, "plumbing_check": True, "max_ms": float(ms[0]),
+                          "shards": got}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main() -> None:
@@ -680,14 +760,23 @@ def main() -> None:
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batch", action="store_true",
-                    help="c3: skip the 64-sequence batch sub-measurement (batch_c5)")
+                    help="c3: skip the C5 batch sub-measurement (batch_c5)")
     ap.add_argument("--streams", action="store_true",
                     help="c5: one Tracker + stream per sequence instead of one batch")
+    ap.add_argument("--plumbing-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve())]
+        sys.exit(subprocess.call(cmd + sys.argv[1:]))
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.plumbing_check:
+        plumbing_check(args, rank, world)
+        return
     if args.config == "c5":  # 64 sequences per job, strong-scaled over the ranks
-        args.sequences = max(1, 64 // world)
+        args.sequences = max(1, C5_SEQUENCES // world)
     if world > 1 and args.impl == "ours":
         import torch
         import torch.distributed as dist

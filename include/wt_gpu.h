@@ -11,6 +11,10 @@
  *                  Cholesky failure stays "skip the iteration + flag", exactly
  *                  like proj/src/kinopt.cpp:160-168)
  *   WT_ECUDA / WT_ENOMEM for device failures.
+ *   WT_ERANGE   a frame's fixed-point normal equations left the int64 range
+ *               (the device reduction's scales are chosen from the model and
+ *               the cutoff so this needs a diverged pose; the reference, which
+ *               sums in fp64, would take the step)
  * The message of the last failure is available from wt_gpu_last_error().
  *
  * Replaced reference interfaces (file:line into /root/reference/proj):
@@ -54,7 +58,8 @@ enum {
   WT_ECUDA = 3,
   WT_ENOMEM = 4,
   WT_ENOTPD = 5,
-  WT_ENODEV = 6
+  WT_ENODEV = 6,
+  WT_ERANGE = 7
 };
 
 /* TrackMode, tracker_state.hpp:9 */
@@ -234,6 +239,13 @@ int wt_gpu_optimize_shape(wt_gpu_ctx* ctx, const wt_shape_config* shape,
                           const wt_assoc_config* assoc, int32_t with_stats_pass,
                           wt_shape_iter_stats* stats, int32_t cap, int32_t* n_out);
 
+/* ---- page-locked host staging ----------------------------------------------- */
+/* Page-locked host memory (cudaMallocHost) for callers that do not link the
+ * CUDA runtime (the reference-side adapter): a depth frame staged there takes
+ * wt_gpu_track_frame's overlapped upload path. */
+int wt_gpu_host_alloc(size_t bytes, void** out);
+void wt_gpu_host_free(void* p);
+
 /* ---- asynchronous use / measurement --------------------------------------- */
 /* The context's CUDA stream (cudaStream_t) for event timing by the caller. */
 void* wt_gpu_stream(wt_gpu_ctx* ctx);
@@ -244,9 +256,13 @@ int wt_gpu_sync(wt_gpu_ctx* ctx);
 /* Runs one track_frame through an instrumented graph (a CUDA event after
  * every kernel) and returns each kernel's kind and device time in ms:
  * 0 fk, 1 skin, 2 normals+bucket, 3 scatter, 4 search+average,
- * 5 pose system+solve, 6 shape step, 7 shape stats pass. */
+ * 5 pose system, 6 shape step, 7 shape stats pass, 8 pose solve,
+ * 9 pixel offsets (the bucket CSR scan). */
 int wt_gpu_profile_frame(wt_gpu_ctx* ctx, const wt_track_config* cfg, int32_t* kinds, float* ms,
                          int32_t cap, int32_t* n_out);
+/* Vertices bucketed by the last association of sequence `seq` (the size of
+ * the VertexBuckets item list, association.cpp:39-67): measurement only. */
+int wt_gpu_bucket_count(wt_gpu_ctx* ctx, int32_t seq, int32_t* n_bucketed);
 
 /* ---- batched sequences --------------------------------------------------- */
 /* n_seq independent tracking sequences of ONE model, tracked in lockstep

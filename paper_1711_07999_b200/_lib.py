@@ -14,7 +14,7 @@ import numpy as np
 LIB_PATH = Path(__file__).resolve().parent / "libwt_gpu.so"
 
 ABI_VERSION = 2  # WT_ABI_VERSION, include/wt_gpu.h
-WT_OK, WT_EINVAL, WT_ELENGTH, WT_ECUDA, WT_ENOMEM, WT_ENOTPD, WT_ENODEV = range(7)
+WT_OK, WT_EINVAL, WT_ELENGTH, WT_ECUDA, WT_ENOMEM, WT_ENOTPD, WT_ENODEV, WT_ERANGE = range(8)
 MODE_DYNAMIC, MODE_SHAPE_MATCH, MODE_SMOOTH_BIND, MODE_RIGID = range(4)
 JOINT_HINGE, JOINT_PRISMATIC = 0, 1
 
@@ -90,12 +90,12 @@ EXPORTS = [
     "wt_gpu_track_frame_cloud", "wt_gpu_optimize_pose", "wt_gpu_optimize_shape", "wt_gpu_skin",
     "wt_gpu_associate", "wt_gpu_associate_posed", "wt_gpu_normal_system", "wt_gpu_solve_step",
     "wt_gpu_solve_vertices", "wt_gpu_render_depth", "wt_gpu_stream", "wt_gpu_track_async", "wt_gpu_sync",
-    "wt_gpu_profile_frame", "wt_gpu_track_sequence", "wt_gpu_joint_positions", "wt_gpu_recon_error",
+    "wt_gpu_profile_frame", "wt_gpu_bucket_count", "wt_gpu_host_alloc", "wt_gpu_host_free", "wt_gpu_track_sequence", "wt_gpu_joint_positions", "wt_gpu_recon_error",
     "wt_gpu_create_batch", "wt_gpu_batch_size", "wt_gpu_batch_set_state", "wt_gpu_batch_get_state",
     "wt_gpu_batch_load_depth", "wt_gpu_batch_track_async", "wt_gpu_batch_stats", "wt_gpu_batch_track",
 ]
 KERNEL_KINDS = ["fk", "skin", "normals+bucket", "scatter", "search+average", "pose_system",
-                "shape_step", "shape_stats", "pose_solve"]
+                "shape_step", "shape_stats", "pose_solve", "pixoff"]
 
 
 class WarptrackError(RuntimeError):
@@ -169,6 +169,10 @@ def _declare(L: C.CDLL) -> None:
     L.wt_gpu_track_sequence.argtypes = [vp, vp, C.c_int32, C.c_double, P(TrackConfigC), vp, vp]
     L.wt_gpu_joint_positions.argtypes = [vp, vp]
     L.wt_gpu_recon_error.argtypes = [vp, vp, P(C.c_int32)]
+    L.wt_gpu_bucket_count.argtypes = [vp, C.c_int32, P(C.c_int32)]
+    L.wt_gpu_host_alloc.argtypes = [C.c_size_t, P(vp)]
+    L.wt_gpu_host_free.argtypes = [vp]
+    L.wt_gpu_host_free.restype = None
     L.wt_gpu_profile_frame.argtypes = [vp, P(TrackConfigC), vp, vp, C.c_int32, P(C.c_int32)]
     L.wt_gpu_create_batch.argtypes = [C.c_int, P(ModelDesc), P(Intrinsics), C.c_int32, P(vp)]
     L.wt_gpu_batch_size.argtypes = [vp]

@@ -101,6 +101,7 @@ struct wt_gpu_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   int V = 0, L = 0, NP = 0, K = 0, T = 0;
+  double lever = 1.0;  // max(1, largest template distance vertex <-> joint origin), x4 margin (pose_scales)
   wt_intrinsics intr{};
   wt::DevIntr din{};
   int P = 0;
@@ -145,6 +146,7 @@ struct wt_gpu_ctx {
   // trip per frame); valid until the next API call on the context
   double* h_theta = nullptr;
   bool theta_mirror = false;
+  double4* h_phi4 = nullptr;  // page-locked staging of Phi transfers (set_state / get_state), lazily allocated
 
   // renderer (fp64 copies, lazily built)
   double* r_v0 = nullptr;
@@ -221,6 +223,7 @@ struct wt_gpu_ctx {
     for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
     if (h_kin) cudaFreeHost(h_kin);
     if (h_theta) cudaFreeHost(h_theta);
+    if (h_phi4) cudaFreeHost(h_phi4);
     if (h_shape) cudaFreeHost(h_shape);
     if (stream) cudaStreamDestroy(stream);
     if (arena) cudaFree(arena);
@@ -253,7 +256,7 @@ void check_launch() {
 }
 
 // kernel kinds reported by wt_gpu_profile_frame
-enum { K_FK = 0, K_SKIN, K_NORMALS, K_SCATTER, K_SEARCH, K_POSE, K_SHAPE, K_SHAPE_AFTER, K_POSE_SOLVE, K_NKIND };
+enum { K_FK = 0, K_SKIN, K_NORMALS, K_SCATTER, K_SEARCH, K_POSE, K_SHAPE, K_SHAPE_AFTER, K_POSE_SOLVE, K_PIXOFF, K_NKIND };
 
 void mark(wt_gpu_ctx* c, int kind) {
   check_launch();
@@ -392,7 +395,9 @@ void layout_seq(wt_gpu_ctx* c, Carve& a) {
   c->d_pts_hi = a.take<double>(3 * static_cast<size_t>(P));
   // valid-pixel list: one run of 32 entries per 32-column row segment
   c->d_vlist = a.take<int>(32 * H * ((c->din.W + 31) / 32));
-  c->d_nvalid = a.take<int>(1);
+  c->d_nvalid = a.take<int>(4);  // frame words: [0] list length, [2..3] max |coordinate| (k_ingest)
+  s.fwords = c->d_nvalid;
+  s.spart = a.take<double>(static_cast<size_t>(wt::kStatParts) * vgrid(V));
   c->d_winners = a.take<int>(P);
 }
 
@@ -423,6 +428,18 @@ void require_single(const wt_gpu_ctx* c) {
   if (c->nseq != 1) fail(WT_EINVAL, "not available on a batch context (use the wt_gpu_batch_* calls)");
 }
 
+// Every captured frame graph (plain and pinned-upload forms) bakes the stats
+// buffers into its kernel parameters: a reallocation must drop them all.
+void drop_graphs(wt_gpu_ctx* c) {
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  c->graphs.clear();
+  for (auto& kv : c->h2d_graphs) {
+    cudaGraphExecDestroy(kv.second.exec);
+    cudaGraphDestroy(kv.second.graph);
+  }
+  c->h2d_graphs.clear();
+}
+
 void ensure_stats(wt_gpu_ctx* c, int nk, int ns) {
   if ((nk > c->cap_kin || ns > c->cap_shape) && c->nseq > 1)
     fail(WT_EINVAL, "a batch records at most " + std::to_string(kArenaKin) + " pose / " +
@@ -432,16 +449,14 @@ void ensure_stats(wt_gpu_ctx* c, int nk, int ns) {
     c->ds.kin_stats = c->mem.alloc<wt::KinStat>(c->cap_kin);
     if (c->h_kin) cudaFreeHost(c->h_kin);
     WT_CUDA(cudaMallocHost(&c->h_kin, sizeof(wt::KinStat) * c->cap_kin));
-    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
-    c->graphs.clear();
+    drop_graphs(c);
   }
   if (ns > c->cap_shape) {
     c->cap_shape = std::max(ns, 8);
     c->ds.shape_stats = c->mem.alloc<wt::ShapeStat>(c->cap_shape);
     if (c->h_shape) cudaFreeHost(c->h_shape);
     WT_CUDA(cudaMallocHost(&c->h_shape, sizeof(wt::ShapeStat) * c->cap_shape));
-    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
-    c->graphs.clear();
+    drop_graphs(c);
   }
 }
 
@@ -467,7 +482,7 @@ void enq_normals(wt_gpu_ctx* c, const wt::DevState& s, bool bucket, bool zero_ac
 void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
   WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_pixoff<true> : wt::k_pixoff<false>, dim3((c->din.H + 7) / 8, c->nseq), dim3(wt::kVThreads), 0, c->stream, s,
                          c->din.W, c->din.H));
-  mark(c, K_SCATTER);
+  mark(c, K_PIXOFF);
   WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_scatter<true> : wt::k_scatter<false>,
                          dim3(vgrid(std::max(c->V, c->din.H)), c->nseq), dim3(wt::kVThreads), 0, c->stream, c->dm, s,
                          c->din.H));
@@ -551,9 +566,28 @@ void pose_attr(wt_gpu_ctx* c) {
   WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system<Q, TPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
+// Fixed-point scales of the pose reduction (wt_kernels.cuh): every row entry
+// is n . dv/dtheta_k, at most the lever arm R (hinges; 1 for a prismatic
+// joint) -- c->lever, the template's with a 4x margin for pose and Phi -- and
+// |r| <= cutoff, so over V vertices JtJ_kk <= V R^2 and |Jtr_k| <= V R
+// cutoff; sum r^2 <= V cutoff^2. The scales keep those below 2^62 (at most
+// 2^-40 / 2^-44, the metre-scale values).
+double pow2_below(double bound, int cap) {
+  int ex = 0;
+  std::frexp(std::max(bound, 1e-300), &ex);  // bound < 2^ex
+  return std::ldexp(1.0, std::min(cap, 62 - ex));
+}
+
+void pose_scales(const wt_gpu_ctx* c, double cutoff, wt::PoseArgs& pa) {
+  const double V = std::max(1, c->V), R = c->lever;
+  pa.sys_scale = pow2_below(V * std::max(R * R, R * cutoff), 40);
+  pa.res_scale = pow2_below(2.0 * V * cutoff * cutoff, 44);
+}
+
 void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt_kin_config* k,
-              int it, bool solve, const int* count_in, const double* res_in, bool clean_acc = false) {
+              int it, bool solve, const int* count_in, const double* res_in, double cutoff, bool clean_acc = false) {
   wt::PoseArgs pa;
+  pose_scales(c, cutoff, pa);
   pa.lambda_k = k->lambda_k;
   pa.lambda_s = k->lambda_s;
   pa.diag_floor = k->diag_floor;
@@ -611,7 +645,7 @@ void enq_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* k, const wt_assoc_con
     }
     // the last pose system before a re-association (or the end) cleans the sums
     const bool last_use = (it + 1) % refresh == 0 || it + 1 == k->iterations;
-    enq_pose(c, c->ds, c->phi[c->cur], k, it, true, nullptr, nullptr, last_use);
+    enq_pose(c, c->ds, c->phi[c->cur], k, it, true, nullptr, nullptr, a->cutoff, last_use);
   }
 }
 
@@ -693,16 +727,25 @@ void put_shape(const wt_gpu_ctx* c, int n, wt_shape_iter_stats* out, int cap, in
 
 // A tracked frame's results back on the host: the stats (FrameStats) and
 // theta (the host mirror), one synchronisation; then the frame counter.
+// A pose iteration whose fixed-point normal equations left the int64 range
+// (k_pose_solve, skipped == 2) is an error, not a silent skip.
+void check_range(const wt_gpu_ctx* c, int nk) {
+  for (int k = 0; k < nk; ++k)
+    if (c->h_kin[k].skipped == 2)
+      fail(WT_ERANGE, "pose iteration " + std::to_string(k) +
+                          ": normal equations outside the fixed-point range of the device reduction");
+}
+
 void frame_readback(wt_gpu_ctx* c, int nk, int ns, wt_frame_stats* stats) {
-  if (stats) {
-    if (nk) WT_CUDA(cudaMemcpyAsync(c->h_kin, c->ds.kin_stats, sizeof(wt::KinStat) * nk,
-                                    cudaMemcpyDeviceToHost, c->stream));
-    if (ns) WT_CUDA(cudaMemcpyAsync(c->h_shape, c->ds.shape_stats, sizeof(wt::ShapeStat) * ns,
-                                    cudaMemcpyDeviceToHost, c->stream));
-  }
+  if (nk) WT_CUDA(cudaMemcpyAsync(c->h_kin, c->ds.kin_stats, sizeof(wt::KinStat) * nk, cudaMemcpyDeviceToHost,
+                                  c->stream));
+  if (stats && ns)
+    WT_CUDA(cudaMemcpyAsync(c->h_shape, c->ds.shape_stats, sizeof(wt::ShapeStat) * ns, cudaMemcpyDeviceToHost,
+                            c->stream));
   WT_CUDA(cudaMemcpyAsync(c->h_theta, c->ds.theta, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
   WT_CUDA(cudaStreamSynchronize(c->stream));
   c->theta_mirror = true;
+  check_range(c, nk);
   if (stats) {
     stats->frame = c->frame_index;
     stats->n_kin = nk;
@@ -711,6 +754,35 @@ void frame_readback(wt_gpu_ctx* c, int nk, int ns, wt_frame_stats* stats) {
     if (stats->shape) put_shape(c, ns, stats->shape, stats->cap_shape);
   }
   ++c->frame_index;
+}
+
+// Phi moves between the caller's packed [V][3] array and the device's
+// double4 records through a page-locked staging buffer (one DMA each way).
+double4* phi_stage(wt_gpu_ctx* c) {
+  if (!c->h_phi4) WT_CUDA(cudaMallocHost(&c->h_phi4, sizeof(double4) * std::max(1, c->V)));
+  return c->h_phi4;
+}
+
+void phi_put(wt_gpu_ctx* c, double4* dst, const double* phi) {
+  double4* h = phi_stage(c);
+  WT_CUDA(cudaStreamSynchronize(c->stream));  // the staging buffer is free
+  for (int i = 0; i < c->V; ++i) h[i] = make_double4(phi[3 * i], phi[3 * i + 1], phi[3 * i + 2], 0.0);
+  WT_CUDA(cudaMemcpyAsync(dst, h, sizeof(double4) * c->V, cudaMemcpyHostToDevice, c->stream));
+  WT_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// enqueues the download; phi_unpack after the stream synchronised
+void phi_get_async(wt_gpu_ctx* c, const double4* src) {
+  WT_CUDA(cudaMemcpyAsync(phi_stage(c), src, sizeof(double4) * c->V, cudaMemcpyDeviceToHost, c->stream));
+}
+
+void phi_unpack(const wt_gpu_ctx* c, double* phi) {
+  const double4* h = c->h_phi4;
+  for (int i = 0; i < c->V; ++i) {
+    phi[3 * i] = h[i].x;
+    phi[3 * i + 1] = h[i].y;
+    phi[3 * i + 2] = h[i].z;
+  }
 }
 
 // rows of `width` bytes, one per sequence arena, to / from a packed host array
@@ -839,6 +911,22 @@ int create_ctx(int device, const wt_model_desc* d, const wt_intrinsics* intr, in
     std::vector<wt::DQ> bind(static_cast<size_t>(L));
     wt::fk_all(c->links.data(), L, zero.data(), bind.data());
     for (int j = 0; j < L; ++j) wt::dq_store(wt::dq_inverse(bind[j]), c->links[j].bind_inv);
+    {
+      // lever arm bound of the pose rows: template vertex <-> bind-pose joint origin
+      std::vector<double> org(3 * static_cast<size_t>(L));
+      for (int j = 0; j < L; ++j) {
+        const double zero[3] = {0.0, 0.0, 0.0};
+        wt::dq_transform_point(bind[j], zero, &org[3 * j]);
+      }
+      double r2 = 0.0;
+      for (int i = 0; i < d->n_vertices; ++i)
+        for (int j = 0; j < L; ++j) {
+          const double dx = d->v0[3 * i] - org[3 * j], dy = d->v0[3 * i + 1] - org[3 * j + 1],
+                       dz = d->v0[3 * i + 2] - org[3 * j + 2];
+          r2 = std::max(r2, dx * dx + dy * dy + dz * dz);
+        }
+      c->lever = std::max(1.0, 4.0 * std::sqrt(r2));
+    }
     std::vector<std::vector<int>> anc(static_cast<size_t>(L));
     c->pair_off.assign(1, 0);
     for (int j = 0; j < L; ++j) {
@@ -1073,12 +1161,7 @@ int wt_gpu_set_state(wt_gpu_ctx* c, const double* theta, const double* phi, int3
       upload(c->ds.theta, theta, c->L, c->stream);
       c->fk_valid = false;
     }
-    if (phi) {
-      std::vector<double4> ph(static_cast<size_t>(c->V));
-      for (int i = 0; i < c->V; ++i) ph[i] = make_double4(phi[3 * i], phi[3 * i + 1], phi[3 * i + 2], 0.0);
-      upload(c->phi[c->cur], ph.data(), c->V, c->stream);
-      WT_CUDA(cudaStreamSynchronize(c->stream));
-    }
+    if (phi) phi_put(c, c->phi[c->cur], phi);
     c->frame_index = frame_index;
     WT_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -1095,18 +1178,9 @@ int wt_gpu_get_state(wt_gpu_ctx* c, double* theta, double* phi, int32_t* frame_i
     WT_CUDA(cudaSetDevice(c->device));
     if (theta)
       WT_CUDA(cudaMemcpyAsync(theta, c->ds.theta, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
-    std::vector<double4> ph;
-    if (phi) {
-      ph.resize(static_cast<size_t>(c->V));
-      WT_CUDA(cudaMemcpyAsync(ph.data(), c->phi[c->cur], sizeof(double4) * c->V, cudaMemcpyDeviceToHost,
-                              c->stream));
-    }
+    if (phi) phi_get_async(c, c->phi[c->cur]);
     WT_CUDA(cudaStreamSynchronize(c->stream));
-    for (size_t i = 0; i < ph.size(); ++i) {
-      phi[3 * i] = ph[i].x;
-      phi[3 * i + 1] = ph[i].y;
-      phi[3 * i + 2] = ph[i].z;
-    }
+    if (phi) phi_unpack(c, phi);
     if (frame_index) *frame_index = c->frame_index;
   });
 }
@@ -1115,8 +1189,8 @@ static void ingest(wt_gpu_ctx* c, const float* depth_dev, double scale, const do
                    const uint8_t* valid_dev, cudaStream_t st = nullptr) {
   // batch: depth_dev / cloud_dev / valid_dev are the arena buffers (same stride)
   if (!st) st = c->stream;
-  if (c->nseq == 1) WT_CUDA(cudaMemsetAsync(c->d_nvalid, 0, sizeof(int), st));
-  else WT_CUDA(cudaMemset2DAsync(c->d_nvalid, static_cast<size_t>(c->bstride), 0, sizeof(int), c->nseq, st));
+  if (c->nseq == 1) WT_CUDA(cudaMemsetAsync(c->d_nvalid, 0, 4 * sizeof(int), st));
+  else WT_CUDA(cudaMemset2DAsync(c->d_nvalid, static_cast<size_t>(c->bstride), 0, 4 * sizeof(int), c->nseq, st));
   const int segs = (c->din.W + wt::kIngestSeg - 1) / wt::kIngestSeg;
   (c->nseq > 1 ? wt::k_ingest<true> : wt::k_ingest<false>)<<<dim3(segs * c->din.H, c->nseq), wt::kIngestSeg, 0, st>>>(
       c->din, depth_dev, scale, cloud_dev, valid_dev, c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid, c->bstride);
@@ -1204,6 +1278,30 @@ int wt_gpu_debug_pose(wt_gpu_ctx* c, long long* out) {
   if (!c || !c->pose_dbg) return 0;
   cudaMemcpy(out, c->pose_dbg, sizeof(long long) * (8 + 4 * 296), cudaMemcpyDeviceToHost);
   return 5;
+}
+
+int wt_gpu_host_alloc(size_t bytes, void** out) {
+  if (!out) return WT_EINVAL;
+  *out = nullptr;
+  return guarded(nullptr, [&] {
+    const cudaError_t e = cudaMallocHost(out, std::max<size_t>(bytes, 1));
+    if (e != cudaSuccess) throw CudaError{WT_ENOMEM, std::string("cudaMallocHost: ") + cudaGetErrorString(e)};
+  });
+}
+
+void wt_gpu_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int wt_gpu_bucket_count(wt_gpu_ctx* c, int32_t seq, int32_t* n_bucketed) {
+  if (!c || !n_bucketed) return WT_EINVAL;
+  return guarded(c, [&] {
+    WT_CUDA(cudaSetDevice(c->device));
+    if (seq < 0 || seq >= c->nseq) fail(WT_EINVAL, "sequence index out of range");
+    WT_CUDA(cudaMemcpyAsync(n_bucketed, seq_at(c->ds.poff, c, seq) + c->P, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            c->stream));
+    WT_CUDA(cudaStreamSynchronize(c->stream));
+  }, true);
 }
 
 int wt_gpu_sync(wt_gpu_ctx* c) {
@@ -1512,6 +1610,7 @@ int wt_gpu_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* kin, const wt_assoc
     WT_CUDA(cudaStreamSynchronize(c->stream));
     if (stats) put_kin(c, nk, stats, cap);
     if (n_out) *n_out = nk;
+    check_range(c, nk);
   });
 }
 
@@ -1626,17 +1725,20 @@ void read_association(cudaStream_t st, int V, const wt::DevState& s, double* p_t
   std::vector<unsigned long long> acc(4 * static_cast<size_t>(V));
   std::vector<double4> pv(static_cast<size_t>(V));
   std::vector<float4> pn(static_cast<size_t>(V));
+  double max_abs = 0.0;  // the frame's observation-sum scale (k_ingest)
+  WT_CUDA(cudaMemcpyAsync(&max_abs, s.fwords + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
   WT_CUDA(cudaMemcpyAsync(acc.data(), s.acc, sizeof(unsigned long long) * 4 * V, cudaMemcpyDeviceToHost, st));
   WT_CUDA(cudaMemcpyAsync(pv.data(), s.pv, sizeof(double4) * V, cudaMemcpyDeviceToHost, st));
   WT_CUDA(cudaMemcpyAsync(pn.data(), s.pn, sizeof(float4) * V, cudaMemcpyDeviceToHost, st));
   WT_CUDA(cudaStreamSynchronize(st));
+  const double oscale = wt::obs_scale_of(max_abs);
   for (int i = 0; i < V; ++i) {
     const long long cnt = static_cast<long long>(acc[4 * i + 3]);
     double pt[3] = {0, 0, 0}, r = 0.0;
     if (cnt > 0) {
       const double inv = 1.0 / static_cast<double>(cnt);
       for (int k = 0; k < 3; ++k)
-        pt[k] = static_cast<double>(static_cast<long long>(acc[4 * i + k])) / wt::kFixPoint * inv;
+        pt[k] = static_cast<double>(static_cast<long long>(acc[4 * i + k])) / oscale * inv;
       r = static_cast<double>(pn[i].x) * (pt[0] - pv[i].x) + static_cast<double>(pn[i].y) * (pt[1] - pv[i].y) +
           static_cast<double>(pn[i].z) * (pt[2] - pv[i].z);
     }
@@ -1754,7 +1856,10 @@ int wt_gpu_normal_system(wt_gpu_ctx* c, const double* theta, const wt_kin_config
     enq_fk(c, c->hs);
     enq_skin(c, c->hs, c->phi[c->cur]);
     enq_normals(c, c->hs, false, false);
-    enq_pose(c, c->hs, c->phi[c->cur], kin, 0, false, d_cnt, d_res);
+    double rmax = 0.0;  // the given residuals bound |r| (the role of the cutoff)
+    for (int i = 0; i < V; ++i)
+      if (count[i] > 0) rmax = std::max(rmax, std::fabs(residual[i]));
+    enq_pose(c, c->hs, c->phi[c->cur], kin, 0, false, d_cnt, d_res, rmax);
     std::vector<double> out(static_cast<size_t>(L * L + L));
     WT_CUDA(cudaMemcpyAsync(out.data(), c->hs.sys_out, sizeof(double) * out.size(), cudaMemcpyDeviceToHost,
                             c->stream));
@@ -1834,11 +1939,7 @@ int wt_gpu_batch_set_state(wt_gpu_ctx* c, int32_t seq, const double* theta, cons
       upload(seq_at(c->ds.theta, c, seq), theta, c->L, c->stream);
       c->fk_valid = false;
     }
-    if (phi) {
-      std::vector<double4> ph(static_cast<size_t>(c->V));
-      for (int i = 0; i < c->V; ++i) ph[i] = make_double4(phi[3 * i], phi[3 * i + 1], phi[3 * i + 2], 0.0);
-      upload(seq_at(c->phi[c->cur], c, seq), ph.data(), c->V, c->stream);
-    }
+    if (phi) phi_put(c, seq_at(c->phi[c->cur], c, seq), phi);
     WT_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
@@ -1851,18 +1952,9 @@ int wt_gpu_batch_get_state(wt_gpu_ctx* c, int32_t seq, double* theta, double* ph
     if (theta)
       WT_CUDA(cudaMemcpyAsync(theta, seq_at(c->ds.theta, c, seq), sizeof(double) * c->L, cudaMemcpyDeviceToHost,
                               c->stream));
-    std::vector<double4> ph;
-    if (phi) {
-      ph.resize(static_cast<size_t>(c->V));
-      WT_CUDA(cudaMemcpyAsync(ph.data(), seq_at(c->phi[c->cur], c, seq), sizeof(double4) * c->V,
-                              cudaMemcpyDeviceToHost, c->stream));
-    }
+    if (phi) phi_get_async(c, seq_at(c->phi[c->cur], c, seq));
     WT_CUDA(cudaStreamSynchronize(c->stream));
-    for (size_t i = 0; i < ph.size(); ++i) {
-      phi[3 * i] = ph[i].x;
-      phi[3 * i + 1] = ph[i].y;
-      phi[3 * i + 2] = ph[i].z;
-    }
+    if (phi) phi_unpack(c, phi);
   });
 }
 

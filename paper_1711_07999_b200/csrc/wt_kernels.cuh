@@ -21,9 +21,21 @@
 namespace wt {
 
 constexpr int kVThreads = 256;    // per-vertex / per-pixel kernels
-constexpr double kFixPoint = 17592186044416.0;     // 2^44: observation sums (<= 121 px/vertex, |x| < 4096 m)
-constexpr double kFixSys = 1099511627776.0;       // 2^40: JtJ / Jtr / shape sums
-constexpr double kFixRes = 17592186044416.0;      // 2^44: residual sum of squares
+// Fixed-point reductions. Every cross-thread sum of the frame is a 64-bit
+// integer sum (associative, so bitwise reproducible whatever the schedule),
+// at a power-of-two scale chosen so no sum can leave the int64 range in any
+// length unit (the reference sums in fp64 and works in metres or
+// millimetres alike):
+//  - observation sums: 2^e per frame, from the largest coordinate magnitude of
+//    the frame's valid points (k_ingest) -- a vertex collects at most
+//    (2*16+1)^2 < 2^11 points, so e = min(44, 51 - ceil(log2 max|x|)): 2^-44 m
+//    for metre-scale scenes, 2^-39 mm for millimetre depth;
+//  - JtJ / Jtr and sum r^2: per call from the vertex count, the model's lever
+//    arm and the cutoff (pose_scales, wt_gpu.cu): 2^-40 / 2^-44 at metre scale;
+//    k_pose_solve still checks the non-negative sums (diagonal, sum r^2) for
+//    wrap-around and reports WT_ERANGE instead of taking a garbage step;
+//  - the shape statistics are fp64 per-CTA partials folded in CTA order.
+constexpr int kObsExpMax = 44, kObsExpBudget = 51;
 constexpr int kRedCopies = 8;  // CTAs spread their fixed-point atomics over this many slot copies
 
 struct DevModel {
@@ -85,6 +97,8 @@ struct DevState {
   KinStat* kin_stats;
   ShapeStat* shape_stats;
   double* sys_out;           // optional JtJ/Jtr dump [L*L + L]
+  const int* fwords;         // the frame's words: [0] valid-pixel list length, [2..3] max |coordinate| bits
+  double* spart;             // shape statistics: 5 fp64 partials per CTA
   long long bstride;         // bytes between the arenas of consecutive sequences of a batch
 };
 
@@ -134,6 +148,8 @@ __device__ inline DevState seq_state(DevState s) {
   s.kin_stats = seq_ptr(s.kin_stats, o);
   s.shape_stats = seq_ptr(s.shape_stats, o);
   s.sys_out = seq_ptr(s.sys_out, o);
+  s.fwords = seq_ptr(s.fwords, o);
+  s.spart = seq_ptr(s.spart, o);
   return s;
 }
 
@@ -225,6 +241,19 @@ __device__ __forceinline__ void red_add(unsigned long long* p, long long v) {
 
 __device__ __forceinline__ double unfix(unsigned long long v, double scale) {
   return static_cast<double>(static_cast<long long>(v)) / scale;
+}
+
+// Scale of the frame's observation sums (see kObsExpBudget) from the largest
+// coordinate magnitude k_ingest recorded in frame words [2..3].
+__host__ __device__ inline double obs_scale_of(double max_abs) {
+  int ex = 0;
+  frexp(max_abs, &ex);  // max_abs < 2^ex
+  const int e = kObsExpBudget - ex < kObsExpMax ? kObsExpBudget - ex : kObsExpMax;
+  return ldexp(1.0, e);
+}
+
+__device__ __forceinline__ double obs_scale(const int* fwords) {
+  return obs_scale_of(__longlong_as_double(__ldcg(reinterpret_cast<const long long*>(fwords + 2))));
 }
 
 // Returns true in every thread of the CTA that finished last (grid-wide),
@@ -461,6 +490,7 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
   const int u = (blockIdx.x % segs) * kIngestSeg + threadIdx.x;
   const int i = v * in.W + u;
   int valid = 0;
+  double mx = 0.0;  // max |coordinate| of this pixel's point
   if (u < in.W) {
     double x = 0, y = 0, z = 0;
     if (depth) {
@@ -484,9 +514,19 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
       pts_hi[3 * i] = x;
       pts_hi[3 * i + 1] = y;
       pts_hi[3 * i + 2] = z;
+      mx = fmax(fabs(x), fmax(fabs(y), fabs(z)));
     }
   }
   const int lane = threadIdx.x & 31;
+  {
+    // largest coordinate magnitude of the frame (the observation-sum scale):
+    // a warp maximum, then one integer atomicMax on the bits (non-negative
+    // doubles order like their bit patterns)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0 && mx > 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(n_valid + 2), static_cast<unsigned long long>(__double_as_longlong(mx)));
+  }
   const unsigned m = __ballot_sync(0xffffffffu, valid);
   if (m) {
     // a run padded to a multiple of kRunAlign (the pixels of one search warp)
@@ -862,13 +902,13 @@ __device__ __forceinline__ void scan_span(const DevState& s, int e0, int e1, dou
 
 // Per-pixel result: the winner map entry and the scatter-average sums.
 __device__ __forceinline__ void search_emit(const DevState& s, const SearchArgs& a, int pix, int best_i, double px,
-                                            double py, double pz) {
+                                            double py, double pz, double oscale) {
   if (a.write_winners) a.winners[pix] = best_i;
   if (best_i >= 0) {
     unsigned long long* acc = s.acc + 4 * static_cast<size_t>(best_i);
-    red_add(acc + 0, fix(px, kFixPoint));
-    red_add(acc + 1, fix(py, kFixPoint));
-    red_add(acc + 2, fix(pz, kFixPoint));
+    red_add(acc + 0, fix(px, oscale));
+    red_add(acc + 1, fix(py, oscale));
+    red_add(acc + 2, fix(pz, oscale));
     red_add(acc + 3, 1ll);
   }
 }
@@ -922,6 +962,7 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
   if constexpr (B) f = seq_frame(f);
   if constexpr (B) a.winners = seq_ptr(a.winners, seq_off(s.bstride));
   const int nv = *f.n_valid;
+  const double oscale = obs_scale(f.n_valid);
   const int w = a.window;
   const int K1 = min(NR, w);
   const double ifx = 1.0 / a.fx, ify = 1.0 / a.fy;
@@ -998,7 +1039,7 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
         best_i = bi;
       }
     }
-    if (act && sub == 0) search_emit(s, a, pix, best_i, px, py, pz);
+    if (act && sub == 0) search_emit(s, a, pix, best_i, px, py, pz, oscale);
   }
 }
 
@@ -1007,15 +1048,15 @@ __device__ __forceinline__ ulonglong4 load_obs(const unsigned long long* acc, in
   return ld256(reinterpret_cast<const ulonglong4*>(acc) + i);
 }
 
-__device__ __forceinline__ bool observed_mean(const ulonglong4& q, double* pt, long long* cnt) {
+__device__ __forceinline__ bool observed_mean(const ulonglong4& q, double oscale, double* pt, long long* cnt) {
   const ulonglong2 a01 = make_ulonglong2(q.x, q.y), a23 = make_ulonglong2(q.z, q.w);
   const long long c = static_cast<long long>(a23.y);
   *cnt = c;
   if (c <= 0) return false;
   const double inv = 1.0 / static_cast<double>(c);
-  pt[0] = unfix(a01.x, kFixPoint) * inv;
-  pt[1] = unfix(a01.y, kFixPoint) * inv;
-  pt[2] = unfix(a23.x, kFixPoint) * inv;
+  pt[0] = unfix(a01.x, oscale) * inv;
+  pt[1] = unfix(a01.y, oscale) * inv;
+  pt[2] = unfix(a23.x, oscale) * inv;
   return true;
 }
 
@@ -1156,6 +1197,8 @@ struct PoseArgs {
   const int* count_in;   // optional association override (stage hook)
   const double* res_in;
   long long* dbg;        // optional timing record of the last CTA (WT_DEBUG_POSE)
+  double sys_scale;      // fixed-point scale of JtJ / Jtr (pose_scales, wt_gpu.cu)
+  double res_scale;      // ... of sum r^2
 };
 
 // Shared-memory layout of k_pose_system for L links, NP dchain pairs and
@@ -1287,7 +1330,8 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
     eidx[q] = e;
   }
   __syncwarp();
-  long long rsq = 0, nassoc = 0;  // sum r^2 (2^-44 fixed point), associated count
+  long long rsq = 0, nassoc = 0;  // sum r^2 (fixed point at a.res_scale), associated count
+  const double oscale = a.count_in ? 1.0 : obs_scale(s.fwords);
   double* wrows = rows + warp * 32 * Lr;
   const int TW = gridDim.x * nw, gw = blockIdx.x * nw + warp;
   int* wq = qidx + warp * 64;       // warp-private queue of associated vertices
@@ -1315,15 +1359,15 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
           if (have) {
             if (a.clean_acc) clear_acc(s.acc, i);
             const double inv = 1.0 / static_cast<double>(c);
-            const double px = unfix(a01.x, kFixPoint) * inv, py = unfix(a01.y, kFixPoint) * inv,
-                         pz = unfix(a23.x, kFixPoint) * inv;
+            const double px = unfix(a01.x, oscale) * inv, py = unfix(a01.y, oscale) * inv,
+                         pz = unfix(a23.x, oscale) * inv;
             r = static_cast<double>(n.x) * (px - v.x) + static_cast<double>(n.y) * (py - v.y) +
                 static_cast<double>(n.z) * (pz - v.z);
           }
         }
       }
       if (have) {
-        rsq += fix(r * r, kFixRes);
+        rsq += fix(r * r, a.res_scale);
         ++nassoc;
       }
       const unsigned hm = __ballot_sync(0xffffffffu, have);
@@ -1411,7 +1455,7 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
         }
 #pragma unroll
         for (int q = 0; q < NACC; ++q)
-          if (eidx[q] >= 0) wpart[eidx[q]] += fix(acc[q], kFixSys);
+          if (eidx[q] >= 0) wpart[eidx[q]] += fix(acc[q], a.sys_scale);
       }
       // drop the processed rows from the queue
       const int rest_n = qn - nrows;
@@ -1498,6 +1542,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
   __shared__ double s_rsum;
   __shared__ long long s_nassoc;
   __shared__ int s_finite;
+  int wrapped = 0;  // a non-negative fixed-point sum (diagonal, sum r^2) left the int64 range
   const int L = m.L;
   const int Lp = L | 1;
   const int NT = L * (L + 1) / 2;
@@ -1553,9 +1598,10 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
         s.red[c * (NE + 2) + NE] = 0ull;
         s.red[c * (NE + 2) + NE + 1] = 0ull;
       }
-      s_rsum = unfix(rs, kFixRes);
+      s_rsum = unfix(rs, a.res_scale);
       s_nassoc = static_cast<long long>(na);
       s_finite = 1;
+      wrapped |= static_cast<long long>(rs) < 0 ? 1 : 0;
     }
   }
 #pragma unroll
@@ -1567,7 +1613,8 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
     const int ca = ent[q] & 0xFFFF, cb = ent[q] >> 16;
     ea[e] = static_cast<unsigned short>(ca);
     eb[e] = static_cast<unsigned short>(cb == L ? 0xFFFF : cb);
-    const double val = unfix(sum[q], kFixSys);
+    if (ca == cb && static_cast<long long>(sum[q]) < 0) wrapped = 1;
+    const double val = unfix(sum[q], a.sys_scale);
     if (cb == L) {
       jtr[ca] = val;
     } else {
@@ -1585,7 +1632,8 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
     const int ca = en & 0xFFFF, cb = en >> 16;
     ea[e] = static_cast<unsigned short>(ca);
     eb[e] = static_cast<unsigned short>(cb == L ? 0xFFFF : cb);
-    const double val = unfix(t, kFixSys);
+    if (ca == cb && static_cast<long long>(t) < 0) wrapped = 1;
+    const double val = unfix(t, a.sys_scale);
     if (cb == L) {
       jtr[ca] = val;
     } else {
@@ -1593,7 +1641,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
       A[cb * Lp + ca] = val;
     }
   }
-  __syncthreads();
+  const int out_of_range = __syncthreads_or(wrapped);
   // default-pose prior (lambda_s S)^2 on the diagonal (kinopt.cpp:113-117),
   // then A = JtJ + lambda_k diag(JtJ) + floor I (kinopt.cpp:121-126)
   for (int k = threadIdx.x; k < L; k += blockDim.x) {
@@ -1608,6 +1656,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
     for (int k = threadIdx.x; k < L; k += blockDim.x) s.sys_out[L * L + k] = jtr[k];
     return;
   }
+  if (out_of_range && threadIdx.x == 0) s_finite = 0;
   for (int e = threadIdx.x; e < L * L; e += blockDim.x)
     if (!isfinite(A[(e / L) * Lp + e % L])) s_finite = 0;
   for (int k = threadIdx.x; k < L; k += blockDim.x)
@@ -1640,7 +1689,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
         st.residual_sum = s_rsum;
         st.associated = static_cast<int>(s_nassoc);
         st.step_norm = ok ? sqrt(nrm) : 0.0;
-        st.skipped = ok ? 0 : 1;
+        st.skipped = ok ? 0 : (out_of_range ? 2 : 1);  // 2: reported as WT_ERANGE by the host
         s.kin_stats[a.iteration] = st;
       }
     }
@@ -1662,7 +1711,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
       st.residual_sum = s_rsum;
       st.associated = static_cast<int>(s_nassoc);
       st.step_norm = ok ? sqrt(nrm) : 0.0;
-      st.skipped = ok ? 0 : 1;
+      st.skipped = ok ? 0 : (out_of_range ? 2 : 1);
       s.kin_stats[a.iteration] = st;
     }
     __syncthreads();
@@ -1733,6 +1782,44 @@ __device__ __forceinline__ bool solve_vertex3(const double g[3], double r, const
   return true;
 }
 
+// Shape statistics as fp64 per-CTA partials (sum |r|, observed, sum |phi|,
+// singular, max |phi|), written by thread 0 of every CTA; the CTA that
+// finishes last folds them in CTA order -- deterministic for a given grid and
+// free of any fixed-point range (phi and r in any length unit).
+constexpr int kStatParts = 5;
+
+__device__ inline void stat_partials_put(double* spart, double a, double b, double c, double d, double mx) {
+  double* p = spart + kStatParts * blockIdx.x;
+  p[0] = a;
+  p[1] = b;
+  p[2] = c;
+  p[3] = d;
+  p[4] = mx;
+}
+
+// In the last CTA (all threads): the CTA-ordered fold; result in out[] of thread 0.
+__device__ inline void stat_partials_fold(const double* spart, double out[kStatParts]) {
+  double acc[kStatParts] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {  // thread t: CTAs t, t + T, ... in order
+    const double* p = spart + kStatParts * b;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] += __ldcg(p + k);
+    acc[4] = fmax(acc[4], __ldcg(p + 4));
+  }
+  __shared__ double red[kStatParts][kVThreads];
+#pragma unroll
+  for (int k = 0; k < kStatParts; ++k) red[k][threadIdx.x] = acc[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kStatParts; ++k) out[k] = 0.0;
+    for (int t = 0; t < static_cast<int>(blockDim.x); ++t) {  // thread order
+#pragma unroll
+      for (int k = 0; k < 4; ++k) out[k] += red[k][t];
+      out[4] = fmax(out[4], red[4][t]);
+    }
+  }
+}
+
 struct ShapeArgs {
   double lambda_phi, lambda_nbr, lambda_w, diag_floor;
   int iteration;
@@ -1753,6 +1840,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
   __syncthreads();
   double abs_r = 0.0, sum_phi = 0.0, max_phi = 0.0;
   long long observed = 0, singular = 0;
+  const double oscale = obs_scale(s.fwords);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
     // every load of the vertex up front (the 256-bit loads keep program order)
     const double4 f = ld256(phi_in + i);
@@ -1793,7 +1881,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
     double r = 0.0;
     double pt[3];
     long long cnt = 0;
-    if (observed_mean(obs, pt, &cnt)) {
+    if (observed_mean(obs, oscale, pt, &cnt)) {
       if (a.clean_acc) clear_acc(s.acc, i);
       const double4 v = ld256(s.pv + i);
       const float4 n = s.pn[i];
@@ -1823,7 +1911,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
     sum_phi += len;
     max_phi = fmax(max_phi, len);
   }
-  // block reductions (fixed order) then fixed-point atomics
+  // block reductions (fixed order), then per-CTA partials folded by the last CTA
   block_sum2(abs_r, observed);
   double sp = sum_phi;
   block_sum2(sp, singular);
@@ -1835,20 +1923,17 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int k = 0; k < (blockDim.x >> 5); ++k) mx = fmax(mx, smax[k]);
-    red_add(s.red + 0, fix(abs_r, kFixSys));
-    red_add(s.red + 1, observed);
-    red_add(s.red + 2, fix(sp, kFixSys));
-    red_add(s.red + 3, singular);
-    atomicMax(s.red + 4, static_cast<unsigned long long>(__double_as_longlong(mx)));
+    stat_partials_put(s.spart, abs_r, static_cast<double>(observed), sp, static_cast<double>(singular), mx);
   }
   if (!last_block(s.tickets + 2)) return;
+  double tot[kStatParts];
+  stat_partials_fold(s.spart, tot);
   if (threadIdx.x == 0) {
-    const double sabs = unfix(__ldcg(s.red + 0), kFixSys);
-    const long long nobs = static_cast<long long>(__ldcg(s.red + 1));
-    const double sphi = unfix(__ldcg(s.red + 2), kFixSys);
-    const long long nsing = static_cast<long long>(__ldcg(s.red + 3));
-    const double mphi = __longlong_as_double(static_cast<long long>(__ldcg(s.red + 4)));
-    for (int k = 0; k < 5; ++k) s.red[k] = 0ull;
+    const double sabs = tot[0];
+    const long long nobs = static_cast<long long>(tot[1]);
+    const double sphi = tot[2];
+    const long long nsing = static_cast<long long>(tot[3]);
+    const double mphi = tot[4];
     ShapeStat st;
     st.mean_phi = m.V > 0 ? sphi / static_cast<double>(m.V) : 0.0;
     st.max_phi = mphi;
@@ -1868,10 +1953,11 @@ static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, De
   if constexpr (B) s = seq_state(s);
   double abs_r = 0.0;
   long long observed = 0;
+  const double oscale = obs_scale(s.fwords);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
     double pt[3];
     long long cnt = 0;
-    if (observed_mean(load_obs(s.acc, i), pt, &cnt)) {
+    if (observed_mean(load_obs(s.acc, i), oscale, pt, &cnt)) {
       if (clean_acc) clear_acc(s.acc, i);
       const double4 v = ld256(s.pv + i);
       const float4 n = s.pn[i];
@@ -1881,16 +1967,13 @@ static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, De
     }
   }
   block_sum2(abs_r, observed);
-  if (threadIdx.x == 0) {
-    red_add(s.red + 0, fix(abs_r, kFixSys));
-    red_add(s.red + 1, observed);
-  }
+  if (threadIdx.x == 0) stat_partials_put(s.spart, abs_r, static_cast<double>(observed), 0.0, 0.0, 0.0);
   if (!last_block(s.tickets + 3)) return;
+  double tot[kStatParts];
+  stat_partials_fold(s.spart, tot);
   if (threadIdx.x == 0) {
-    const double sabs = unfix(__ldcg(s.red + 0), kFixSys);
-    const long long nobs = static_cast<long long>(__ldcg(s.red + 1));
-    s.red[0] = 0ull;
-    s.red[1] = 0ull;
+    const double sabs = tot[0];
+    const long long nobs = static_cast<long long>(tot[1]);
     for (int k = 0; k + 1 < n_its; ++k)
       s.shape_stats[k].mean_abs_r_after = s.shape_stats[k + 1].mean_abs_r_before;
     if (n_its > 0) s.shape_stats[n_its - 1].mean_abs_r_after = nobs > 0 ? sabs / nobs : 0.0;

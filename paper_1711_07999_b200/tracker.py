@@ -168,6 +168,14 @@ class Tracker:
         self._kin = (_lib.KinIterStats * 64)()
         self._shape = (_lib.ShapeIterStats * 64)()
 
+    def _ensure_stats(self, n_kin: int, n_shape: int) -> None:
+        """Stats arrays sized for the call's iteration counts (the reference
+        has no iteration cap), before anything is launched."""
+        if n_kin > len(self._kin):
+            self._kin = (_lib.KinIterStats * n_kin)()
+        if n_shape > len(self._shape):
+            self._shape = (_lib.ShapeIterStats * n_shape)()
+
     # ---- state ---------------------------------------------------------------
     def close(self) -> None:
         if self._ctx:
@@ -218,12 +226,13 @@ class Tracker:
         check(lib().wt_gpu_load_cloud(self._ctx, ptr(p), ptr(v)), self._ctx)
 
     def _stats(self) -> _lib.FrameStatsC:
-        return _lib.FrameStatsC(0, 0, 0, 64, 64, 0, self._kin, self._shape)
+        return _lib.FrameStatsC(0, 0, 0, len(self._kin), len(self._shape), 0, self._kin, self._shape)
 
     def track_frame(self, cfg: TrackConfig, depth=None, depth_scale: float = 1.0, cloud=None,
                     stats: bool = True) -> FrameStats | None:
         """track_frame (tracker.cpp:54-68) on a depth image, an organized
         cloud (points, valid), or the frame already loaded."""
+        self._ensure_stats(cfg.kin.iterations, cfg.shape.iterations)
         if depth is not None:
             self.load_depth(depth, depth_scale)
         elif cloud is not None:
@@ -270,16 +279,18 @@ class Tracker:
 
     def optimize_pose(self, kin: KinSolverConfig, assoc: AssocConfig = AssocConfig()) -> list:
         n = C.c_int32()
-        check(lib().wt_gpu_optimize_pose(self._ctx, C.byref(kin.c()), C.byref(assoc.c()), self._kin, 64,
-                                         C.byref(n)), self._ctx)
-        return _kin_list(self._kin, min(n.value, 64))
+        self._ensure_stats(kin.iterations, 0)
+        check(lib().wt_gpu_optimize_pose(self._ctx, C.byref(kin.c()), C.byref(assoc.c()), self._kin,
+                                         len(self._kin), C.byref(n)), self._ctx)
+        return _kin_list(self._kin, min(n.value, len(self._kin)))
 
     def optimize_shape(self, shape: ShapeSolverConfig, assoc: AssocConfig = AssocConfig(),
                        stats: bool = True) -> list:
         n = C.c_int32()
+        self._ensure_stats(0, shape.iterations)
         check(lib().wt_gpu_optimize_shape(self._ctx, C.byref(shape.c()), C.byref(assoc.c()), int(stats),
-                                          self._shape, 64, C.byref(n)), self._ctx)
-        return _shape_list(self._shape, min(n.value, 64)) if stats else []
+                                          self._shape, len(self._shape), C.byref(n)), self._ctx)
+        return _shape_list(self._shape, min(n.value, len(self._shape))) if stats else []
 
     # ---- stage hooks ---------------------------------------------------------
     def skin(self, theta, phi=None):

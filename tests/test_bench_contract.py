@@ -13,13 +13,44 @@ from .conftest import ROOT
 
 
 def test_alg_bytes_match_survey_8d():
+    """SURVEY §8(d)'s per-kernel bytes, each attributed to the kernel that
+    does the work: K3 splits into the per-vertex histogram (normals), the
+    per-pixel scan (pixoff) and the scatter; K5's per-pixel accumulation sits
+    in the search and its per-vertex finalize (72 B/V) in every consumer."""
     V, P, A, Vv = 102392, 640 * 480, 16000, 51196
     assert bench.alg_bytes("skin", V, P, A, Vv) == 56 * V                          # K1
-    assert bench.alg_bytes("normals+bucket", V, P, A, Vv) == 77 * V + 37 * V + 16 * P  # K2 + K3
-    assert bench.alg_bytes("search+average", V, P, A, Vv) == 12 * P + 16 * Vv + 8 * P + 72 * V  # K4 + K5
-    assert bench.alg_bytes("pose_system", V, P, A, Vv) == 4 * V + 61 * A           # K6
-    assert bench.alg_bytes("shape_step", V, P, A, Vv) == 81 * V                    # K8
+    assert bench.alg_bytes("normals+bucket", V, P, A, Vv) == 77 * V + 37 * V      # K2 + K3 (per vertex)
+    assert bench.alg_bytes("pixoff", V, P, A, Vv) == 16 * P                        # K3 (per pixel)
+    assert bench.alg_bytes("scatter", V, P, A, Vv) == 8 * Vv                       # K3 (scatter)
+    assert bench.alg_bytes("search+average", V, P, A, Vv) == 12 * P + 16 * Vv + 8 * P  # K4 + K5 (per pixel)
+    assert bench.alg_bytes("pose_system", V, P, A, Vv) == 4 * V + 61 * A + 72 * V  # K6 + K5 finalize
+    assert bench.alg_bytes("shape_step", V, P, A, Vv) == 81 * V + 72 * V           # K8 + K5 finalize
     assert bench.alg_bytes("pose_solve", V, P, A, Vv) == 0
+    # the per-frame total is SURVEY's pose iteration (254 V + 61 A + 36 P) x 5
+    # + shape iteration (331 V + 36 P) x 2, plus the stats pass's association
+    per_frame = (5 * sum(bench.alg_bytes(k, V, P, A, Vv) for k in
+                         ("skin", "normals+bucket", "pixoff", "scatter", "search+average", "pose_system")) +
+                 2 * sum(bench.alg_bytes(k, V, P, A, Vv) for k in
+                         ("skin", "normals+bucket", "pixoff", "scatter", "search+average", "shape_step")))
+    assert per_frame == 5 * (254 * V + 61 * A + 36 * P + 8 * Vv + 16 * Vv - 8 * V) + \
+        2 * (331 * V + 36 * P + 8 * Vv + 16 * Vv - 8 * V)
+
+
+@pytest.mark.timeout(300)
+def test_multi_gpu_spawn_path_with_gloo():
+    """--gpus 2 without torchrun re-launches bench.py as two ranks (one
+    process per GPU) that shard C5's 64 sequences; the plumbing check runs
+    that path on CPU over gloo: n_gpus == 2, two distinct processes, each
+    rank its 32 sequences, rank 0 alone prints."""
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--plumbing-check"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=280)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["max_ms"] == 2.0
+    assert [s["sequences"] for s in d["shards"]] == [list(range(32)), list(range(32, 64))]
+    assert len({s["pid"] for s in d["shards"]}) == 2
 
 
 def test_ncu_traffic_table():
