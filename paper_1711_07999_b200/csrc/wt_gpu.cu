@@ -1725,13 +1725,13 @@ void read_association(cudaStream_t st, int V, const wt::DevState& s, double* p_t
   std::vector<unsigned long long> acc(4 * static_cast<size_t>(V));
   std::vector<double4> pv(static_cast<size_t>(V));
   std::vector<float4> pn(static_cast<size_t>(V));
-  double max_abs = 0.0;  // the frame's observation-sum scale (k_ingest)
-  WT_CUDA(cudaMemcpyAsync(&max_abs, s.fwords + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
+  long long max_abs = 0;  // bits of the frame's largest coordinate magnitude (k_ingest): the sums' scale
+  WT_CUDA(cudaMemcpyAsync(&max_abs, s.fwords + 2, sizeof(long long), cudaMemcpyDeviceToHost, st));
   WT_CUDA(cudaMemcpyAsync(acc.data(), s.acc, sizeof(unsigned long long) * 4 * V, cudaMemcpyDeviceToHost, st));
   WT_CUDA(cudaMemcpyAsync(pv.data(), s.pv, sizeof(double4) * V, cudaMemcpyDeviceToHost, st));
   WT_CUDA(cudaMemcpyAsync(pn.data(), s.pn, sizeof(float4) * V, cudaMemcpyDeviceToHost, st));
   WT_CUDA(cudaStreamSynchronize(st));
-  const double oscale = wt::obs_scale_of(max_abs);
+  const double oscale = wt::obs_scale_of_bits(max_abs);
   for (int i = 0; i < V; ++i) {
     const long long cnt = static_cast<long long>(acc[4 * i + 3]);
     double pt[3] = {0, 0, 0}, r = 0.0;

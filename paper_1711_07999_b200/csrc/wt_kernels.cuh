@@ -244,16 +244,22 @@ __device__ __forceinline__ double unfix(unsigned long long v, double scale) {
 }
 
 // Scale of the frame's observation sums (see kObsExpBudget) from the largest
-// coordinate magnitude k_ingest recorded in frame words [2..3].
-__host__ __device__ inline double obs_scale_of(double max_abs) {
-  int ex = 0;
-  frexp(max_abs, &ex);  // max_abs < 2^ex
+// coordinate magnitude k_ingest recorded in frame words [2..3]: 2^e with
+// e = min(44, 51 - ex), max_abs < 2^ex, built from the exponent bits.
+__host__ __device__ inline double obs_scale_of_bits(long long bits) {
+  const int biased = static_cast<int>((bits >> 52) & 0x7FF);
+  const int ex = biased == 0 ? 0 : biased - 1022;  // frexp's exponent (0 for zero / subnormal)
   const int e = kObsExpBudget - ex < kObsExpMax ? kObsExpBudget - ex : kObsExpMax;
-  return ldexp(1.0, e);
+  union {
+    long long i;
+    double d;
+  } u;
+  u.i = static_cast<long long>(e + 1023) << 52;
+  return u.d;
 }
 
 __device__ __forceinline__ double obs_scale(const int* fwords) {
-  return obs_scale_of(__longlong_as_double(__ldcg(reinterpret_cast<const long long*>(fwords + 2))));
+  return obs_scale_of_bits(__ldcg(reinterpret_cast<const long long*>(fwords + 2)));
 }
 
 // Returns true in every thread of the CTA that finished last (grid-wide),
@@ -1797,25 +1803,35 @@ __device__ inline void stat_partials_put(double* spart, double a, double b, doub
   p[4] = mx;
 }
 
-// In the last CTA (all threads): the CTA-ordered fold; result in out[] of thread 0.
+// In the last CTA (all threads): a fixed-shape fold -- thread t sums CTAs
+// t, t + T, ... in order, a shuffle butterfly per warp, then the warps in
+// order -- deterministic for a given grid; result in out[] of thread 0.
 __device__ inline void stat_partials_fold(const double* spart, double out[kStatParts]) {
   double acc[kStatParts] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {  // thread t: CTAs t, t + T, ... in order
+  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
     const double* p = spart + kStatParts * b;
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[k] += __ldcg(p + k);
     acc[4] = fmax(acc[4], __ldcg(p + 4));
   }
-  __shared__ double red[kStatParts][kVThreads];
 #pragma unroll
-  for (int k = 0; k < kStatParts; ++k) red[k][threadIdx.x] = acc[k];
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    acc[4] = fmax(acc[4], __shfl_xor_sync(0xffffffffu, acc[4], o));
+  }
+  __shared__ double red[kStatParts][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < kStatParts; ++k) red[k][wid] = acc[k];
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int k = 0; k < kStatParts; ++k) out[k] = 0.0;
-    for (int t = 0; t < static_cast<int>(blockDim.x); ++t) {  // thread order
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {  // warp order
 #pragma unroll
-      for (int k = 0; k < 4; ++k) out[k] += red[k][t];
-      out[4] = fmax(out[4], red[4][t]);
+      for (int k = 0; k < 4; ++k) out[k] += red[k][w];
+      out[4] = fmax(out[4], red[4][w]);
     }
   }
 }
@@ -1948,7 +1964,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
 // Closing measurement pass of optimize_shape (shapeopt.cpp:112-129): mean
 // |r| over observed vertices of a fresh association; fills mean_abs_r_after.
 template <bool B>
-static __global__ void __launch_bounds__(kVThreads) k_shape_after(DevModel m, DevState s, int n_its, int clean_acc) {
+static __global__ void __launch_bounds__(kVThreads, 5) k_shape_after(DevModel m, DevState s, int n_its, int clean_acc) {
   pdl_entry();
   if constexpr (B) s = seq_state(s);
   double abs_r = 0.0;

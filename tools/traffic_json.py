@@ -8,7 +8,7 @@ import collections
 import json
 import sys
 
-KIND = {"k_skin": "skin", "k_normals": "normals+bucket", "k_pixoff": "scatter", "k_scatter": "scatter",
+KIND = {"k_skin": "skin", "k_normals": "normals+bucket", "k_pixoff": "pixoff", "k_scatter": "scatter",
         "k_search": "search+average", "k_pose_system": "pose_system", "k_pose_solve": "pose_solve",
         "k_shape": "shape_step", "k_shape_after": "shape_stats", "k_fk": "fk", "k_ingest": "ingest"}
 
