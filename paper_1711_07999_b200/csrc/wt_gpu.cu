@@ -182,6 +182,8 @@ struct wt_gpu_ctx {
   std::vector<int> prof_kind;
 
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<const void*, int> resident;  // CTAs of 256 threads resident per SM, per kernel (occupancy API)
+  int sms = 148;
 
   // sequence driver: pinned staging + device double buffer + copy stream
   cudaStream_t copy_stream = nullptr;
@@ -270,6 +272,21 @@ void mark(wt_gpu_ctx* c, int kind) {
 }
 
 int vgrid(int n) { return std::max(1, (n + wt::kVThreads - 1) / wt::kVThreads); }
+
+// One wave of `kernel` (kVThreads per CTA) on this device: resident CTAs per
+// SM from the occupancy calculator (registers and shared memory as compiled)
+// times the SM count.
+template <class K>
+int full_wave(wt_gpu_ctx* c, K kernel) {
+  const void* key = reinterpret_cast<const void*>(kernel);
+  auto it = c->resident.find(key);
+  if (it == c->resident.end()) {
+    int n = 0;
+    WT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, wt::kVThreads, 0));
+    it = c->resident.emplace(key, std::max(1, n)).first;
+  }
+  return it->second * c->sms;
+}
 
 // per-sequence CTAs of a one-wave grid of `ctas` CTAs shared by a batch,
 // times batch_mult waves for a batch (WT_WAVE_<kind> overrides it, experiments)
@@ -516,16 +533,16 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
   static const int narrow_from = getenv("WT_NARROW_SEARCH_FROM") ? atoi(getenv("WT_NARROW_SEARCH_FROM")) : 8;
   const bool narrow = c->nseq > 1 && c->nseq >= narrow_from;
   const int G = narrow ? wt::kSearchGroupBatch : wt::kSearchGroupSolo;  // grid sizing
-  const int grid = std::max(1, std::min(c->P * G / wt::kVThreads + 1, wave(c, 5 * 148, "SEARCH", 8.0)));
   // a lone frame of more than 2^20 pixels (C4) has enough pixels in flight to
   // be throughput-bound: one lane per core row, 8-lane groups (1080p: 572 ->
   // 647 frames/s against the VGA form)
   const bool big_frame = c->nseq == 1 && c->P > (1 << 20);
-  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? (narrow ? wt::k_search<true>
-                                              : wt::k_search<true, wt::kNearRingsSolo, wt::kSearchGroupSolo,
-                                                             wt::kSearchSplitSolo>)
-                                     : (big_frame ? wt::k_search<false, wt::kNearRingsSolo, 8, 1> : wt::k_search<false>),
-                         dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
+  auto kern = c->nseq > 1 ? (narrow ? wt::k_search<true>
+                                    : wt::k_search<true, wt::kNearRingsSolo, wt::kSearchGroupSolo, wt::kSearchSplitSolo>)
+                          : (big_frame ? wt::k_search<false, wt::kNearRingsSolo, 8, 1> : wt::k_search<false>);
+  // one wave (warps stride over the pixel groups); a batch shares 8 waves between its sequences
+  const int grid = std::max(1, std::min(c->P * G / wt::kVThreads + 1, wave(c, full_wave(c, kern), "SEARCH", 8.0)));
+  WT_CUDA(wt::launch_pdl(kern, dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
   mark(c, K_SEARCH);
 }
 
@@ -582,6 +599,8 @@ void pose_scales(const wt_gpu_ctx* c, double cutoff, wt::PoseArgs& pa) {
   const double V = std::max(1, c->V), R = c->lever;
   pa.sys_scale = pow2_below(V * std::max(R * R, R * cutoff), 40);
   pa.res_scale = pow2_below(2.0 * V * cutoff * cutoff, 44);
+  pa.sys_inv = 1.0 / pa.sys_scale;  // exact (powers of two)
+  pa.res_inv = 1.0 / pa.res_scale;
 }
 
 void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt_kin_config* k,
@@ -881,6 +900,7 @@ int create_ctx(int device, const wt_model_desc* d, const wt_intrinsics* intr, in
     c->device = device;
     WT_CUDA(cudaSetDevice(device));
     WT_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    WT_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
     c->L = d->n_links;
     c->V = d->n_vertices;
     c->T = d->n_triangles;

@@ -91,7 +91,7 @@ struct DevState {
   int* row_cnt;       // [H] bucketed vertices per image row (cleared by k_scatter)
   int* poff;          // [P+1] row-major pixel offsets: the VertexBuckets CSR
   double4* items;     // bucketed vertices in pixel order (x,y,z, bits: vertex index)
-  unsigned long long* acc;   // [V*4] fixed-point sum x,y,z + count
+  unsigned long long* acc;   // [V*4] fixed-point sums x,y,z + count (one 256-bit record)
   unsigned long long* red;   // reduction slots (self-cleaning)
   unsigned* tickets;         // last-CTA tickets (self-cleaning)
   KinStat* kin_stats;
@@ -196,8 +196,8 @@ __device__ __forceinline__ void st256(ulonglong4* p, ulonglong4 v) {
 // association last (the pose system before the next re-association, the
 // shape step, the stats pass) zeroes the sums it read, so k_normals need not
 // clear all V of them before every search.
-__device__ __forceinline__ void clear_acc(unsigned long long* acc, int i) {
-  st256(reinterpret_cast<ulonglong4*>(acc) + i, make_ulonglong4(0ull, 0ull, 0ull, 0ull));
+__device__ __forceinline__ void clear_obs(const DevState& s, int i) {
+  st256(reinterpret_cast<ulonglong4*>(s.acc) + i, make_ulonglong4(0ull, 0ull, 0ull, 0ull));
 }
 
 // ---------------------------------------------------------------------------
@@ -239,14 +239,17 @@ __device__ __forceinline__ void red_add(unsigned long long* p, long long v) {
   atomicAdd(p, static_cast<unsigned long long>(v));
 }
 
-__device__ __forceinline__ double unfix(unsigned long long v, double scale) {
-  return static_cast<double>(static_cast<long long>(v)) / scale;
+// inv_scale = 1 / scale, exact: every fixed-point scale is a power of two
+// (a multiplication instead of an fp64 division per value)
+__device__ __forceinline__ double unfix(unsigned long long v, double inv_scale) {
+  return static_cast<double>(static_cast<long long>(v)) * inv_scale;
 }
 
 // Scale of the frame's observation sums (see kObsExpBudget) from the largest
 // coordinate magnitude k_ingest recorded in frame words [2..3]: 2^e with
 // e = min(44, 51 - ex), max_abs < 2^ex, built from the exponent bits.
-__host__ __device__ inline double obs_scale_of_bits(long long bits) {
+// (inverse = true: 2^-e, for unfix)
+__host__ __device__ inline double obs_scale_of_bits(long long bits, bool inverse = false) {
   const int biased = static_cast<int>((bits >> 52) & 0x7FF);
   const int ex = biased == 0 ? 0 : biased - 1022;  // frexp's exponent (0 for zero / subnormal)
   const int e = kObsExpBudget - ex < kObsExpMax ? kObsExpBudget - ex : kObsExpMax;
@@ -254,12 +257,12 @@ __host__ __device__ inline double obs_scale_of_bits(long long bits) {
     long long i;
     double d;
   } u;
-  u.i = static_cast<long long>(e + 1023) << 52;
+  u.i = static_cast<long long>((inverse ? -e : e) + 1023) << 52;
   return u.d;
 }
 
-__device__ __forceinline__ double obs_scale(const int* fwords) {
-  return obs_scale_of_bits(__ldcg(reinterpret_cast<const long long*>(fwords + 2)));
+__device__ __forceinline__ double obs_scale(const int* fwords, bool inverse = false) {
+  return obs_scale_of_bits(__ldcg(reinterpret_cast<const long long*>(fwords + 2)), inverse);
 }
 
 // Returns true in every thread of the CTA that finished last (grid-wide),
@@ -734,7 +737,7 @@ static __global__ void __launch_bounds__(kVThreads, B ? 3 : 2) k_normals(DevMode
       nz = n.z;
       valid = n.w != 0.0f;
     }
-    if (zero_acc) clear_acc(s.acc, i);
+    if (zero_acc) clear_obs(s, i);
     if (do_bucket) {
       // bucket_occupancy (association.cpp:39-56): per-pixel and per-row
       // counts as fire-and-forget reductions (no value comes back, so no
@@ -894,15 +897,15 @@ __device__ __forceinline__ void scan_span(const DevState& s, int e0, int e1, dou
                                           double cut2, double& best_x, int& best_i, int step = 1) {
   const long long ck = d2_key(cut2);
   long long bk = best_i < 0 ? LLONG_MAX : d2_key(best_x);
-  for (int e = e0; e < e1; e += step) {
-    const double4 it = ld256(s.items + e);
+  auto consider = [&](const double4& it) {
     const long long xk = d2_key(exact_d2(it, px, py, pz));
     const int vi = static_cast<int>(__double_as_longlong(it.w));
     if (xk <= ck && (xk < bk || (xk == bk && vi < best_i))) {
       bk = xk;
       best_i = vi;
     }
-  }
+  };
+  for (int e = e0; e < e1; e += step) consider(ld256(s.items + e));
   if (best_i >= 0) best_x = __longlong_as_double(bk);
 }
 
@@ -944,25 +947,53 @@ __device__ __forceinline__ void search_emit(const DevState& s, const SearchArgs&
 #ifndef WT_SEARCH_SOLO_SPL
 #define WT_SEARCH_SOLO_SPL 3
 #endif
+#ifndef WT_SEARCH_BATCH_G
+#define WT_SEARCH_BATCH_G 4
+#endif
+#ifndef WT_SEARCH_BATCH_SPL
+#define WT_SEARCH_BATCH_SPL 1
+#endif
 constexpr int kNearRingsSolo = 2, kSearchGroupSolo = WT_SEARCH_SOLO_G, kSearchSplitSolo = WT_SEARCH_SOLO_SPL;
-constexpr int kNearRingsBatch = 1, kSearchGroupBatch = 4, kSearchSplitBatch = 1;
+constexpr int kNearRingsBatch = 1, kSearchGroupBatch = WT_SEARCH_BATCH_G, kSearchSplitBatch = WT_SEARCH_BATCH_SPL;
 
+// Lexicographic (d^2, index) minimum over the G lanes of a group (lanes
+// [g*G, g*G + G) of the warp); every lane of the group ends with it. A
+// butterfly for power-of-two G, a fold over the group's lanes otherwise (the
+// minimum does not depend on the order).
 template <int G>
 __device__ __forceinline__ void group_min(double& bx, int& bi) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) {
-    const double ox = __shfl_xor_sync(0xffffffffu, bx, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+  auto take = [&](double ox, int oi) {
     if (oi >= 0 && (bi < 0 || ox < bx || (ox == bx && oi < bi))) {
       bx = ox;
       bi = oi;
     }
+  };
+  if constexpr ((G & (G - 1)) == 0) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) take(__shfl_xor_sync(0xffffffffu, bx, o), __shfl_xor_sync(0xffffffffu, bi, o));
+  } else {
+    const int lane = threadIdx.x & 31, base = lane - lane % G;
+    const double x0 = bx;
+    const int i0 = bi;
+    bx = INFINITY;
+    bi = -1;
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      const int src = min(base + t, 31);
+      const double ox = __shfl_sync(0xffffffffu, x0, src);
+      const int oi = __shfl_sync(0xffffffffu, i0, src);
+      if (base + t < 32) take(ox, oi);
+    }
   }
 }
 
+#ifndef WT_SEARCH_MINB_BATCH
+#define WT_SEARCH_MINB_BATCH 5  // resident CTAs per SM the batch search is compiled for
+#endif
 template <bool B, int NR = B ? kNearRingsBatch : kNearRingsSolo, int G = B ? kSearchGroupBatch : kSearchGroupSolo,
           int SPL = B ? kSearchSplitBatch : kSearchSplitSolo>
-static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFrame f, SearchArgs a) {
+static __global__ void __launch_bounds__(kVThreads, B ? WT_SEARCH_MINB_BATCH : 4) k_search(DevState s, DevFrame f,
+                                                                                        SearchArgs a) {
   pdl_entry();
   if constexpr (B) s = seq_state(s);
   if constexpr (B) f = seq_frame(f);
@@ -972,13 +1003,13 @@ static __global__ void __launch_bounds__(kVThreads) k_search(DevState s, DevFram
   const int w = a.window;
   const int K1 = min(NR, w);
   const double ifx = 1.0 / a.fx, ify = 1.0 / a.fy;
-  const int lane = threadIdx.x & 31, sub = lane & (G - 1);
-  constexpr int PPW = 32 / G;  // pixels per warp
+  const int lane = threadIdx.x & 31, sub = lane % G;
+  constexpr int PPW = 32 / G;  // pixels per warp (lanes from PPW * G on idle)
   const int TW = gridDim.x * (blockDim.x >> 5);
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   for (int base = gw * PPW; base < nv; base += TW * PPW) {
     const int j = base + lane / G;
-    const int pix = j < nv ? f.vlist[j] : -1;
+    const int pix = (lane < PPW * G && j < nv) ? f.vlist[j] : -1;
     const bool act = pix >= 0;
     const int pu = pix % a.W, pv = pix / a.W;
     double px = 0, py = 0, pz = 0;
@@ -1054,15 +1085,14 @@ __device__ __forceinline__ ulonglong4 load_obs(const unsigned long long* acc, in
   return ld256(reinterpret_cast<const ulonglong4*>(acc) + i);
 }
 
-__device__ __forceinline__ bool observed_mean(const ulonglong4& q, double oscale, double* pt, long long* cnt) {
+__device__ __forceinline__ bool observed_mean(const ulonglong4& q, double oinv, double* pt) {
   const ulonglong2 a01 = make_ulonglong2(q.x, q.y), a23 = make_ulonglong2(q.z, q.w);
   const long long c = static_cast<long long>(a23.y);
-  *cnt = c;
   if (c <= 0) return false;
   const double inv = 1.0 / static_cast<double>(c);
-  pt[0] = unfix(a01.x, oscale) * inv;
-  pt[1] = unfix(a01.y, oscale) * inv;
-  pt[2] = unfix(a23.x, oscale) * inv;
+  pt[0] = unfix(a01.x, oinv) * inv;
+  pt[1] = unfix(a01.y, oinv) * inv;
+  pt[2] = unfix(a23.x, oinv) * inv;
   return true;
 }
 
@@ -1137,7 +1167,7 @@ __device__ inline int block_ldlt_solve(int L, int lda, double* A, double* b, dou
 // pivot but stays a few hundred instructions, resident after the first pass.
 // The arithmetic (operands and order of every FMA) is unchanged.
 template <int N>
-__device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b, double* x) {
+__device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b, double* x, double (*scol)[32]) {
   const int lane = threadIdx.x & 31;
   const bool row = lane < L;
   double a[N];
@@ -1149,26 +1179,32 @@ __device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b
   double dinv = 1.0;
   int ok = 1;
   // Fully unrolled over the pivots: a[j] is this lane's entry of column j
-  // (static register indices, no shifting), and pivot k shuffles and updates
-  // only the trailing columns k+1..N-1 -- half the work of a rolled loop, the
-  // same operations on every entry that is read.
+  // (static register indices, no shifting), and pivot k updates only the
+  // trailing columns k+1..N-1. Column k of the current Schur complement
+  // (every lane's a[k]) and the right-hand side are published through
+  // shared memory -- one store per lane, then broadcast loads -- instead of
+  // one 64-bit shuffle per entry (two SHFLs each); the two column buffers
+  // alternate, so one warp barrier per pivot suffices. Same FMAs, same
+  // operands as a shuffle broadcast.
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    const double dk = __shfl_sync(0xffffffffu, a[k], k);
+    double* col = scol[2 * (k & 1)];
+    double* rhs = scol[2 * (k & 1) + 1];
+    col[lane] = a[k];
+    rhs[lane] = bi;
+    __syncwarp();
+    const double dk = col[k];
     ok &= dk > 0.0 ? 1 : 0;  // uniform; padded pivots are 1
     const double inv = __drcp_rn(dk);
-    const double zk = __shfl_sync(0xffffffffu, bi, k);
+    const double zk = rhs[k];
     const bool act = lane > k;
     const double lik = a[k] * inv;
     if (lane == k) dinv = inv;
     // Unpredicated: entries with t > lane (or lane <= k) are upper-triangle
     // values no later pivot reads, so updating them is harmless; every entry
     // that is read gets exactly the FMA the predicated form did.
-    double cj[N];
 #pragma unroll
-    for (int t = k + 1; t < N; ++t) cj[t] = __shfl_sync(0xffffffffu, a[k], t);  // A[t][k], unscaled
-#pragma unroll
-    for (int t = k + 1; t < N; ++t) a[t] = __fma_rn(-lik, cj[t], a[t]);  // explicit FMA (exact unit)
+    for (int t = k + 1; t < N; ++t) a[t] = __fma_rn(-lik, col[t], a[t]);  // A[t][k], unscaled
     if (act) {
       bi = __fma_rn(-lik, zk, bi);
       if (row) A[lane * lda + k] = lik;
@@ -1203,8 +1239,8 @@ struct PoseArgs {
   const int* count_in;   // optional association override (stage hook)
   const double* res_in;
   long long* dbg;        // optional timing record of the last CTA (WT_DEBUG_POSE)
-  double sys_scale;      // fixed-point scale of JtJ / Jtr (pose_scales, wt_gpu.cu)
-  double res_scale;      // ... of sum r^2
+  double sys_scale, sys_inv;  // fixed-point scale of JtJ / Jtr (pose_scales, wt_gpu.cu) and its inverse
+  double res_scale, res_inv;  // ... of sum r^2
 };
 
 // Shared-memory layout of k_pose_system for L links, NP dchain pairs and
@@ -1337,7 +1373,7 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
   }
   __syncwarp();
   long long rsq = 0, nassoc = 0;  // sum r^2 (fixed point at a.res_scale), associated count
-  const double oscale = a.count_in ? 1.0 : obs_scale(s.fwords);
+  const double oinv = a.count_in ? 1.0 : obs_scale(s.fwords, true);
   double* wrows = rows + warp * 32 * Lr;
   const int TW = gridDim.x * nw, gw = blockIdx.x * nw + warp;
   int* wq = qidx + warp * 64;       // warp-private queue of associated vertices
@@ -1363,10 +1399,10 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
           const long long c = static_cast<long long>(a23.y);
           have = c > 0;
           if (have) {
-            if (a.clean_acc) clear_acc(s.acc, i);
+            if (a.clean_acc) clear_obs(s, i);
             const double inv = 1.0 / static_cast<double>(c);
-            const double px = unfix(a01.x, oscale) * inv, py = unfix(a01.y, oscale) * inv,
-                         pz = unfix(a23.x, oscale) * inv;
+            const double px = unfix(a01.x, oinv) * inv, py = unfix(a01.y, oinv) * inv,
+                         pz = unfix(a23.x, oinv) * inv;
             r = static_cast<double>(n.x) * (px - v.x) + static_cast<double>(n.y) * (py - v.y) +
                 static_cast<double>(n.z) * (pz - v.z);
           }
@@ -1604,7 +1640,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
         s.red[c * (NE + 2) + NE] = 0ull;
         s.red[c * (NE + 2) + NE + 1] = 0ull;
       }
-      s_rsum = unfix(rs, a.res_scale);
+      s_rsum = unfix(rs, a.res_inv);
       s_nassoc = static_cast<long long>(na);
       s_finite = 1;
       wrapped |= static_cast<long long>(rs) < 0 ? 1 : 0;
@@ -1620,7 +1656,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
     ea[e] = static_cast<unsigned short>(ca);
     eb[e] = static_cast<unsigned short>(cb == L ? 0xFFFF : cb);
     if (ca == cb && static_cast<long long>(sum[q]) < 0) wrapped = 1;
-    const double val = unfix(sum[q], a.sys_scale);
+    const double val = unfix(sum[q], a.sys_inv);
     if (cb == L) {
       jtr[ca] = val;
     } else {
@@ -1639,7 +1675,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
     ea[e] = static_cast<unsigned short>(ca);
     eb[e] = static_cast<unsigned short>(cb == L ? 0xFFFF : cb);
     if (ca == cb && static_cast<long long>(t) < 0) wrapped = 1;
-    const double val = unfix(t, a.sys_scale);
+    const double val = unfix(t, a.sys_inv);
     if (cb == L) {
       jtr[ca] = val;
     } else {
@@ -1669,15 +1705,19 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
     if (!isfinite(jtr[k])) s_finite = 0;
   __syncthreads();
   const long long t3 = clock64();
-  if (L <= 32) {
+#ifndef WT_POSE_BLOCK_SOLVE
+#define WT_POSE_BLOCK_SOLVE 0
+#endif
+  if (L <= 32 && !WT_POSE_BLOCK_SOLVE) {
     if (warp == 0) {
       int ok = 0;
       if (s_finite) {
-        if (L <= 8) ok = warp_ldlt_solve<8>(L, Lp, A, jtr, s_x);
-        else if (L <= 16) ok = warp_ldlt_solve<16>(L, Lp, A, jtr, s_x);
-        else if (L <= 20) ok = warp_ldlt_solve<20>(L, Lp, A, jtr, s_x);
-        else if (L <= 24) ok = warp_ldlt_solve<24>(L, Lp, A, jtr, s_x);
-        else ok = warp_ldlt_solve<32>(L, Lp, A, jtr, s_x);
+        __shared__ double scol[4][32];
+        if (L <= 8) ok = warp_ldlt_solve<8>(L, Lp, A, jtr, s_x, scol);
+        else if (L <= 16) ok = warp_ldlt_solve<16>(L, Lp, A, jtr, s_x, scol);
+        else if (L <= 20) ok = warp_ldlt_solve<20>(L, Lp, A, jtr, s_x, scol);
+        else if (L <= 24) ok = warp_ldlt_solve<24>(L, Lp, A, jtr, s_x, scol);
+        else ok = warp_ldlt_solve<32>(L, Lp, A, jtr, s_x, scol);
       }
       // theta -= x (kinopt.cpp:161-165), optional clamp, iteration stats
       double xk = 0.0;
@@ -1856,7 +1896,7 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
   __syncthreads();
   double abs_r = 0.0, sum_phi = 0.0, max_phi = 0.0;
   long long observed = 0, singular = 0;
-  const double oscale = obs_scale(s.fwords);
+  const double oinv = obs_scale(s.fwords, true);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
     // every load of the vertex up front (the 256-bit loads keep program order)
     const double4 f = ld256(phi_in + i);
@@ -1896,9 +1936,8 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
     double g[3] = {0.0, 0.0, 0.0};
     double r = 0.0;
     double pt[3];
-    long long cnt = 0;
-    if (observed_mean(obs, oscale, pt, &cnt)) {
-      if (a.clean_acc) clear_acc(s.acc, i);
+    if (observed_mean(obs, oinv, pt)) {
+      if (a.clean_acc) clear_obs(s, i);
       const double4 v = ld256(s.pv + i);
       const float4 n = s.pn[i];
       const double ro = static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
@@ -1969,12 +2008,11 @@ static __global__ void __launch_bounds__(kVThreads, 5) k_shape_after(DevModel m,
   if constexpr (B) s = seq_state(s);
   double abs_r = 0.0;
   long long observed = 0;
-  const double oscale = obs_scale(s.fwords);
+  const double oinv = obs_scale(s.fwords, true);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
     double pt[3];
-    long long cnt = 0;
-    if (observed_mean(load_obs(s.acc, i), oscale, pt, &cnt)) {
-      if (clean_acc) clear_acc(s.acc, i);
+    if (observed_mean(load_obs(s.acc, i), oinv, pt)) {
+      if (clean_acc) clear_obs(s, i);
       const double4 v = ld256(s.pv + i);
       const float4 n = s.pn[i];
       abs_r += fabs(static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +

@@ -12,6 +12,7 @@ using namespace wt;
 template <int N>
 __global__ void k_ldlt(int L, long long* cyc, double* out) {
   __shared__ double A[32 * 33], b[32], x[32];
+  __shared__ double scol[4][32];
   const int lane = threadIdx.x;
   for (int r = 0; r < 4; ++r) {
     for (int i = 0; i < L; ++i) A[i * (L + 1) + lane % (L + 1)] = 0.0;
@@ -22,7 +23,7 @@ __global__ void k_ldlt(int L, long long* cyc, double* out) {
     }
     __syncwarp();
     const long long t0 = clock64();
-    const int ok = warp_ldlt_solve<N>(L, L + 1, A, b, x);
+    const int ok = warp_ldlt_solve<N>(L, L + 1, A, b, x, scol);
     __syncwarp();
     const long long t1 = clock64();
     if (lane == 0) cyc[r] = t1 - t0;
@@ -41,6 +42,48 @@ void run(int L) {
     k_ldlt<N><<<1, 32>>>(L, dc, dout);
     cudaMemcpy(c, dc, sizeof(c), cudaMemcpyDeviceToHost);
     printf("N=%d L=%d launch %d: cycles %lld %lld %lld %lld\n", N, L, rep, c[0], c[1], c[2], c[3]);
+  }
+  cudaFree(dc);
+  cudaFree(dout);
+}
+
+// block_ldlt_solve (the CTA-wide form): 256 threads, one barrier per pivot
+__global__ void k_bldlt(int L, long long* cyc, double* out) {
+  __shared__ double A[32 * 33], b[32], x[32];
+  __shared__ unsigned short ea[600], eb[600];
+  const int NT = L * (L + 1) / 2;
+  for (int e = threadIdx.x; e < NT; e += blockDim.x) {
+    int r = 0, rem = e;
+    while (rem >= L - r) { rem -= L - r; ++r; }
+    ea[e] = r;
+    eb[e] = r + rem;
+  }
+  for (int r = 0; r < 4; ++r) {
+    for (int e = threadIdx.x; e < L * (L + 1); e += blockDim.x) {
+      const int i = e / (L + 1), j = e % (L + 1);
+      A[e] = j < L ? 1.0 / (1.0 + i + j) + (i == j ? L : 0.0) : 0.0;
+    }
+    if (threadIdx.x < L) b[threadIdx.x] = 1.0 + threadIdx.x;
+    __syncthreads();
+    const long long t0 = clock64();
+    const int ok = block_ldlt_solve(L, L + 1, A, b, x, ea, eb, NT);
+    __syncthreads();
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[r] = t1 - t0;
+    if (ok && threadIdx.x < L) out[threadIdx.x] = x[threadIdx.x];
+  }
+}
+
+void run_block(int L) {
+  long long* dc;
+  double* dout;
+  cudaMalloc(&dc, sizeof(long long) * 4);
+  cudaMalloc(&dout, sizeof(double) * 32);
+  long long c[4];
+  for (int rep = 0; rep < 2; ++rep) {
+    k_bldlt<<<1, 256>>>(L, dc, dout);
+    cudaMemcpy(c, dc, sizeof(c), cudaMemcpyDeviceToHost);
+    printf("block L=%d launch %d: cycles %lld %lld %lld %lld\n", L, rep, c[0], c[1], c[2], c[3]);
   }
   cudaFree(dc);
   cudaFree(dout);
@@ -83,6 +126,8 @@ int main() {
   run<8>(6);
   run<20>(20);
   run<32>(27);
+  run_block(20);
+  run_block(27);
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }

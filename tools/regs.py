@@ -2,6 +2,7 @@
 
     python tools/regs.py [repo_root] [unit.cu ...]
 """
+import os
 import re
 import subprocess
 import sys
@@ -12,7 +13,7 @@ units = sys.argv[2:] or ["wt_gpu.cu", "wt_exact.cu"]
 for u in units:
     cmd = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
            "-I", str(root / "include"), "-I", str(root / "paper_1711_07999_b200/csrc"), "--expt-relaxed-constexpr",
-           "-Xptxas", "-v", "-c", str(root / "paper_1711_07999_b200/csrc" / u), "-o", "/dev/null"]
+           *os.environ.get("WT_NVCC_FLAGS", "").split(), "-Xptxas", "-v", "-c", str(root / "paper_1711_07999_b200/csrc" / u), "-o", "/dev/null"]
     if u != "wt_gpu.cu":
         cmd.insert(-4, "-fmad=false")
     out = subprocess.run(cmd, capture_output=True, text=True).stderr
