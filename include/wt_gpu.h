@@ -239,6 +239,35 @@ int wt_gpu_optimize_shape(wt_gpu_ctx* ctx, const wt_shape_config* shape,
                           const wt_assoc_config* assoc, int32_t with_stats_pass,
                           wt_shape_iter_stats* stats, int32_t cap, int32_t* n_out);
 
+/* ---- model preprocessing on the device ----------------------------------------- */
+/* subdivide(mesh, iterations) (skinmesh.cpp:490-511: Catmull-Clark of
+ * positions, phi and skin weights by catmull_clark_once :298-470, then
+ * truncate_weights :265-280), SkinnedMesh::finalize() (skinmesh.cpp:13-58:
+ * triangles + vertex->triangle CSR) and, for k_neighbors > 0,
+ * build_neighbors(v0, k) (skinmesh.cpp:196-247) -- all on the device, bitwise
+ * the reference's. iterations == 0 only finalizes (weights kept as given).
+ * Inputs: template vertices, phi (NULL: zeros), weight rows as in
+ * wt_model_desc, polygons as CSR. The result is read with wt_gpu_mesh_sizes /
+ * wt_gpu_mesh_export (any output pointer may be NULL) and released with
+ * wt_gpu_mesh_free. Errors: WT_EINVAL (bad input; an edge with more than two
+ * faces, the reference's NonManifold), WT_ENODEV, WT_ECUDA / WT_ENOMEM; the
+ * message is wt_gpu_mesh_last_error(). */
+typedef struct wt_mesh wt_mesh;
+int wt_gpu_mesh_subdivide(int device, int32_t n_vertices, int32_t n_links, const double* v0, const double* phi,
+                          const int32_t* weight_count, const int32_t* weight_link, const double* weight,
+                          int32_t n_polys, const int32_t* poly_offsets, const int32_t* poly_items,
+                          int32_t iterations, int32_t k_neighbors, wt_mesh** out);
+int wt_gpu_mesh_sizes(const wt_mesh* mesh, int32_t* n_vertices, int32_t* n_polys, int32_t* n_poly_items,
+                      int32_t* n_triangles, int32_t* n_neighbors_per_vertex);
+int wt_gpu_mesh_export(const wt_mesh* mesh, double* v0, double* phi, int32_t* weight_count, int32_t* weight_link,
+                       double* weight, int32_t* poly_offsets, int32_t* poly_items, int32_t* triangles,
+                       int32_t* vtri_offsets, int32_t* vtri_items, int32_t* neighbors);
+void wt_gpu_mesh_free(wt_mesh* mesh);
+const char* wt_gpu_mesh_last_error(void);
+/* build_neighbors(v0, k) alone (skinmesh.cpp:196-247): out[n][min(k, n-1)],
+ * each row ascending by (squared distance, index); k <= 16. */
+int wt_gpu_build_neighbors(int device, int32_t n, const double* v0, int32_t k, int32_t* out);
+
 /* ---- page-locked host staging ----------------------------------------------- */
 /* Page-locked host memory (cudaMallocHost) for callers that do not link the
  * CUDA runtime (the reference-side adapter): a depth frame staged there takes

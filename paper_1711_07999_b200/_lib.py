@@ -90,7 +90,8 @@ EXPORTS = [
     "wt_gpu_track_frame_cloud", "wt_gpu_optimize_pose", "wt_gpu_optimize_shape", "wt_gpu_skin",
     "wt_gpu_associate", "wt_gpu_associate_posed", "wt_gpu_normal_system", "wt_gpu_solve_step",
     "wt_gpu_solve_vertices", "wt_gpu_render_depth", "wt_gpu_stream", "wt_gpu_track_async", "wt_gpu_sync",
-    "wt_gpu_profile_frame", "wt_gpu_bucket_count", "wt_gpu_host_alloc", "wt_gpu_host_free", "wt_gpu_track_sequence", "wt_gpu_joint_positions", "wt_gpu_recon_error",
+    "wt_gpu_profile_frame", "wt_gpu_bucket_count", "wt_gpu_mesh_subdivide", "wt_gpu_mesh_sizes",
+    "wt_gpu_mesh_export", "wt_gpu_mesh_free", "wt_gpu_mesh_last_error", "wt_gpu_build_neighbors", "wt_gpu_host_alloc", "wt_gpu_host_free", "wt_gpu_track_sequence", "wt_gpu_joint_positions", "wt_gpu_recon_error",
     "wt_gpu_create_batch", "wt_gpu_batch_size", "wt_gpu_batch_set_state", "wt_gpu_batch_get_state",
     "wt_gpu_batch_load_depth", "wt_gpu_batch_track_async", "wt_gpu_batch_stats", "wt_gpu_batch_track",
 ]
@@ -170,6 +171,14 @@ def _declare(L: C.CDLL) -> None:
     L.wt_gpu_joint_positions.argtypes = [vp, vp]
     L.wt_gpu_recon_error.argtypes = [vp, vp, P(C.c_int32)]
     L.wt_gpu_bucket_count.argtypes = [vp, C.c_int32, P(C.c_int32)]
+    L.wt_gpu_mesh_subdivide.argtypes = [C.c_int, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, C.c_int32, vp, vp,
+                                        C.c_int32, C.c_int32, P(vp)]
+    L.wt_gpu_mesh_sizes.argtypes = [vp, P(C.c_int32), P(C.c_int32), P(C.c_int32), P(C.c_int32), P(C.c_int32)]
+    L.wt_gpu_mesh_export.argtypes = [vp] + [vp] * 11
+    L.wt_gpu_mesh_free.argtypes = [vp]
+    L.wt_gpu_mesh_free.restype = None
+    L.wt_gpu_mesh_last_error.restype = C.c_char_p
+    L.wt_gpu_build_neighbors.argtypes = [C.c_int, C.c_int32, vp, C.c_int32, vp]
     L.wt_gpu_host_alloc.argtypes = [C.c_size_t, P(vp)]
     L.wt_gpu_host_free.argtypes = [vp]
     L.wt_gpu_host_free.restype = None

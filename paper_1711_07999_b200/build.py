@@ -27,6 +27,7 @@ UNITS = [
     ("wt_gpu.cu", []),
     ("wt_exact.cu", ["-fmad=false"]),
     ("wt_render.cu", ["-fmad=false"]),
+    ("wt_model.cu", ["-fmad=false"]),
 ]
 
 

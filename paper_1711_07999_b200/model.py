@@ -388,13 +388,14 @@ def _humanoid_at(h: float, depth: float) -> ModelBundle:
 
 
 def make_humanoid(target_vertices: int = 100_000, depth: float = 2.2, neighbors: int = 4,
-                  levels: int | None = None) -> ModelBundle:
+                  levels: int | None = None, device: int | None = None) -> ModelBundle:
     """20-link humanoid (one prismatic root, hinges about x/y/z axes): a coarse
     capsule rig refined by `levels` Catmull-Clark subdivisions (the reference
     tracks subdivided templates, acceptance.cpp:543-548), with the coarse
     spacing solved so the result has ~target_vertices (within ~3%). Placed
     `depth` metres in front of the camera, head up in the image, 3 cm off the
-    optical axis. Finalized, with k-NN neighbour sets."""
+    optical axis. Finalized, with k-NN neighbour sets. With a device the
+    subdivision, finalize and neighbour search run on that GPU (same bits)."""
     if levels is None:
         levels = 1 if target_vertices < 20_000 else (2 if target_vertices <= 200_000 else 3)
     base_target = target_vertices / (4.0 ** levels)
@@ -410,6 +411,8 @@ def make_humanoid(target_vertices: int = 100_000, depth: float = 2.2, neighbors:
         else:
             hi = mid
     b = _humanoid_at(best[0], depth)
+    if device is not None:
+        return subdivide_on_device(b, levels, neighbors, device)
     b.finalize()
     return subdivide(b, levels, neighbors) if levels > 0 else b.with_neighbors(neighbors)
 
@@ -594,9 +597,75 @@ def _truncate_weights(W: np.ndarray):
     return cnt, links, wts
 
 
+def _mesh_check(rc: int) -> None:
+    if rc != _lib.WT_OK:
+        msg = (_lib.lib().wt_gpu_mesh_last_error() or b"").decode(errors="replace")
+        cls = {_lib.WT_EINVAL: _lib.ValidationError, _lib.WT_ELENGTH: _lib.LengthMismatch}.get(rc, _lib.WarptrackError)
+        raise cls(rc, msg)
+
+
+def subdivide_on_device(b: ModelBundle, iterations: int, neighbors: int = 4, device: int = 0) -> ModelBundle:
+    """subdivide + finalize + build_neighbors on the GPU (wt_gpu_mesh_subdivide,
+    wt_model.cu): bitwise the reference's (skinmesh.cpp:13-58,145-511) and the
+    host path below. iterations == 0 only finalizes and builds neighbours."""
+    import ctypes as C
+    L = _lib.lib()
+    V = b.vertex_count
+    sizes = [len(p) for p in b.polys]
+    poff = np.zeros(len(sizes) + 1, np.int32)
+    poff[1:] = np.cumsum(sizes)
+    pitems = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in b.polys])
+                                  if b.polys else np.zeros(0, np.int32), np.int32)
+    v0 = np.ascontiguousarray(b.v0, np.float64)
+    phi = None if b.phi is None or b.phi.shape != b.v0.shape else np.ascontiguousarray(b.phi, np.float64)
+    wc = np.ascontiguousarray(b.weight_count, np.int32)
+    wl = np.ascontiguousarray(b.weight_link, np.int32)
+    ww = np.ascontiguousarray(b.weight, np.float64)
+    h = C.c_void_p()
+    _mesh_check(L.wt_gpu_mesh_subdivide(device, V, b.link_count, _lib.ptr(v0), _lib.ptr(phi), _lib.ptr(wc),
+                                        _lib.ptr(wl), _lib.ptr(ww), len(sizes), _lib.ptr(poff), _lib.ptr(pitems),
+                                        iterations, neighbors, C.byref(h)))
+    try:
+        n = [C.c_int32() for _ in range(5)]
+        _mesh_check(L.wt_gpu_mesh_sizes(h, *[C.byref(x) for x in n]))
+        nv, nf, ni, nt, k = (x.value for x in n)
+        o = dict(v0=np.zeros((nv, 3)), phi=np.zeros((nv, 3)), weight_count=np.zeros(nv, np.int32),
+                 weight_link=np.zeros((nv, 4), np.int32), weight=np.zeros((nv, 4)),
+                 poff=np.zeros(nf + 1, np.int32), pitems=np.zeros(ni, np.int32), triangles=np.zeros((nt, 3), np.int32),
+                 vtri_offsets=np.zeros(nv + 1, np.int32), vtri_items=np.zeros(3 * nt, np.int32),
+                 nbr=np.zeros((nv, k), np.int32))
+        _mesh_check(L.wt_gpu_mesh_export(h, *[_lib.ptr(o[x]) for x in (
+            "v0", "phi", "weight_count", "weight_link", "weight", "poff", "pitems", "triangles", "vtri_offsets",
+            "vtri_items", "nbr")]))
+    finally:
+        L.wt_gpu_mesh_free(h)
+    polys = np.split(o["pitems"], o["poff"][1:-1]) if nf else []
+    out = replace(b, v0=o["v0"], phi=o["phi"], weight_count=o["weight_count"], weight_link=o["weight_link"],
+                  weight=o["weight"], polys=[p.tolist() for p in polys], triangles=o["triangles"],
+                  vtri_offsets=o["vtri_offsets"], vtri_items=o["vtri_items"])
+    if neighbors > 0:
+        out.nbr_offsets = np.arange(nv + 1, dtype=np.int32) * k
+        out.nbr_items = o["nbr"].reshape(-1)
+    else:
+        out.nbr_offsets, out.nbr_items = None, None
+    return out
+
+
+def build_neighbors_on_device(v0: np.ndarray, k: int, device: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """build_neighbors (skinmesh.cpp:196-247) on the GPU (wt_gpu_build_neighbors):
+    CSR (offsets, items) as build_neighbors below."""
+    nv = v0.shape[0]
+    want = max(0, min(k, nv - 1))
+    out = np.zeros((nv, want), np.int32)
+    _mesh_check(_lib.lib().wt_gpu_build_neighbors(device, nv, _lib.ptr(np.ascontiguousarray(v0, np.float64)), k,
+                                                  _lib.ptr(out)))
+    return np.arange(nv + 1, dtype=np.int32) * want, out.reshape(-1)
+
+
 def subdivide(b: ModelBundle, iterations: int, neighbors: int = 4) -> ModelBundle:
     """subdivide (skinmesh.cpp:490-511) + build_neighbors(v0, 4), as the
-    reference's Python binding subdivide_model does (bindings.cpp:154-161)."""
+    reference's Python binding subdivide_model does (bindings.cpp:154-161).
+    Host restatement (numpy); subdivide_on_device is the GPU path."""
     L = b.link_count
     W = np.zeros((b.vertex_count, L))
     for s in range(4):
