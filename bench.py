@@ -181,11 +181,14 @@ class ClockSampler:
 SUBJECT_DEPTH = 1.6
 
 
-def make_workload(cfg_name: str):
+def make_workload(cfg_name: str, device: int | None = None):
+    """The config's model, intrinsics and TrackConfig. With a device the model
+    is subdivided / finalized / k-NN'd on that GPU (subdivide_on_device, the
+    same bits as the host path the reference arm uses)."""
     from paper_1711_07999_b200.model import make_humanoid
     from paper_1711_07999_b200.tracker import AssocConfig, Intrinsics, KinSolverConfig, ShapeSolverConfig, TrackConfig
     W, H, nv, mode, kits, sits = CONFIGS[cfg_name]
-    bundle = make_humanoid(nv, depth=SUBJECT_DEPTH)
+    bundle = make_humanoid(nv, depth=SUBJECT_DEPTH, device=device)
     intr = Intrinsics.scaled(W, H)
     cfg = TrackConfig(mode=mode, kin=KinSolverConfig(iterations=kits), shape=ShapeSolverConfig(iterations=max(sits, 1)),
                       assoc=AssocConfig())
@@ -262,6 +265,34 @@ def parity_line(bundle, intr, cfg, frames_host, theta0, ref_thetas, device: int)
         trk.close()
     return {"max_abs_dtheta": worst, "frames": len(ref_thetas), "tolerance": 1e-6,
             "vs": "the cpu_baseline leg (the reference on the host) on the same frames from the same start"}
+
+
+def reference_api_e2e(bundle, intr, frames_host, steps: int):
+    """The reference's own C++ API on the GPU: oracle/_ref/adapter_bench (the
+    reference library with adapter/warptrack_gpu.cpp linked in, as
+    INTEGRATION.md integrates it) loads this model with the reference's
+    load_model and the frames with its SequenceReader, and times
+    warptrack::gpu::track_frame on the reference's CloudFrames and
+    warptrack::gpu::run_tracking over the .wts. None where not built."""
+    import tempfile
+    exe = ROOT / "oracle" / "_ref" / "adapter_bench"
+    from oracle import ref
+    if not exe.exists() or not ref.available():
+        return None
+    with tempfile.TemporaryDirectory() as td:
+        ref.RefModel.from_bundle(bundle).save(Path(td) / "model.json")
+        fr = np.stack([np.asarray(f) for f in frames_host])
+        ref.write_sequence(Path(td) / "seq.wts", intr.c(), fr)
+        warm = 3
+        n = min(steps, fr.shape[0] - warm - 1)
+        out = subprocess.run([str(exe), str(Path(td) / "model.json"), str(Path(td) / "seq.wts"), str(warm), str(n)],
+                             capture_output=True, text=True, timeout=600)
+    if out.returncode != 0:
+        return {"error": out.stderr.strip()[-300:]}
+    try:
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return {"error": out.stdout.strip()[-300:]}
 
 
 def workload_config(args, bundle, intr, cfg) -> dict:
@@ -358,7 +389,7 @@ def roofline_of(kernels, peak, peak_src, config):
     return roof, frame
 
 
-def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+def run_ours(args, rank: int, world: int, local_rank: int, emit: bool = True):
     import ctypes as C
 
     import torch
@@ -369,7 +400,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    bundle, intr, cfg = make_workload(args.config)
+    bundle, intr, cfg = make_workload(args.config, device=local_rank)
     S = args.sequences
     trackers = [Tracker(bundle, intr, trajectory(bundle, 0, rank * S + s), device=local_rank) for s in range(S)]
     L = W.lib()
@@ -526,7 +557,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if rank != 0:
         for t_ in trackers:
             t_.close()
-        return
+        return None
     roof, frame = roofline_of(kernels, peak, peak_src, args.config)
     kits, sits = CONFIGS[args.config][4], CONFIGS[args.config][5]
     line = {
@@ -575,9 +606,26 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                                                          trajectory(bundle, 0, 0))
         line["parity"] = parity_line(bundle, intr, cfg, cpu_frames, trajectory(bundle, 0, 0), ref_thetas,
                                      local_rank)
-    print(json.dumps(line), flush=True)
+        api = reference_api_e2e(bundle, intr, [f.numpy() for f in frames_host[0]], args.steps)
+        if api is not None:
+            line["e2e_reference_api"] = api
     for t_ in trackers:
         t_.close()
+    if world == 1 and args.config == "c3" and not args.no_batch:
+        # C4, the 1920x1080 / 409k-vertex stress configuration, one sequence
+        cargs = argparse.Namespace(**{**vars(args), "config": "c4", "sequences": 1, "steps": 10, "warmup": 3,
+                                      "no_batch": True, "no_cpu_baseline": True})
+        c4 = run_ours(cargs, rank, world, local_rank, emit=False)
+        line["c4"] = {k: c4[k] for k in ("value", "unit", "ms_per_step", "steps", "gn_iterations_per_s",
+                                         "workload_stats", "e2e", "roofline", "frame_roofline", "gpu_launches",
+                                         "clocks")}
+        line["c4"]["workload"] = c4["config"]["workload"]
+        line["c4"]["kernels"] = {k: {kk: v[kk] for kk in ("avg_us", "us_per_frame", "achieved_gbs", "frac",
+                                                          "dram_bytes_per_launch", "dram_frac")}
+                                 for k, v in c4["kernels"].items()}
+    if emit:
+        print(json.dumps(line), flush=True)
+    return line
 
 
 def run_batched(args, rank: int, world: int, local_rank: int, emit: bool = True):
@@ -593,7 +641,7 @@ def run_batched(args, rank: int, world: int, local_rank: int, emit: bool = True)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    bundle, intr, cfg = make_workload(args.config)
+    bundle, intr, cfg = make_workload(args.config, device=local_rank)
     S = args.sequences
     seqs = [rank * S + s for s in range(S)]
     th0 = np.stack([trajectory(bundle, 0, q) for q in seqs])

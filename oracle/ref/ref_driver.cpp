@@ -217,6 +217,12 @@ int wtref_subdivide(const wtref_model* in, int iterations, wtref_model** out) {
   });
 }
 
+// save_model (seqio.cpp:20-417): the bundle as JSON + .wtm sidecar, for tools
+// that load it back with the reference's own load_model.
+int wtref_save_model(const wtref_model* m, const char* path) {
+  return guarded([&] { save_model(path, m->bundle); });
+}
+
 // rigidify (tracker.cpp:24-43).
 int wtref_rigidify(const wtref_model* in, wtref_model** out) {
   return guarded([&] {
