@@ -267,11 +267,25 @@ def parity_line(bundle, intr, cfg, frames_host, theta0, ref_thetas, device: int)
             "vs": "the cpu_baseline leg (the reference on the host) on the same frames from the same start"}
 
 
+def write_desc(bundle, path) -> None:
+    """A raw wt_model_desc dump (tests/cpp/adapter_bench.cpp reads it)."""
+    L, V, T = bundle.link_count, bundle.vertex_count, bundle.triangle_count
+    with open(path, "wb") as f:
+        np.array([L, V, T, bundle.vtri_items.size, bundle.nbr_items.size], np.int32).tofile(f)
+        for a, dt in ((bundle.parent, np.int32), (bundle.parent_offset, np.float64), (bundle.joint_kind, np.int32),
+                      (bundle.joint_axis, np.float64), (bundle.theta_index, np.int32), (bundle.v0, np.float64),
+                      (bundle.phi if bundle.phi is not None else np.zeros_like(bundle.v0), np.float64),
+                      (bundle.weight_count, np.int32), (bundle.weight_link, np.int32), (bundle.weight, np.float64),
+                      (bundle.triangles, np.int32), (bundle.vtri_offsets, np.int32), (bundle.vtri_items, np.int32),
+                      (bundle.nbr_offsets, np.int32), (bundle.nbr_items, np.int32)):
+            np.ascontiguousarray(a, dt).tofile(f)
+
+
 def reference_api_e2e(bundle, intr, frames_host, steps: int):
-    """The reference's own C++ API on the GPU: oracle/_ref/adapter_bench (the
+    """The reference's own C++ API on the GPU: oracle/_ref/adapter_bench is the
     reference library with adapter/warptrack_gpu.cpp linked in, as
-    INTEGRATION.md integrates it) loads this model with the reference's
-    load_model and the frames with its SequenceReader, and times
+    INTEGRATION.md integrates it. It builds the reference ModelBundle of this
+    model, reads the frames with the reference's SequenceReader, and times
     warptrack::gpu::track_frame on the reference's CloudFrames and
     warptrack::gpu::run_tracking over the .wts. None where not built."""
     import tempfile
@@ -280,12 +294,12 @@ def reference_api_e2e(bundle, intr, frames_host, steps: int):
     if not exe.exists() or not ref.available():
         return None
     with tempfile.TemporaryDirectory() as td:
-        ref.RefModel.from_bundle(bundle).save(Path(td) / "model.json")
+        write_desc(bundle, Path(td) / "model.desc")
         fr = np.stack([np.asarray(f) for f in frames_host])
         ref.write_sequence(Path(td) / "seq.wts", intr.c(), fr)
         warm = 3
-        n = min(steps, fr.shape[0] - warm - 1)
-        out = subprocess.run([str(exe), str(Path(td) / "model.json"), str(Path(td) / "seq.wts"), str(warm), str(n)],
+        n = min(steps, fr.shape[0] - warm)
+        out = subprocess.run([str(exe), str(Path(td) / "model.desc"), str(Path(td) / "seq.wts"), str(warm), str(n)],
                              capture_output=True, text=True, timeout=600)
     if out.returncode != 0:
         return {"error": out.stderr.strip()[-300:]}
@@ -798,6 +812,8 @@ def _free_port() -> int:
 
 
 def main() -> None:
+    import faulthandler
+    faulthandler.enable()  # a crash in native code still names the Python frame
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)

@@ -85,10 +85,6 @@ class RefModel:
         _check(lib().wtref_subdivide(self.h, iterations, C.byref(h)))
         return RefModel(h)
 
-    def save(self, path) -> None:
-        """save_model (the reference's JSON + .wtm bundle files)."""
-        _check(lib().wtref_save_model(self.h, str(path).encode()))
-
     def rigidify(self) -> "RefModel":
         h = C.c_void_p()
         _check(lib().wtref_rigidify(self.h, C.byref(h)))

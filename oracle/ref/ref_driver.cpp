@@ -143,6 +143,9 @@ struct wtref_model {
   ModelBundle bundle;
 };
 
+// The bundle behind a handle (C++ tools linking this driver, e.g. adapter_bench).
+const warptrack::ModelBundle* wtref_bundle_of(const wtref_model* m) { return m ? &m->bundle : nullptr; }
+
 struct wtref_tracker {
   std::shared_ptr<wtref_model> model;
   TrackerState state;
@@ -215,12 +218,6 @@ int wtref_subdivide(const wtref_model* in, int iterations, wtref_model** out) {
     m->bundle.mesh.neighbors = build_neighbors(m->bundle.mesh.v0, 4);
     *out = m.release();
   });
-}
-
-// save_model (seqio.cpp:20-417): the bundle as JSON + .wtm sidecar, for tools
-// that load it back with the reference's own load_model.
-int wtref_save_model(const wtref_model* m, const char* path) {
-  return guarded([&] { save_model(path, m->bundle); });
 }
 
 // rigidify (tracker.cpp:24-43).
