@@ -235,8 +235,35 @@ __device__ __forceinline__ long long fix(double x, double scale) {
   return __double2ll_rn(x * scale);
 }
 
+// Global-memory atomics in explicit PTX. A batched kernel rebases its
+// pointers per sequence (seq_state), after which the compiler can no longer
+// prove they address global memory: atomicAdd then compiles to a generic
+// ATOM.E plus a shared-memory CAS fallback path, and a result-less add no
+// longer becomes the fire-and-forget RED. Every pointer passed here is global.
 __device__ __forceinline__ void red_add(unsigned long long* p, long long v) {
-  atomicAdd(p, static_cast<unsigned long long>(v));
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)),
+               "l"(static_cast<unsigned long long>(v))
+               : "memory");
+}
+
+__device__ __forceinline__ void red_add(int* p, int v) {
+  asm volatile("red.global.add.s32 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_max(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.global.max.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ int atom_add(int* p, int v) {
+  int old;
+  asm volatile("atom.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ unsigned atom_add(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
+  return old;
 }
 
 // inv_scale = 1 / scale, exact: every fixed-point scale is a power of two
@@ -272,7 +299,7 @@ __device__ __forceinline__ bool last_block(unsigned* ticket) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned t = atomicAdd(ticket, 1u);
+    const unsigned t = atom_add(ticket, 1u);
     is_last = (t == gridDim.x - 1);  // per sequence (blockIdx.y)
     if (is_last) *ticket = 0u;
   }
@@ -534,14 +561,14 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0 && mx > 0.0)
-      atomicMax(reinterpret_cast<unsigned long long*>(n_valid + 2), static_cast<unsigned long long>(__double_as_longlong(mx)));
+      red_max(reinterpret_cast<unsigned long long*>(n_valid + 2), static_cast<unsigned long long>(__double_as_longlong(mx)));
   }
   const unsigned m = __ballot_sync(0xffffffffu, valid);
   if (m) {
     // a run padded to a multiple of kRunAlign (the pixels of one search warp)
     const int n = __popc(m), padded = (n + kRunAlign - 1) & ~(kRunAlign - 1);
     int base = 0;
-    if (lane == 0) base = atomicAdd(n_valid, padded);
+    if (lane == 0) base = atom_add(n_valid, padded);
     base = __shfl_sync(0xffffffffu, base, 0);
     if (valid) vlist[base + __popc(m & ((1u << lane) - 1u))] = i;
     if (lane >= n && lane < padded) vlist[base + lane] = -1;
@@ -753,8 +780,8 @@ static __global__ void __launch_bounds__(kVThreads, B ? 3 : 2) k_normals(DevMode
         }
       }
       if (pix >= 0) {
-        atomicAdd(&s.pix_cnt[pix], 1);
-        atomicAdd(&s.row_cnt[row], 1);
+        red_add(&s.pix_cnt[pix], 1);
+        red_add(&s.row_cnt[row], 1);
       }
       s.vpix[i] = pix;
     }
@@ -834,7 +861,7 @@ __device__ __forceinline__ void scatter_vertex(const DevModel& m, const DevState
   // the bucket's slots are poff[pix] + (count - 1) .. poff[pix]: taken by
   // counting the bucket size back down, which leaves the counts at zero for
   // the next association (no cursor array, no clearing pass)
-  st256(s.items + __ldg(s.poff + pix) + atomicSub(&s.pix_cnt[pix], 1) - 1,
+  st256(s.items + __ldg(s.poff + pix) + atom_add(&s.pix_cnt[pix], -1) - 1,
         make_double4(v.x, v.y, v.z, __longlong_as_double(static_cast<long long>(i))));
 }
 
