@@ -277,12 +277,12 @@ int vgrid(int n) { return std::max(1, (n + wt::kVThreads - 1) / wt::kVThreads); 
 // SM from the occupancy calculator (registers and shared memory as compiled)
 // times the SM count.
 template <class K>
-int full_wave(wt_gpu_ctx* c, K kernel) {
+int full_wave(wt_gpu_ctx* c, K kernel, int threads = wt::kVThreads, size_t smem = 0) {
   const void* key = reinterpret_cast<const void*>(kernel);
   auto it = c->resident.find(key);
   if (it == c->resident.end()) {
     int n = 0;
-    WT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, wt::kVThreads, 0));
+    WT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem));
     it = c->resident.emplace(key, std::max(1, n)).first;
   }
   return it->second * c->sms;
@@ -559,9 +559,13 @@ void enq_associate(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* 
 // ~22 vertices per warp at C3 (one scan chunk each)
 int pose_threads(const wt_gpu_ctx*) { return 128; }
 
-int pose_grid(const wt_gpu_ctx* c) {
+// one wave of the pose kernel (occupancy calculator: registers and the
+// dynamic shared memory of this skeleton)
+template <class K>
+int pose_grid(wt_gpu_ctx* c, K kernel) {
   const int warps = pose_threads(c) / 32;
-  return std::max(1, std::min((c->V + 32 * warps - 1) / (32 * warps), wave(c, 4 * 148, "POSE")));
+  const int wave_ctas = full_wave(c, kernel, pose_threads(c), wt::pose_smem_bytes(c->L, c->NP, warps));
+  return std::max(1, std::min((c->V + 32 * warps - 1) / (32 * warps), wave(c, wave_ctas, "POSE")));
 }
 
 // JtJ entries per lane (upper triangle + Jtr) held in registers
@@ -572,7 +576,8 @@ int pose_q(int L) {
 
 template <int Q, int TPL>
 void launch_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt::PoseArgs& pa) {
-  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_pose_system<Q, TPL, true> : wt::k_pose_system<Q, TPL, false>, dim3(pose_grid(c), c->nseq), dim3(pose_threads(c)),
+  auto kern = c->nseq > 1 ? wt::k_pose_system<Q, TPL, true> : wt::k_pose_system<Q, TPL, false>;
+  WT_CUDA(wt::launch_pdl(kern, dim3(pose_grid(c, kern), c->nseq), dim3(pose_threads(c)),
                          wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32), c->stream, c->dm, s, phi, pa));
 }
 
