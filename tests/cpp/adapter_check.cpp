@@ -149,7 +149,39 @@ int main(int argc, char** argv) {
     }
   }
 
-  // 4. errors map onto the reference's exception types
+  // 4. the context cache follows the model, not just the state's address: the
+  //    same TrackerState object re-pointed at a rigidified model (same vertex
+  //    and link counts, different weights) must track with the new weights
+  {
+    TrackConfig cfg;
+    cfg.kin.iterations = 5;
+    cfg.shape.iterations = 2;
+    const ModelBundle rigid = rigidify(bundle);
+    TrackerState gpu_state = make_tracker(bundle, pose_at(sk, 0));
+    const CloudFrame f1 = render_frame(bundle, pose_at(sk, 1), {}, intr, NoiseSpec{}, 1);
+    gpu::track_frame(gpu_state, f1, intr, cfg);  // caches a context for the blended model
+    gpu_state.mesh = rigid.mesh;                 // same object, another model
+    gpu_state.theta = pose_at(sk, 1);
+    TrackerState cpu = make_tracker(rigid, pose_at(sk, 1));
+    cpu.frame_index = gpu_state.frame_index;
+    const CloudFrame f2 = render_frame(rigid, pose_at(sk, 2), {}, intr, NoiseSpec{}, 2);
+    track_frame(cpu, f2, intr, cfg);
+    gpu::track_frame(gpu_state, f2, intr, cfg);
+    expect(max_abs(cpu.theta, gpu_state.theta) <= 1e-6, "model swapped under the same TrackerState: theta",
+           max_abs(cpu.theta, gpu_state.theta), 1e-6);
+    expect(max_abs(cpu.mesh.phi, gpu_state.mesh.phi) <= 1e-6, "model swapped under the same TrackerState: phi",
+           max_abs(cpu.mesh.phi, gpu_state.mesh.phi), 1e-6);
+    // stats are appended to the caller's vector (kinopt.cpp:153-169)
+    std::vector<KinIterStats> st;
+    KinSolverConfig kin;
+    kin.iterations = 3;
+    gpu::optimize_pose(gpu_state, f2, intr, kin, AssocConfig{}, 1, &st);
+    gpu::optimize_pose(gpu_state, f2, intr, kin, AssocConfig{}, 1, &st);
+    expect(st.size() == 6, "optimize_pose appends its stats", static_cast<double>(st.size()), 6.0);
+    gpu::release(gpu_state);
+  }
+
+  // 5. errors map onto the reference's exception types
   {
     TrackerState bad = make_tracker(bundle, sk.zero_pose());
     bad.theta.resize(2);
