@@ -600,6 +600,8 @@ def run_ours(args, rank: int, world: int, local_rank: int, emit: bool = True):
         "gpu_launches": args.steps * S * (nker + 1),
         "clocks": clk.summary(),
     }
+    if getattr(args, "oversubscribed", False):
+        line["oversubscribed"] = "more ranks than GPUs: a functional check of the N>1 path, not a scaling number"
     if batch is not None:
         line["batch_c5"] = {
             "workload": batch["config"]["workload"], "value": batch["value"], "unit": "frames/s",
@@ -841,11 +843,23 @@ def main() -> None:
         return
     if args.config == "c5":  # 64 sequences per job, strong-scaled over the ranks
         args.sequences = max(1, C5_SEQUENCES // world)
+    oversubscribed = False
     if world > 1 and args.impl == "ours":
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        ngpu = torch.cuda.device_count()
+        if ngpu < world:
+            # more ranks than GPUs (a functional check of the N > 1 path on a
+            # smaller box): ranks share devices, gloo carries the barriers and
+            # the max over ranks; the numbers are not a scaling measurement
+            oversubscribed = True
+            local_rank = local_rank % max(ngpu, 1)
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    args.oversubscribed = oversubscribed
     if args.impl == "reference":
         run_reference(args, rank, world)
     elif args.config == "c5" and not args.streams:
