@@ -1406,6 +1406,14 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
   int* wq = qidx + warp * 64;       // warp-private queue of associated vertices
   double* wqr = qres + warp * 64;   // ... and their residuals
   int qn = 0;                       // warp-uniform queue length (< 32 between chunks)
+  // A batch (long scans: thousands of owned vertices per warp at C5) loads
+  // the next 32 owned vertices' sums one chunk ahead and the posed vertex and
+  // normal only for the associated ones (C5: 322 -> 299 us per launch); a lone
+  // sequence (two chunks per warp) keeps the one-round form (no spills).
+  constexpr bool WT_POSE_SCAN_AHEAD = B;
+  ulonglong4 q_next = make_ulonglong4(0ull, 0ull, 0ull, 0ull);
+  if (WT_POSE_SCAN_AHEAD && !a.count_in && gw + TW * lane < m.V)
+    q_next = ld256(reinterpret_cast<const ulonglong4*>(s.acc) + gw + TW * lane);
   for (int jb = 0;; jb += 32) {
     const bool more = gw + TW * jb < m.V;
     if (more) {
@@ -1414,17 +1422,26 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
       const int i = gw + TW * (jb + lane);
       bool have = false;
       double r = 0.0;
+      ulonglong4 q_cur = q_next;
+      if (WT_POSE_SCAN_AHEAD && !a.count_in) {
+        const int inext = gw + TW * (jb + 32 + lane);
+        if (inext < m.V) q_next = ld256(reinterpret_cast<const ulonglong4*>(s.acc) + inext);
+      }
       if (i < m.V) {
         if (a.count_in) {
           have = a.count_in[i] > 0;
           r = have ? a.res_in[i] : 0.0;
         } else {
-          const ulonglong4 q = ld256(reinterpret_cast<const ulonglong4*>(s.acc) + i);
+          const ulonglong4 q = WT_POSE_SCAN_AHEAD ? q_cur : ld256(reinterpret_cast<const ulonglong4*>(s.acc) + i);
           const ulonglong2 a01 = make_ulonglong2(q.x, q.y), a23 = make_ulonglong2(q.z, q.w);
-          const double4 v = ld256(s.pv + i);
-          const float4 n = s.pn[i];
           const long long c = static_cast<long long>(a23.y);
           have = c > 0;
+          double4 v = make_double4(0, 0, 0, 0);
+          float4 n = make_float4(0, 0, 0, 0);
+          if (!WT_POSE_SCAN_AHEAD || have) {
+            v = ld256(s.pv + i);
+            n = s.pn[i];
+          }
           if (have) {
             if (a.clean_acc) clear_obs(s, i);
             const double inv = 1.0 / static_cast<double>(c);
