@@ -1410,7 +1410,10 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
   // the next 32 owned vertices' sums one chunk ahead and the posed vertex and
   // normal only for the associated ones (C5: 322 -> 299 us per launch); a lone
   // sequence (two chunks per warp) keeps the one-round form (no spills).
-  constexpr bool WT_POSE_SCAN_AHEAD = B;
+#ifndef WT_POSE_AHEAD_MODE
+#define WT_POSE_AHEAD_MODE 0  // 0: batch only, 1: always, 2: never (experiments)
+#endif
+  constexpr bool WT_POSE_SCAN_AHEAD = WT_POSE_AHEAD_MODE == 1 ? true : (WT_POSE_AHEAD_MODE == 2 ? false : B);
   ulonglong4 q_next = make_ulonglong4(0ull, 0ull, 0ull, 0ull);
   if (WT_POSE_SCAN_AHEAD && !a.count_in && gw + TW * lane < m.V)
     q_next = ld256(reinterpret_cast<const ulonglong4*>(s.acc) + gw + TW * lane);
