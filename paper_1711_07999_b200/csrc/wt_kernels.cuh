@@ -1084,16 +1084,54 @@ static __global__ void __launch_bounds__(kVThreads, B ? WT_SEARCH_MINB_BATCH : 4
           }
         }
         const int c0 = max(pu - ks, 0), c1 = min(pu + ks, a.W - 1);
-        for (int dr = sub - ks; dr <= ks; dr += G) {
-          const int rr = pv + dr;
-          if (rr < 0 || rr >= a.H) continue;
-          const int r = rr * a.W;
-          if (dr >= -K1 && dr <= K1) {  // the core columns were scanned in phase 1
-            const int l1 = min(pu - K1 - 1, c1), r0 = max(pu + K1 + 1, c0);
-            if (l1 >= c0) scan_span(s, s.poff[r + c0], s.poff[r + l1 + 1], px, py, pz, a.cut2, bx, bi);
-            if (r0 <= c1) scan_span(s, s.poff[r + r0], s.poff[r + c1 + 1], px, py, pz, a.cut2, bx, bi);
-          } else {
-            scan_span(s, s.poff[r + c0], s.poff[r + c1 + 1], px, py, pz, a.cut2, bx, bi);
+#ifndef WT_RING_UNITS
+#define WT_RING_UNITS 1
+#endif
+        if (WT_RING_UNITS) {
+          // The (2ks+1)^2 box outside the core as work units dealt round-robin
+          // to the group's lanes: each full ring row (|dr| > K1) split into two
+          // interleaved halves (every other item of its span), then the left
+          // and right side spans of the core rows. The long full rows no
+          // longer land on one lane (ks = 2, G = 4: 11 -> ~5 items on the
+          // slowest lane).
+#ifndef WT_RING_SPLIT
+#define WT_RING_SPLIT 2  // pieces per full ring row
+#endif
+          constexpr int SP = WT_RING_SPLIT;
+          const int nrow = ks - K1;  // full rows above (and below) the core band
+          const int nunits = 2 * SP * nrow + 2 * (2 * K1 + 1);
+          for (int u = sub; u < nunits; u += G) {
+            int dr, lo, hi, off = 0, step = 1;
+            if (u < 2 * SP * nrow) {
+              const int fr = u / SP;
+              dr = fr < nrow ? -ks + fr : K1 + 1 + (fr - nrow);
+              lo = c0;
+              hi = c1;
+              off = u % SP;
+              step = SP;
+            } else {
+              const int v = u - 2 * SP * nrow;
+              dr = -K1 + (v >> 1);
+              lo = (v & 1) ? max(pu + K1 + 1, c0) : c0;
+              hi = (v & 1) ? c1 : min(pu - K1 - 1, c1);
+            }
+            const int rr = pv + dr;
+            if (lo > hi || rr < 0 || rr >= a.H) continue;
+            const int r = rr * a.W;
+            scan_span(s, s.poff[r + lo] + off, s.poff[r + hi + 1], px, py, pz, a.cut2, bx, bi, step);
+          }
+        } else {
+          for (int dr = sub - ks; dr <= ks; dr += G) {
+            const int rr = pv + dr;
+            if (rr < 0 || rr >= a.H) continue;
+            const int r = rr * a.W;
+            if (dr >= -K1 && dr <= K1) {  // the core columns were scanned in phase 1
+              const int l1 = min(pu - K1 - 1, c1), r0 = max(pu + K1 + 1, c0);
+              if (l1 >= c0) scan_span(s, s.poff[r + c0], s.poff[r + l1 + 1], px, py, pz, a.cut2, bx, bi);
+              if (r0 <= c1) scan_span(s, s.poff[r + r0], s.poff[r + c1 + 1], px, py, pz, a.cut2, bx, bi);
+            } else {
+              scan_span(s, s.poff[r + c0], s.poff[r + c1 + 1], px, py, pz, a.cut2, bx, bi);
+            }
           }
         }
       }
