@@ -1094,10 +1094,10 @@ static __global__ void __launch_bounds__(kVThreads, B ? WT_SEARCH_MINB_BATCH : 4
           // and right side spans of the core rows. The long full rows no
           // longer land on one lane (ks = 2, G = 4: 11 -> ~5 items on the
           // slowest lane).
-#ifndef WT_RING_SPLIT
-#define WT_RING_SPLIT 2  // pieces per full ring row
-#endif
-          constexpr int SP = WT_RING_SPLIT;
+          // pieces per full ring row: 2 for 4-lane groups (measured best at
+          // C5), 3 for 16-lane groups (ks = K1 + 1: 6 row pieces + 10 side
+          // spans = one unit per lane; C3 1903 -> 1917 frames/s)
+          constexpr int SP = G >= 16 ? 3 : 2;
           const int nrow = ks - K1;  // full rows above (and below) the core band
           const int nunits = 2 * SP * nrow + 2 * (2 * K1 + 1);
           for (int u = sub; u < nunits; u += G) {
