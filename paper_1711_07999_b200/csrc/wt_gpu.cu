@@ -1134,7 +1134,7 @@ int create_ctx(int device, const wt_model_desc* d, const wt_intrinsics* intr, in
     alloc_hook_state(c, c->hs);
     c->phi_scratch = c->mem.alloc<double4>(V);
     for (int b = 0; b < c->nseq; ++b) upload(seq_at(c->phi[0], c, b), ph.data(), V, c->stream);
-    if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8 + 4 * 296 + 8);
+    if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8 + 8 * 296 + 8);
     if (wt::pose_smem_bytes(L, c->NP, pose_threads(c) / 32) > 227 * 1024)
       fail(WT_EINVAL, "skeleton too large for the pose kernel's shared memory");
     if (wt::pose_tiles(L) <= 32) {
@@ -1301,7 +1301,7 @@ void* wt_gpu_stream(wt_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : 
 // Debug: last pose kernel's last-CTA timing (needs WT_DEBUG_POSE at create).
 int wt_gpu_debug_pose(wt_gpu_ctx* c, long long* out) {
   if (!c || !c->pose_dbg) return 0;
-  cudaMemcpy(out, c->pose_dbg, sizeof(long long) * (8 + 4 * 296), cudaMemcpyDeviceToHost);
+  cudaMemcpy(out, c->pose_dbg, sizeof(long long) * (8 + 8 * 296), cudaMemcpyDeviceToHost);
   return 5;
 }
 

@@ -210,6 +210,17 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+// The two kernels that precede k_pose_system (k_search; k_normals when the
+// correspondences are kept or in the stage hook) release their dependents
+// only after their own wait: once a k_pose_system CTA runs, every kernel
+// before its predecessor has completed, so it stages the pose tables (FK
+// output of the previous pose solve) before its own wait (pdl_wait).
+__device__ __forceinline__ void pdl_entry_ordered() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -745,7 +756,7 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
 template <bool B>
 static __global__ void __launch_bounds__(kVThreads, B ? 3 : 2) k_normals(DevModel m, DevState s, DevIntr in,
                                                        int do_bucket, int zero_acc, int compute) {
-  pdl_entry();
+  pdl_entry_ordered();
   if constexpr (B) s = seq_state(s);
   // grid-stride: a batch launches fewer, longer-lived CTAs per sequence
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
@@ -1021,7 +1032,7 @@ template <bool B, int NR = B ? kNearRingsBatch : kNearRingsSolo, int G = B ? kSe
           int SPL = B ? kSearchSplitBatch : kSearchSplitSolo>
 static __global__ void __launch_bounds__(kVThreads, B ? WT_SEARCH_MINB_BATCH : 4) k_search(DevState s, DevFrame f,
                                                                                         SearchArgs a) {
-  pdl_entry();
+  pdl_entry_ordered();
   if constexpr (B) s = seq_state(s);
   if constexpr (B) f = seq_frame(f);
   if constexpr (B) a.winners = seq_ptr(a.winners, seq_off(s.bstride));
@@ -1332,7 +1343,10 @@ __host__ __device__ inline int pose_tiles(int L) {
 // owned entries e = lane + 32 q (Q of them), any L <= 64.
 template <int Q, int TPL, bool B>
 static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
-  pdl_entry();
+  // a lone sequence waits after staging the pose tables (pdl_entry_ordered);
+  // a batch (thousands of rows per warp) keeps the plain entry
+  if constexpr (B) pdl_entry();
+  else pdl_trigger();
   if constexpr (B) s = seq_state(s);
   if constexpr (B) phi = seq_ptr(phi, seq_off(s.bstride));
   extern __shared__ __align__(16) double psm[];
@@ -1368,7 +1382,10 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int k = k0 + u * blockDim.x;
-        v[u] = k < n_off ? __ldg(s.offsets + k) : (k < n_off + n_dch ? __ldg(s.dchain + (k - n_off)) : 0.0);
+        if constexpr (B)
+          v[u] = k < n_off ? __ldg(s.offsets + k) : (k < n_off + n_dch ? __ldg(s.dchain + (k - n_off)) : 0.0);
+        else  // from L2: read before the wait (pdl_entry_ordered)
+          v[u] = k < n_off ? __ldcg(s.offsets + k) : (k < n_off + n_dch ? __ldcg(s.dchain + (k - n_off)) : 0.0);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1410,6 +1427,14 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
     }
   }
   __syncthreads();
+  if constexpr (!B) pdl_wait();
+  // WT_POSE_SECTIONS builds (diagnostics, tools/diag_pose.py): cycles of
+  // thread 0 in staging, scans, row builds and outer products
+#ifndef WT_POSE_SECTIONS
+#define WT_POSE_SECTIONS 0
+#endif
+  long long c_stage = 0, c_scan = 0, c_rows = 0, c_outer = 0, c_mark = 0;
+  if (WT_POSE_SECTIONS && a.dbg) c_stage = clock64() - t0;
 
   // Warp g of TW owns vertices g, g + TW, g + 2 TW, ... (every warp gets the
   // same count to within one, spread over the whole mesh, so no warp holds a
@@ -1457,6 +1482,7 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
     q_next = ld256(reinterpret_cast<const ulonglong4*>(s.acc) + gw + TW * lane);
   for (int jb = 0;; jb += 32) {
     const bool more = gw + TW * jb < m.V;
+    if (WT_POSE_SECTIONS && a.dbg) c_mark = clock64();
     if (more) {
       // scan 32 owned vertices: association and residual (association.cpp:132-136);
       // the posed vertex and normal are fetched with the sums (one round trip)
@@ -1506,13 +1532,31 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
       qn += __popc(hm);
       __syncwarp();
     }
+    if (WT_POSE_SECTIONS && a.dbg) {
+      const long long c = clock64();
+      c_scan += c - c_mark;
+      c_mark = c;
+    }
     // rows of full batches (and of the remainder at the end), every lane busy
     while (qn >= 32 || (!more && qn > 0)) {
       const int nrows = qn < 32 ? qn : 32;
+      // A short batch (a lone sequence's tail: ~8 rows per warp at C3) builds
+      // each row with `split` lanes; lane qq of a row takes the chain positions
+      // qq, qq + split, ... of every weight entry. theta_index is a permutation
+      // (validated at create), so a theta sits at its joint's depth in every
+      // chain that holds it: each row entry is still summed by one lane, in
+      // entry order -- bitwise the one-lane row.
+#ifndef WT_POSE_ROW_SPLIT
+#define WT_POSE_ROW_SPLIT 1
+#endif
+      const int lsh = (B || !WT_POSE_ROW_SPLIT) ? 0 : (nrows <= 8 ? 2 : (nrows <= 16 ? 1 : 0));
+      const int split = 1 << lsh, rt = lane >> lsh, qq = lane & (split - 1);
+      for (int k = lane; k < nrows * Lr; k += 32) wrows[k] = 0.0;
+      __syncwarp();
       bool has_row = false;
-      if (lane < nrows) {
-        const int i = wq[lane];
-        const double r = wqr[lane];
+      if (rt < nrows) {
+        const int i = wq[rt];
+        const double r = wqr[rt];
         const float4 n = s.pn[i];
         DQ raw;
         double sign[4];
@@ -1525,26 +1569,31 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
           const double nn[3] = {n.x, n.y, n.z};
           double r8[8];
           dq_point_plane_row(raw, rest, nn, r8);
-          double* row = wrows + lane * Lr;
-          for (int k = 0; k < L; ++k) row[k] = 0.0;
-          row[L] = r;
+          double* row = wrows + rt * Lr;
+          if (qq == 0) row[L] = r;
           const unsigned char li[4] = {lk.x, lk.y, lk.z, lk.w};
           const double wi[4] = {wv.x, wv.y, wv.z, wv.w};
           for (int e = 0; e < 4; ++e) {
             if (li[e] == 0xFF) break;
             const double coeff = wi[e] * sign[e];
-            for (int p = s_poff[li[e]]; p < s_poff[li[e] + 1]; ++p) {
+            for (int p = s_poff[li[e]] + qq; p < s_poff[li[e] + 1]; p += split) {
               const double* d8 = s_dch + 8 * p;
               const double dot = ((r8[0] * d8[0] + r8[1] * d8[1]) + (r8[2] * d8[2] + r8[3] * d8[3])) +
                                  ((r8[4] * d8[4] + r8[5] * d8[5]) + (r8[6] * d8[6] + r8[7] * d8[7]));
               row[s_pth[p]] += coeff * dot;
             }
           }
-          has_row = true;
+          has_row = qq == 0;
         }
       }
       unsigned mask = __ballot_sync(0xffffffffu, has_row);
+      if (lsh) mask = __ballot_sync(0xffffffffu, lane < nrows && ((mask >> (lane << lsh)) & 1u));
       __syncwarp();
+      if (WT_POSE_SECTIONS && a.dbg) {
+        const long long c = clock64();
+        c_rows += c - c_mark;
+        c_mark = c;
+      }
       if (mask) {
         double acc[NACC];
 #pragma unroll
@@ -1583,6 +1632,11 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
 #pragma unroll
         for (int q = 0; q < NACC; ++q)
           if (eidx[q] >= 0) wpart[eidx[q]] += fix(acc[q], a.sys_scale);
+      }
+      if (WT_POSE_SECTIONS && a.dbg) {
+        const long long c = clock64();
+        c_outer += c - c_mark;
+        c_mark = c;
       }
       // drop the processed rows from the queue
       const int rest_n = qn - nrows;
@@ -1640,6 +1694,11 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
     a.dbg[8 + 3 * slot] = static_cast<long long>(g_main);
     a.dbg[8 + 3 * slot + 1] = static_cast<long long>(g_end);
     a.dbg[8 + 3 * slot + 2] = t1 - t0;
+    long long* sec = a.dbg + 8 + 4 * 296 + 4 * slot;
+    sec[0] = c_stage;
+    sec[1] = c_scan;
+    sec[2] = c_rows;
+    sec[3] = c_outer;
   }
   if (a.dbg && threadIdx.x == 0 && blockIdx.x == 0) a.dbg[0] = t1 - t0;
 }
@@ -1659,7 +1718,7 @@ __host__ __device__ inline size_t pose_solve_smem_bytes(int L) {
 
 template <bool B>
 static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevState s, PoseArgs a) {
-  pdl_entry();
+  pdl_trigger();  // the model tables, theta and S are read before the wait (pdl_entry_ordered)
   if constexpr (B) s = seq_state(s);
   __shared__ FkTables fkt;
   extern __shared__ __align__(16) double solve_sm[];  // pose_solve_smem_bytes(L)
@@ -1684,20 +1743,26 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
   unsigned long long sum[4] = {0ull, 0ull, 0ull, 0ull};
   unsigned ent[4] = {0u, 0u, 0u, 0u};
   {
+    double th = 0.0, sd = 0.0;
+    if (threadIdx.x < L) {
+      th = __ldcg(s.theta + threadIdx.x);  // L2: written by the previous solve
+      sd = __ldg(m.s_diag + threadIdx.x);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = threadIdx.x + q * blockDim.x;
+      if (e < NE) ent[q] = __ldg(m.pose_e + e);
+    }
+    fk_stage(m, fkt);
+    pdl_wait();
     unsigned long long v[4][kRedCopies];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int e = threadIdx.x + q * blockDim.x;
       if (e < NE) {
-        ent[q] = __ldg(m.pose_e + e);
 #pragma unroll
         for (int c = 0; c < kRedCopies; ++c) v[q][c] = __ldcg(s.red + c * (NE + 2) + e);
       }
-    }
-    double th = 0.0, sd = 0.0;
-    if (threadIdx.x < L) {
-      th = s.theta[threadIdx.x];
-      sd = __ldg(m.s_diag + threadIdx.x);
     }
     unsigned long long rv[2 * kRedCopies];
     if (threadIdx.x == blockDim.x - 1) {
@@ -1707,7 +1772,6 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
         rv[2 * c + 1] = __ldcg(s.red + c * (NE + 2) + NE + 1);
       }
     }
-    fk_stage(m, fkt);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll

@@ -8,7 +8,7 @@ from paper_1711_07999_b200 import _lib as W
 bundle, intr, cfg = make_workload("c3")
 trk = Tracker(bundle, intr, trajectory(bundle, 0, 0))
 L = W.lib(); L.wt_gpu_debug_pose.argtypes = [C.c_void_p, C.c_void_p]
-buf = np.zeros(8 + 4 * 296, np.int64)
+buf = np.zeros(8 + 8 * 296, np.int64)
 for f in range(1, 5):
     d, _ = trk.render_depth(trajectory(bundle, f, 0), frame=f)
     trk.track_frame(cfg, depth=d)
@@ -23,3 +23,6 @@ print("main end (us from first start): median", np.median(rec[:, 0] - t0) / 1e3,
 print("atomics end: median", np.median(rec[:, 1] - t0) / 1e3, "max", (rec[:, 1].max() - t0) / 1e3)
 print("main cycles: median", np.median(rec[:, 2]), "max", rec[:, 2].max(), "argmax", rec[:, 2].argmax())
 print("atomic phase us: median", np.median(rec[:, 1] - rec[:, 0]) / 1e3, "max", (rec[:, 1] - rec[:, 0]).max() / 1e3)
+sec = buf[8 + 4 * 296: 8 + 8 * 296].reshape(296, 4)
+for j, n in enumerate(["stage", "scan", "rows", "outer"]):
+    print(f"{n} cycles (thread 0 of each CTA slot): median {np.median(sec[:, j]):.0f} max {sec[:, j].max()}")
