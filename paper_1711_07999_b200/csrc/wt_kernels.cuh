@@ -591,12 +591,19 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
 // K1 skinning: v = normalize(blend)(v0 + phi) (skinmesh.cpp:112-121).
 
 // One vertex: offsets in shared memory, every load issued before the arithmetic.
+// The model's weights and template vertex (constants) may come preloaded.
+struct SkinConst {
+  double4 wv, a;
+  uchar4 lk;
+};
+__device__ __forceinline__ SkinConst skin_const(const DevModel& m, int i) {
+  return {ld256(m.wgt + i), ld256(m.v0 + i), m.wlink[i]};
+}
 __device__ __forceinline__ void skin_vertex(const DevModel& m, const DevState& s, const double4* phi,
-                                            const double* s_off, int i) {
-  const double4 wv = ld256(m.wgt + i);  // all loads first (the 256-bit loads keep program order)
-  const double4 a = ld256(m.v0 + i);
+                                            const double* s_off, int i, const SkinConst& k) {
   const double4 f = ld256(phi + i);
-  const uchar4 lk = m.wlink[i];
+  const double4 wv = k.wv, a = k.a;
+  const uchar4 lk = k.lk;
   const double rest[3] = {a.x + f.x, a.y + f.y, a.z + f.z};
   DQ raw;
   double sign[4];
@@ -613,15 +620,21 @@ __device__ __forceinline__ void skin_vertex(const DevModel& m, const DevState& s
 
 template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_skin(DevModel m, DevState s, const double4* phi) {
+  // the first vertex's model constants load before the wait, under the
+  // predecessor's tail (the one-CTA pose solve, at C3 ~10 us)
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  SkinConst k0{};
+  if (i0 < m.V) k0 = skin_const(m, i0);
   pdl_entry();
   if constexpr (B) s = seq_state(s);
   if constexpr (B) phi = seq_ptr(phi, seq_off(s.bstride));
   extern __shared__ double s_off[];
   load_offsets(m, s, s_off);
   __syncthreads();
+  if (i0 < m.V) skin_vertex(m, s, phi, s_off, i0, k0);
   // grid-stride: a batch launches fewer, longer-lived CTAs per sequence
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x)
-    skin_vertex(m, s, phi, s_off, i);
+  for (int i = i0 + gridDim.x * blockDim.x; i < m.V; i += gridDim.x * blockDim.x)
+    skin_vertex(m, s, phi, s_off, i, skin_const(m, i));
 }
 
 // One of eight register values by a 3-bit slot (a select tree, no local memory).
@@ -680,10 +693,11 @@ __device__ __forceinline__ void fan_cross(unsigned rot, double vx, double vy, do
 // formed from registers with static indices; only the CSR-order summation
 // picks them by fan position (a select tree), so the arithmetic and its order
 // are the reference's.
-__device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* pv, int i, const double4& v,
-                                              double& nx, double& ny, double& nz) {
+// q: the vertex's fan ids (fan_nb row, a model constant; k_normals loads
+// the first vertex's before its PDL wait).
+__device__ __forceinline__ bool vertex_normal_q(const DevModel& m, const double4* pv, int i, const double4& v,
+                                                const ulonglong4& q, double& nx, double& ny, double& nz) {
   double ax = 0, ay = 0, az = 0;
-  const ulonglong4 q = ld256(reinterpret_cast<const ulonglong4*>(m.fan_nb + 8 * static_cast<size_t>(i)));
   const int id[8] = {static_cast<int>(q.x), static_cast<int>(q.x >> 32), static_cast<int>(q.y),
                      static_cast<int>(q.y >> 32), static_cast<int>(q.z), static_cast<int>(q.z >> 32),
                      static_cast<int>(q.w), static_cast<int>(q.w >> 32)};
@@ -745,6 +759,13 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
   nz = az / len;
   return v.w != 0.0;
 }
+__device__ __forceinline__ ulonglong4 fan_ids(const DevModel& m, int i) {
+  return ld256(reinterpret_cast<const ulonglong4*>(m.fan_nb + 8 * static_cast<size_t>(i)));
+}
+__device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* pv, int i, const double4& v,
+                                              double& nx, double& ny, double& nz) {
+  return vertex_normal_q(m, pv, i, v, fan_ids(m, i), nx, ny, nz);
+}
 
 // ---------------------------------------------------------------------------
 // K2 normals (skinmesh.cpp:125-139) fused with K3a: back-face cull, projection
@@ -756,16 +777,20 @@ __device__ __forceinline__ bool vertex_normal(const DevModel& m, const double4* 
 template <bool B>
 static __global__ void __launch_bounds__(kVThreads, B ? 3 : 2) k_normals(DevModel m, DevState s, DevIntr in,
                                                        int do_bucket, int zero_acc, int compute) {
+  // the first vertex's fan ids (model constants) load before the wait
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  ulonglong4 q0 = make_ulonglong4(0ull, 0ull, 0ull, 0ull);
+  if (compute && i0 < m.V) q0 = fan_ids(m, i0);
   pdl_entry_ordered();
   if constexpr (B) s = seq_state(s);
   // grid-stride: a batch launches fewer, longer-lived CTAs per sequence
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
+  for (int i = i0; i < m.V; i += gridDim.x * blockDim.x) {
     const double4 v = ld256(s.pv + i);
     const double vx = v.x, vy = v.y, vz = v.z;
     double nx = 0, ny = 0, nz = 0;
     bool valid;
     if (compute) {
-      valid = vertex_normal(m, s.pv, i, v, nx, ny, nz);
+      valid = vertex_normal_q(m, s.pv, i, v, i == i0 ? q0 : fan_ids(m, i), nx, ny, nz);
       s.pn[i] = make_float4(static_cast<float>(nx), static_cast<float>(ny), static_cast<float>(nz),
                             valid ? 1.0f : 0.0f);
     } else {  // normals given (loose-vertex association)
@@ -1032,30 +1057,46 @@ template <bool B, int NR = B ? kNearRingsBatch : kNearRingsSolo, int G = B ? kSe
           int SPL = B ? kSearchSplitBatch : kSearchSplitSolo>
 static __global__ void __launch_bounds__(kVThreads, B ? WT_SEARCH_MINB_BATCH : 4) k_search(DevState s, DevFrame f,
                                                                                         SearchArgs a) {
-  pdl_entry_ordered();
   if constexpr (B) s = seq_state(s);
   if constexpr (B) f = seq_frame(f);
   if constexpr (B) a.winners = seq_ptr(a.winners, seq_off(s.bstride));
-  const int nv = *f.n_valid;
-  const double oscale = obs_scale(f.n_valid);
-  const int w = a.window;
-  const int K1 = min(NR, w);
-  const double ifx = 1.0 / a.fx, ify = 1.0 / a.fy;
   const int lane = threadIdx.x & 31, sub = lane % G;
   constexpr int PPW = 32 / G;  // pixels per warp (lanes from PPW * G on idle)
   const int TW = gridDim.x * (blockDim.x >> 5);
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // The frame's pixel list and points (k_ingest, at the frame start: several
+  // kernels back, complete once this CTA runs -- pdl_entry_ordered) of the
+  // first pixel are read before the wait, from L2; the bucket lists after.
+  // (A lone sequence only: a batch's CTAs loop over many pixels.)
+  const int nv = __ldcg(f.n_valid);
+  int pix = -1;
+  double px = 0, py = 0, pz = 0;
+  if constexpr (!B) {
+    const int j = gw * PPW + lane / G;
+    pix = (lane < PPW * G && j < nv) ? __ldcg(f.vlist + j) : -1;
+    if (pix >= 0) {
+      px = __ldcg(f.pts_hi + 3 * pix);
+      py = __ldcg(f.pts_hi + 3 * pix + 1);
+      pz = __ldcg(f.pts_hi + 3 * pix + 2);
+    }
+  }
+  pdl_entry_ordered();
+  const double oscale = obs_scale(f.n_valid);
+  const int w = a.window;
+  const int K1 = min(NR, w);
+  const double ifx = 1.0 / a.fx, ify = 1.0 / a.fy;
   for (int base = gw * PPW; base < nv; base += TW * PPW) {
-    const int j = base + lane / G;
-    const int pix = (lane < PPW * G && j < nv) ? f.vlist[j] : -1;
+    if (B || base != gw * PPW) {
+      const int j = base + lane / G;
+      pix = (lane < PPW * G && j < nv) ? f.vlist[j] : -1;
+      if (pix >= 0) {
+        px = f.pts_hi[3 * pix];
+        py = f.pts_hi[3 * pix + 1];
+        pz = f.pts_hi[3 * pix + 2];
+      }
+    }
     const bool act = pix >= 0;
     const int pu = pix % a.W, pv = pix / a.W;
-    double px = 0, py = 0, pz = 0;
-    if (act) {
-      px = f.pts_hi[3 * pix];
-      py = f.pts_hi[3 * pix + 1];
-      pz = f.pts_hi[3 * pix + 2];
-    }
     double best_x = INFINITY;
     int best_i = -1;
     if (act && sub < (2 * K1 + 1) * SPL) {
@@ -2033,88 +2074,149 @@ struct ShapeArgs {
 
 constexpr int kNbrAhead = 4;  // neighbour gathers issued together in k_shape (kNN k = 4)
 
+// The loads of one vertex of the shape step that do not depend on the
+// association: phi and its neighbours' (the neighbour sum nd, in list order),
+// and -- PRE: read before the PDL wait, from L2 -- the posed vertex, normal
+// and skin weights, which otherwise load only for observed vertices.
+struct ShapeIn {
+  double ph[3], nd[3];
+  int ncount;
+  double4 v, wv;
+  float4 n;
+  uchar4 lk;
+};
+__device__ __forceinline__ double4 ld256_cg(const double4* p) {
+  double4 v;
+  asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+template <bool PRE>
+__device__ __forceinline__ ShapeIn shape_gather(const DevModel& m, const DevState& s, const double4* phi_in, int i) {
+  ShapeIn in;
+  const double4 f = PRE ? ld256_cg(phi_in + i) : ld256(phi_in + i);
+  if (PRE) {
+    in.v = ld256_cg(s.pv + i);
+    in.n = __ldcg(s.pn + i);
+    in.wv = ld256(m.wgt + i);
+    in.lk = m.wlink[i];
+  }
+  in.ph[0] = f.x;
+  in.ph[1] = f.y;
+  in.ph[2] = f.z;
+  in.nd[0] = in.nd[1] = in.nd[2] = 0.0;
+  in.ncount = 0;
+  // the first kNbrAhead neighbour indices, then their phi, all in flight at
+  // once; summed in list order up to the first -1 (as the loop below)
+  int jn[kNbrAhead];
+  double4 fn[kNbrAhead];
+#pragma unroll
+  for (int k = 0; k < kNbrAhead; ++k) jn[k] = k < m.K ? m.nbr[k * m.V + i] : -1;
+#pragma unroll
+  for (int k = 0; k < kNbrAhead; ++k) {
+    const double4* q = phi_in + (jn[k] >= 0 ? jn[k] : i);
+    fn[k] = PRE ? ld256_cg(q) : ld256(q);
+  }
+  bool more = true;
+#pragma unroll
+  for (int k = 0; k < kNbrAhead; ++k) {
+    if (!more || jn[k] < 0) {
+      more = false;
+      continue;
+    }
+    in.nd[0] += in.ph[0] - fn[k].x;
+    in.nd[1] += in.ph[1] - fn[k].y;
+    in.nd[2] += in.ph[2] - fn[k].z;
+    ++in.ncount;
+  }
+  for (int k = kNbrAhead; more && k < m.K; ++k) {
+    const int j = m.nbr[k * m.V + i];
+    if (j < 0) break;
+    const double4 fj = PRE ? ld256_cg(phi_in + j) : ld256(phi_in + j);
+    in.nd[0] += in.ph[0] - fj.x;
+    in.nd[1] += in.ph[1] - fj.y;
+    in.nd[2] += in.ph[2] - fj.z;
+    ++in.ncount;
+  }
+  return in;
+}
+
+struct ShapeAcc {
+  double abs_r = 0.0, sum_phi = 0.0, max_phi = 0.0;
+  long long observed = 0, singular = 0;
+};
+// One vertex of the shape step given its gathered inputs (PRE: posed vertex,
+// normal and weights included).
+template <bool PRE>
+__device__ __forceinline__ void shape_vertex(const DevModel& m, const DevState& s, const double* s_off,
+                                             const ShapeArgs& a, double4* phi_out, double oinv, int i,
+                                             const ShapeIn& in, ShapeAcc& acc) {
+  const ulonglong4 obs = load_obs(s.acc, i);
+  const double* ph = in.ph;
+  double g[3] = {0.0, 0.0, 0.0};
+  double r = 0.0;
+  double pt[3];
+  if (observed_mean(obs, oinv, pt)) {
+    if (a.clean_acc) clear_obs(s, i);
+    const double4 v = PRE ? in.v : ld256(s.pv + i);
+    const float4 n = PRE ? in.n : s.pn[i];
+    const double ro = static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
+                      static_cast<double>(n.z) * (pt[2] - v.z);
+    acc.abs_r += fabs(ro);
+    ++acc.observed;
+    DQ raw;
+    double sign[4];
+    if (n.w != 0.0f && blend_vertex(s_off, PRE ? in.wv : ld256(m.wgt + i), PRE ? in.lk : m.wlink[i], raw, sign)) {
+      // dr/dphi = -(R^T n), R = rotation of the normalised blend
+      double R[9];
+      dq_rotation(dq_normalize(raw), R);
+      g[0] = -(R[0] * n.x + R[3] * n.y + R[6] * n.z);
+      g[1] = -(R[1] * n.x + R[4] * n.y + R[7] * n.z);
+      g[2] = -(R[2] * n.x + R[5] * n.y + R[8] * n.z);
+      r = ro;
+    }
+  }
+  double delta[3];
+  const bool ok = solve_vertex3(g, r, ph, in.nd, in.ncount, a.lambda_phi, a.lambda_nbr, a.lambda_w,
+                                a.diag_floor, delta);
+  acc.singular += ok ? 0 : 1;
+  const double nx = ph[0] - delta[0], ny = ph[1] - delta[1], nz = ph[2] - delta[2];
+  st256(phi_out + i, make_double4(nx, ny, nz, 0.0));
+  const double len = sqrt(nx * nx + ny * ny + nz * nz);
+  acc.sum_phi += len;
+  acc.max_phi = fmax(acc.max_phi, len);
+}
+
 template <bool B>
 static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState s, const double4* phi_in,
                                                      double4* phi_out, ShapeArgs a) {
-  pdl_entry();
   if constexpr (B) s = seq_state(s);
   if constexpr (B) phi_in = seq_ptr(phi_in, seq_off(s.bstride));
   if constexpr (B) phi_out = seq_ptr(phi_out, seq_off(s.bstride));
   extern __shared__ double s_off[];
-  load_offsets(m, s, s_off);
-  __syncthreads();
-  double abs_r = 0.0, sum_phi = 0.0, max_phi = 0.0;
-  long long observed = 0, singular = 0;
-  const double oinv = obs_scale(s.fwords, true);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.V; i += gridDim.x * blockDim.x) {
-    // every load of the vertex up front (the 256-bit loads keep program order)
-    const double4 f = ld256(phi_in + i);
-    const ulonglong4 obs = load_obs(s.acc, i);
-    const double ph[3] = {f.x, f.y, f.z};
-    double nd[3] = {0.0, 0.0, 0.0};
-    int ncount = 0;
-    // the first kNbrAhead neighbour indices, then their phi, all in flight at
-    // once; summed in list order up to the first -1 (as the loop below)
-    int jn[kNbrAhead];
-    double4 fn[kNbrAhead];
-#pragma unroll
-    for (int k = 0; k < kNbrAhead; ++k) jn[k] = k < m.K ? m.nbr[k * m.V + i] : -1;
-#pragma unroll
-    for (int k = 0; k < kNbrAhead; ++k) fn[k] = ld256(phi_in + (jn[k] >= 0 ? jn[k] : i));
-    bool more = true;
-#pragma unroll
-    for (int k = 0; k < kNbrAhead; ++k) {
-      if (!more || jn[k] < 0) {
-        more = false;
-        continue;
-      }
-      nd[0] += ph[0] - fn[k].x;
-      nd[1] += ph[1] - fn[k].y;
-      nd[2] += ph[2] - fn[k].z;
-      ++ncount;
-    }
-    for (int k = kNbrAhead; more && k < m.K; ++k) {
-      const int j = m.nbr[k * m.V + i];
-      if (j < 0) break;
-      const double4 fj = ld256(phi_in + j);
-      nd[0] += ph[0] - fj.x;
-      nd[1] += ph[1] - fj.y;
-      nd[2] += ph[2] - fj.z;
-      ++ncount;
-    }
-    double g[3] = {0.0, 0.0, 0.0};
-    double r = 0.0;
-    double pt[3];
-    if (observed_mean(obs, oinv, pt)) {
-      if (a.clean_acc) clear_obs(s, i);
-      const double4 v = ld256(s.pv + i);
-      const float4 n = s.pn[i];
-      const double ro = static_cast<double>(n.x) * (pt[0] - v.x) + static_cast<double>(n.y) * (pt[1] - v.y) +
-                        static_cast<double>(n.z) * (pt[2] - v.z);
-      abs_r += fabs(ro);
-      ++observed;
-      DQ raw;
-      double sign[4];
-      if (n.w != 0.0f && blend_vertex(s_off, ld256(m.wgt + i), m.wlink[i], raw, sign)) {
-        // dr/dphi = -(R^T n), R = rotation of the normalised blend
-        double R[9];
-        dq_rotation(dq_normalize(raw), R);
-        g[0] = -(R[0] * n.x + R[3] * n.y + R[6] * n.z);
-        g[1] = -(R[1] * n.x + R[4] * n.y + R[7] * n.z);
-        g[2] = -(R[2] * n.x + R[5] * n.y + R[8] * n.z);
-        r = ro;
-      }
-    }
-    double delta[3];
-    const bool ok = solve_vertex3(g, r, ph, nd, ncount, a.lambda_phi, a.lambda_nbr, a.lambda_w,
-                                  a.diag_floor, delta);
-    singular += ok ? 0 : 1;
-    const double nx = ph[0] - delta[0], ny = ph[1] - delta[1], nz = ph[2] - delta[2];
-    st256(phi_out + i, make_double4(nx, ny, nz, 0.0));
-    const double len = sqrt(nx * nx + ny * ny + nz * nz);
-    sum_phi += len;
-    max_phi = fmax(max_phi, len);
+  // A lone sequence gathers its first vertex and stages the pose offsets
+  // before the PDL wait: phi (the previous shape step's), the posed vertex
+  // and normal are several kernels back, complete once this CTA runs
+  // (pdl_entry_ordered); only the association sums need the wait.
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  ShapeIn pre{};
+  if constexpr (!B) {
+    if (i0 < m.V) pre = shape_gather<true>(m, s, phi_in, i0);
+    for (int k = threadIdx.x; k < m.L * 8; k += blockDim.x) s_off[k] = __ldcg(s.offsets + k);
   }
+  pdl_entry();
+  if constexpr (B) load_offsets(m, s, s_off);
+  __syncthreads();
+  ShapeAcc acc;
+  const double oinv = obs_scale(s.fwords, true);
+  int i = i0;
+  if (!B && i0 < m.V) {
+    shape_vertex<true>(m, s, s_off, a, phi_out, oinv, i0, pre, acc);
+    i += gridDim.x * blockDim.x;
+  }
+  for (; i < m.V; i += gridDim.x * blockDim.x)
+    shape_vertex<false>(m, s, s_off, a, phi_out, oinv, i, shape_gather<false>(m, s, phi_in, i), acc);
+  double abs_r = acc.abs_r, sum_phi = acc.sum_phi, max_phi = acc.max_phi;
+  long long observed = acc.observed, singular = acc.singular;
   // block reductions (fixed order), then per-CTA partials folded by the last CTA
   block_sum2(abs_r, observed);
   double sp = sum_phi;
