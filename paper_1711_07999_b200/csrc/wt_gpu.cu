@@ -623,8 +623,11 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
   pa.count_in = count_in;
   pa.res_in = res_in;
   pa.dbg = c->pose_dbg;
-  if (wt::pose_tiles(c->L) <= 32) {
-    launch_pose<1, 1>(c, s, phi, pa);
+  const int edge = wt::pose_tile_edge(c->L);
+  if (edge == 3) {
+    launch_pose<1, 3>(c, s, phi, pa);
+  } else if (edge == 4) {
+    launch_pose<1, 4>(c, s, phi, pa);
   } else {
     switch (pose_q(c->L)) {
       case 8: launch_pose<8, 0>(c, s, phi, pa); break;
@@ -1137,8 +1140,11 @@ int create_ctx(int device, const wt_model_desc* d, const wt_intrinsics* intr, in
     if (getenv("WT_DEBUG_POSE")) c->pose_dbg = c->mem.alloc<long long>(8 + 8 * 296 + 8);
     if (wt::pose_smem_bytes(L, c->NP, pose_threads(c) / 32) > 227 * 1024)
       fail(WT_EINVAL, "skeleton too large for the pose kernel's shared memory");
-    if (wt::pose_tiles(L) <= 32) {
-      pose_attr<1, 1>(c);
+    const int edge = wt::pose_tile_edge(L);
+    if (edge == 3) {
+      pose_attr<1, 3>(c);
+    } else if (edge == 4) {
+      pose_attr<1, 4>(c);
     } else {
       switch (pose_q(L)) {
         case 8: pose_attr<8, 0>(c); break;

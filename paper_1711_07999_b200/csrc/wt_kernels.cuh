@@ -210,11 +210,11 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
-// The two kernels that precede k_pose_system (k_search; k_normals when the
-// correspondences are kept or in the stage hook) release their dependents
-// only after their own wait: once a k_pose_system CTA runs, every kernel
-// before its predecessor has completed, so it stages the pose tables (FK
-// output of the previous pose solve) before its own wait (pdl_wait).
+// k_search and k_normals release their dependents only after their own
+// wait: once a CTA of their successor runs, every kernel before its
+// predecessor has completed, and it may read that output before its own
+// wait (pdl_wait) -- k_pose_system and k_pose_solve the FK output of the
+// previous pose solve, k_shape phi and the posed mesh.
 __device__ __forceinline__ void pdl_entry_ordered() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1069,6 +1069,7 @@ static __global__ void __launch_bounds__(kVThreads, B ? WT_SEARCH_MINB_BATCH : 4
   // first pixel are read before the wait, from L2; the bucket lists after.
   // (A lone sequence only: a batch's CTAs loop over many pixels.)
   const int nv = __ldcg(f.n_valid);
+  const double oscale = obs_scale(f.n_valid);
   int pix = -1;
   double px = 0, py = 0, pz = 0;
   if constexpr (!B) {
@@ -1081,7 +1082,6 @@ static __global__ void __launch_bounds__(kVThreads, B ? WT_SEARCH_MINB_BATCH : 4
     }
   }
   pdl_entry_ordered();
-  const double oscale = obs_scale(f.n_valid);
   const int w = a.window;
   const int K1 = min(NR, w);
   const double ifx = 1.0 / a.fx, ify = 1.0 / a.fy;
@@ -1371,17 +1371,23 @@ __host__ __device__ inline size_t pose_smem_bytes(int L, int NP, int warps) {
          (sizeof(double) + sizeof(int)) * warps * 64 + 16;
 }
 
-// Upper 4x4 tiles of the L x (L+1) block [JtJ | Jtr]: tile (bi, bj), bj >= bi.
-__host__ __device__ inline int pose_tiles(int L) {
-  const int nbr = (L + 3) >> 2, nbc = (L + 4) >> 2;
+// Upper T x T tiles of the L x (L+1) block [JtJ | Jtr]: tile (bi, bj), bj >= bi.
+__host__ __device__ inline int pose_tiles(int L, int T = 4) {
+  const int nbr = (L + T - 1) / T, nbc = (L + T) / T;
   int n = 0;
   for (int bi = 0; bi < nbr; ++bi) n += nbc - bi;
   return n;
 }
+// Tile edge of the pose kernel for L links: 3 while the 3x3 tiles fit one
+// warp (L <= 20: 28 tiles, 9 FMAs per row per lane), else 4 (L <= 27), else
+// 0 (lane-owned entries).
+__host__ __device__ inline int pose_tile_edge(int L) {
+  return pose_tiles(L, 3) <= 32 ? 3 : (pose_tiles(L, 4) <= 32 ? 4 : 0);
+}
 
-// TPL = 1: every lane owns one 4x4 tile of [JtJ | Jtr] (needs pose_tiles(L)
-// <= 32, i.e. L <= 27): per row 8 shared loads feed 16 FMAs. TPL = 0: lane-
-// owned entries e = lane + 32 q (Q of them), any L <= 64.
+// TPL = T (3 or 4): every lane owns one T x T tile of [JtJ | Jtr]: per row
+// 2T shared loads feed T^2 FMAs. TPL = 0: lane-owned entries
+// e = lane + 32 q (Q of them), any L <= 64.
 template <int Q, int TPL, bool B>
 static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
   // a lone sequence waits after staging the pose tables (pdl_entry_ordered);
@@ -1408,6 +1414,7 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
       (reinterpret_cast<uintptr_t>(eb + NE) + 15) & ~static_cast<uintptr_t>(15));  // nw * 64
   int* qidx = reinterpret_cast<int*>(qres + nw * 64);                             // nw * 64
 
+  const double oinv = a.count_in ? 1.0 : obs_scale(s.fwords, true);  // frame words (k_ingest)
   const long long t0 = clock64();
   if (a.dbg && threadIdx.x == 0) {
     unsigned long long g0;
@@ -1453,10 +1460,10 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
       }
     }
   }
-  // this lane's tile (TPL == 1)
+  // this lane's tile (TPL > 0)
   int tbi = -1, tbj = -1;
-  if (TPL == 1) {
-    const int nbr = (L + 3) >> 2, nbc = (L + 4) >> 2;
+  if (TPL > 0) {
+    const int nbr = (L + TPL - 1) / TPL, nbc = (L + TPL) / TPL;
     int t = lane;
     for (int bi = 0; bi < nbr; ++bi) {
       if (t < nbc - bi) {
@@ -1484,7 +1491,7 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
   // their rows (fill_row) in a warp-private shared tile, every lane busy, and
   // the batch's outer products are accumulated in fp64 registers in
   // ascending queue order, then added to 2^-40 fixed-point integers.
-  constexpr int NACC = TPL == 1 ? 16 : Q;
+  constexpr int NACC = TPL > 0 ? TPL * TPL : Q;
   // fixed-point accumulators: the warp's NE entries in shared memory, each
   // owned by exactly one lane (no atomics)
   long long* wpart = part + warp * NE;
@@ -1493,8 +1500,8 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
 #pragma unroll
   for (int q = 0; q < NACC; ++q) {
     int e = -1;
-    if (TPL == 1) {
-      const int ra = 4 * tbi + q / 4, cb = 4 * tbj + q % 4;
+    if (TPL > 0) {
+      const int ra = TPL * tbi + q / TPL, cb = TPL * tbj + q % TPL;
       if (tbi >= 0 && ra < L && cb <= L && (cb == L || ra <= cb))
         e = cb == L ? NT + ra : ra * L - ra * (ra - 1) / 2 + (cb - ra);
     } else {
@@ -1504,7 +1511,6 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
   }
   __syncwarp();
   long long rsq = 0, nassoc = 0;  // sum r^2 (fixed point at a.res_scale), associated count
-  const double oinv = a.count_in ? 1.0 : obs_scale(s.fwords, true);
   double* wrows = rows + warp * 32 * Lr;
   const int TW = gridDim.x * nw, gw = blockIdx.x * nw + warp;
   int* wq = qidx + warp * 64;       // warp-private queue of associated vertices
@@ -1639,23 +1645,23 @@ static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevSt
         double acc[NACC];
 #pragma unroll
         for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
-        if (TPL == 1) {
+        if (TPL > 0) {
           if (tbi >= 0) {
-            const int ca = 4 * tbi, cb = 4 * tbj;
+            const int ca = TPL * tbi, cb = TPL * tbj;
             while (mask) {
               const int t = __ffs(mask) - 1;
               mask &= mask - 1;
               const double* row = wrows + t * Lr;
-              double ra[4], rb[4];
+              double ra[TPL > 0 ? TPL : 1], rb[TPL > 0 ? TPL : 1];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
+              for (int u = 0; u < TPL; ++u) {
                 ra[u] = row[min(ca + u, L)];  // clamped: in-bounds, discarded beyond L
                 rb[u] = row[min(cb + u, L)];
               }
 #pragma unroll
-              for (int u = 0; u < 4; ++u)
+              for (int u = 0; u < TPL; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[4 * u + v] += ra[u] * rb[v];
+                for (int v = 0; v < TPL; ++v) acc[TPL * u + v] += ra[u] * rb[v];
             }
           }
         } else {
@@ -2203,11 +2209,11 @@ static __global__ void __launch_bounds__(kVThreads) k_shape(DevModel m, DevState
     if (i0 < m.V) pre = shape_gather<true>(m, s, phi_in, i0);
     for (int k = threadIdx.x; k < m.L * 8; k += blockDim.x) s_off[k] = __ldcg(s.offsets + k);
   }
+  const double oinv = obs_scale(s.fwords, true);  // frame words (k_ingest)
   pdl_entry();
   if constexpr (B) load_offsets(m, s, s_off);
   __syncthreads();
   ShapeAcc acc;
-  const double oinv = obs_scale(s.fwords, true);
   int i = i0;
   if (!B && i0 < m.V) {
     shape_vertex<true>(m, s, s_off, a, phi_out, oinv, i0, pre, acc);

@@ -218,10 +218,10 @@ def test_errors_surface():
     t.close()
 
 
-@pytest.mark.parametrize("links", [6, 27, 28, 40])
+@pytest.mark.parametrize("links", [6, 20, 21, 27, 28, 40])
 def test_long_chains_against_oracle(links):
-    """Both JtJ accumulation layouts (4x4 lane tiles up to 27 links, lane-
-    owned entries beyond) and both solvers (one-warp LDL^T up to 32 links,
+    """Every JtJ accumulation layout (3x3 lane tiles up to 20 links, 4x4 up to
+    27, lane-owned entries beyond) and both solvers (one-warp LDL^T up to 32 links,
     block LDL^T beyond): normal system and two pose iterations on a cloud vs
     the C oracle."""
     from . import rigs
