@@ -206,6 +206,7 @@ struct wt_gpu_ctx {
   cudaStream_t up_stream = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   std::function<void()> before_search;  // the join, run once by the next enq_search
+  bool walk_back = false;               // seq_walk: the next batched launch walks the sequences backwards
 
   ~wt_gpu_ctx() {
     for (int b = 0; b < 2; ++b) {
@@ -479,30 +480,40 @@ void ensure_stats(wt_gpu_ctx* c, int nk, int ns) {
 
 // ---- kernel launch helpers (all on ctx->stream) ------------------------------
 
+// A batch walks its sequences in alternating order from one launch to the
+// next (blockIdx.y ascending, then descending: a negative stride, seq_off):
+// the sequences a kernel touched last are still in L2 when the next kernel
+// starts with them.
+wt::DevState seq_walk(wt_gpu_ctx* c, wt::DevState s) {
+  if (c->nseq > 1 && c->walk_back) s.bstride = -s.bstride;
+  c->walk_back = !c->walk_back;
+  return s;
+}
+
 void enq_fk(wt_gpu_ctx* c, const wt::DevState& s) {
-  wt::launch_fk(c->stream, c->nseq, c->dm, s);
+  wt::launch_fk(c->stream, c->nseq, c->dm, seq_walk(c, s));
   mark(c, K_FK);
 }
 
 void enq_skin(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi) {
-  wt::launch_skin(c->stream, vgrid(c->V), c->nseq, c->L, c->dm, s, phi);
+  wt::launch_skin(c->stream, vgrid(c->V), c->nseq, c->L, c->dm, seq_walk(c, s), phi);
   mark(c, K_SKIN);
 }
 
 void enq_normals(wt_gpu_ctx* c, const wt::DevState& s, bool bucket, bool zero_acc,
                  bool compute = true) {
-  wt::launch_normals(c->stream, vgrid(c->V), c->nseq, c->dm, s, c->din, bucket ? 1 : 0, zero_acc ? 1 : 0,
+  wt::launch_normals(c->stream, vgrid(c->V), c->nseq, c->dm, seq_walk(c, s), c->din, bucket ? 1 : 0, zero_acc ? 1 : 0,
                      compute ? 1 : 0);
   mark(c, K_NORMALS);
 }
 
 void enq_scatter(wt_gpu_ctx* c, const wt::DevState& s) {
-  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_pixoff<true> : wt::k_pixoff<false>, dim3((c->din.H + 7) / 8, c->nseq), dim3(wt::kVThreads), 0, c->stream, s,
-                         c->din.W, c->din.H));
+  WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_pixoff<true> : wt::k_pixoff<false>, dim3((c->din.H + 7) / 8, c->nseq), dim3(wt::kVThreads), 0, c->stream,
+                         seq_walk(c, s), c->din.W, c->din.H));
   mark(c, K_PIXOFF);
   WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_scatter<true> : wt::k_scatter<false>,
-                         dim3(vgrid(std::max(c->V, c->din.H)), c->nseq), dim3(wt::kVThreads), 0, c->stream, c->dm, s,
-                         c->din.H));
+                         dim3(vgrid(std::max(c->V, c->din.H)), c->nseq), dim3(wt::kVThreads), 0, c->stream, c->dm,
+                         seq_walk(c, s), c->din.H));
   mark(c, K_SCATTER);
 }
 
@@ -542,7 +553,9 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
                           : (big_frame ? wt::k_search<false, wt::kNearRingsSolo, 8, 1> : wt::k_search<false>);
   // one wave (warps stride over the pixel groups); a batch shares 8 waves between its sequences
   const int grid = std::max(1, std::min(c->P * G / wt::kVThreads + 1, wave(c, full_wave(c, kern), "SEARCH", 8.0)));
-  WT_CUDA(wt::launch_pdl(kern, dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, s, f, sa));
+  const wt::DevState sw = seq_walk(c, s);
+  f.bstride = sw.bstride;
+  WT_CUDA(wt::launch_pdl(kern, dim3(grid, c->nseq), dim3(wt::kVThreads), 0, c->stream, sw, f, sa));
   mark(c, K_SEARCH);
 }
 
@@ -578,7 +591,8 @@ template <int Q, int TPL>
 void launch_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt::PoseArgs& pa) {
   auto kern = c->nseq > 1 ? wt::k_pose_system<Q, TPL, true> : wt::k_pose_system<Q, TPL, false>;
   WT_CUDA(wt::launch_pdl(kern, dim3(pose_grid(c, kern), c->nseq), dim3(pose_threads(c)),
-                         wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32), c->stream, c->dm, s, phi, pa));
+                         wt::pose_smem_bytes(c->L, c->NP, pose_threads(c) / 32), c->stream, c->dm, seq_walk(c, s), phi,
+                         pa));
 }
 
 template <int Q, int TPL>
@@ -637,7 +651,7 @@ void enq_pose(wt_gpu_ctx* c, const wt::DevState& s, const double4* phi, const wt
     }
   }
   mark(c, K_POSE);
-  wt::launch_pose_solve(c->stream, c->nseq, c->L, c->dm, s, pa);
+  wt::launch_pose_solve(c->stream, c->nseq, c->L, c->dm, seq_walk(c, s), pa);
   mark(c, K_POSE_SOLVE);
 }
 
@@ -654,7 +668,7 @@ void enq_shape(wt_gpu_ctx* c, const wt_shape_config* sc, int it, const double4* 
   sa.iteration = it;
   sa.clean_acc = 1;
   WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_shape<true> : wt::k_shape<false>, dim3(shape_grid(c), c->nseq), dim3(wt::kVThreads), sizeof(double) * 8 * c->L, c->stream,
-                         c->dm, c->ds, in, out, sa));
+                         c->dm, seq_walk(c, c->ds), in, out, sa));
   mark(c, K_SHAPE);
 }
 
@@ -690,7 +704,7 @@ int enq_optimize_shape(wt_gpu_ctx* c, int cur, const wt_shape_config* sc, const 
     enq_skin(c, c->ds, c->phi[cur]);
     enq_associate(c, c->ds, a, nullptr);
     WT_CUDA(wt::launch_pdl(c->nseq > 1 ? wt::k_shape_after<true> : wt::k_shape_after<false>, dim3(shape_grid(c), c->nseq), dim3(wt::kVThreads), 0, c->stream, c->dm,
-                           c->ds, sc->iterations, 1));
+                           seq_walk(c, c->ds), sc->iterations, 1));
     mark(c, K_SHAPE_AFTER);
   }
   return cur;

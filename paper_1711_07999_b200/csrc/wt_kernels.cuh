@@ -124,8 +124,11 @@ __device__ __forceinline__ T* seq_ptr(T* p, long long off) {
   return p ? reinterpret_cast<T*>(reinterpret_cast<unsigned long long>(p) + off) : p;
 }
 
+// A negative stride walks the batch backwards: blockIdx.y = 0 is the last
+// sequence (the host alternates the direction from launch to launch, seq_walk).
 __device__ __forceinline__ long long seq_off(long long bstride) {
-  return static_cast<long long>(blockIdx.y) * bstride;
+  return bstride >= 0 ? static_cast<long long>(blockIdx.y) * bstride
+                      : static_cast<long long>(gridDim.y - 1 - blockIdx.y) * -bstride;
 }
 
 __device__ inline DevState seq_state(DevState s) {
