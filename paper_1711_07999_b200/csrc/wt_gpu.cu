@@ -132,7 +132,7 @@ struct wt_gpu_ctx {
   float* d_depth = nullptr;
   uint8_t* d_valid = nullptr;
   double* d_pts_hi = nullptr;
-  int* d_vlist = nullptr;
+  double4* d_vpts = nullptr;  // valid-pixel list records (point, pixel; k_ingest -> k_search)
   int* d_nvalid = nullptr;
   int* d_winners = nullptr;
   bool frame_loaded = false;
@@ -412,7 +412,7 @@ void layout_seq(wt_gpu_ctx* c, Carve& a) {
   c->d_valid = a.take<uint8_t>(P);
   c->d_pts_hi = a.take<double>(3 * static_cast<size_t>(P));
   // valid-pixel list: one run of 32 entries per 32-column row segment
-  c->d_vlist = a.take<int>(32 * H * ((c->din.W + 31) / 32));
+  c->d_vpts = a.take<double4>(32 * H * ((c->din.W + 31) / 32));
   c->d_nvalid = a.take<int>(4);  // frame words: [0] list length, [2..3] max |coordinate| (k_ingest)
   s.fwords = c->d_nvalid;
   s.spart = a.take<double>(static_cast<size_t>(wt::kStatParts) * vgrid(V));
@@ -523,7 +523,7 @@ void enq_search(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* a, 
     c->before_search = nullptr;
     join();
   }
-  wt::DevFrame f{c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid, c->bstride};
+  wt::DevFrame f{c->d_valid, c->d_pts_hi, c->d_vpts, c->d_nvalid, c->bstride};
   wt::SearchArgs sa;
   sa.fx = c->din.fx;
   sa.fy = c->din.fy;
@@ -1238,7 +1238,7 @@ static void ingest(wt_gpu_ctx* c, const float* depth_dev, double scale, const do
   else WT_CUDA(cudaMemset2DAsync(c->d_nvalid, static_cast<size_t>(c->bstride), 0, 4 * sizeof(int), c->nseq, st));
   const int segs = (c->din.W + wt::kIngestSeg - 1) / wt::kIngestSeg;
   (c->nseq > 1 ? wt::k_ingest<true> : wt::k_ingest<false>)<<<dim3(segs * c->din.H, c->nseq), wt::kIngestSeg, 0, st>>>(
-      c->din, depth_dev, scale, cloud_dev, valid_dev, c->d_valid, c->d_pts_hi, c->d_vlist, c->d_nvalid, c->bstride);
+      c->din, depth_dev, scale, cloud_dev, valid_dev, c->d_valid, c->d_pts_hi, c->d_vpts, c->d_nvalid, c->bstride);
   check_launch();
 }
 

@@ -105,7 +105,7 @@ struct DevState {
 struct DevFrame {
   const uint8_t* valid;  // per pixel
   const double* pts_hi;  // per pixel fp64 point (valid pixels only)
-  const int* vlist;      // valid pixel indices
+  const double4* vpts;   // valid-pixel list: the pixel's point and index (bits of .w; -1 padding)
   const int* n_valid;
   long long bstride;
 };
@@ -161,7 +161,7 @@ __device__ inline DevFrame seq_frame(DevFrame f) {
   if (o == 0) return f;
   f.valid = seq_ptr(f.valid, o);
   f.pts_hi = seq_ptr(f.pts_hi, o);
-  f.vlist = seq_ptr(f.vlist, o);
+  f.vpts = seq_ptr(f.vpts, o);
   f.n_valid = seq_ptr(f.n_valid, o);
   return f;
 }
@@ -179,6 +179,12 @@ __device__ inline DevFrame seq_frame(DevFrame f) {
 __device__ __forceinline__ double4 ld256(const double4* p) {
   double4 v;
   asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+// From L2 (reads issued before a PDL wait: never a stale L1 line).
+__device__ __forceinline__ double4 ld256_cg(const double4* p) {
+  double4 v;
+  asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
   return v;
 }
 __device__ __forceinline__ ulonglong4 ld256(const ulonglong4* p) {
@@ -523,7 +529,7 @@ constexpr int kRunAlign = 4;  // valid-pixel runs padded to 4 entries (a batch s
 template <bool B>
 static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const float* depth, double scale,
                                                       const double* cloud, const uint8_t* cloud_valid,
-                                                      uint8_t* pvalid, double* pts_hi, int* vlist,
+                                                      uint8_t* pvalid, double* pts_hi, double4* vpts,
                                                       int* n_valid, long long bstride) {
   if constexpr (B) {  // sequence blockIdx.y of a batch (see seq_state)
     const long long o = seq_off(bstride);
@@ -532,7 +538,7 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
     cloud_valid = seq_ptr(cloud_valid, o);
     pvalid = seq_ptr(pvalid, o);
     pts_hi = seq_ptr(pts_hi, o);
-    vlist = seq_ptr(vlist, o);
+    vpts = seq_ptr(vpts, o);
     n_valid = seq_ptr(n_valid, o);
   }
   const int segs = (in.W + kIngestSeg - 1) / kIngestSeg;
@@ -541,8 +547,8 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
   const int i = v * in.W + u;
   int valid = 0;
   double mx = 0.0;  // max |coordinate| of this pixel's point
+  double x = 0, y = 0, z = 0;
   if (u < in.W) {
-    double x = 0, y = 0, z = 0;
     if (depth) {
       const float d = depth[i];
       if (d > 0.0f && isfinite(d)) {
@@ -584,8 +590,10 @@ static __global__ void __launch_bounds__(kIngestSeg) k_ingest(DevIntr in, const 
     int base = 0;
     if (lane == 0) base = atom_add(n_valid, padded);
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (valid) vlist[base + __popc(m & ((1u << lane) - 1u))] = i;
-    if (lane >= n && lane < padded) vlist[base + lane] = -1;
+    if (valid)
+      st256(vpts + base + __popc(m & ((1u << lane) - 1u)),
+            make_double4(x, y, z, __longlong_as_double(static_cast<long long>(i))));
+    if (lane >= n && lane < padded) st256(vpts + base + lane, make_double4(0.0, 0.0, 0.0, __longlong_as_double(-1ll)));
   }
 }
 
@@ -1073,30 +1081,31 @@ static __global__ void __launch_bounds__(kVThreads, B ? WT_SEARCH_MINB_BATCH : 4
   // (A lone sequence only: a batch's CTAs loop over many pixels.)
   const int nv = __ldcg(f.n_valid);
   const double oscale = obs_scale(f.n_valid);
-  int pix = -1;
-  double px = 0, py = 0, pz = 0;
+  // the list record (point, pixel) of this lane's pixel; a lone sequence
+  // loads it one grid-stride step ahead: the first before the wait, the
+  // next one as each step starts
+  double4 rec = make_double4(0.0, 0.0, 0.0, __longlong_as_double(-1ll));
+  const bool lane_on = lane < PPW * G;
   if constexpr (!B) {
     const int j = gw * PPW + lane / G;
-    pix = (lane < PPW * G && j < nv) ? __ldcg(f.vlist + j) : -1;
-    if (pix >= 0) {
-      px = __ldcg(f.pts_hi + 3 * pix);
-      py = __ldcg(f.pts_hi + 3 * pix + 1);
-      pz = __ldcg(f.pts_hi + 3 * pix + 2);
-    }
+    if (lane_on && j < nv) rec = ld256_cg(f.vpts + j);
   }
   pdl_entry_ordered();
   const int w = a.window;
   const int K1 = min(NR, w);
   const double ifx = 1.0 / a.fx, ify = 1.0 / a.fy;
   for (int base = gw * PPW; base < nv; base += TW * PPW) {
-    if (B || base != gw * PPW) {
+    if constexpr (B) {  // a batch: no registers to spare for the step ahead
       const int j = base + lane / G;
-      pix = (lane < PPW * G && j < nv) ? f.vlist[j] : -1;
-      if (pix >= 0) {
-        px = f.pts_hi[3 * pix];
-        py = f.pts_hi[3 * pix + 1];
-        pz = f.pts_hi[3 * pix + 2];
-      }
+      rec = make_double4(0.0, 0.0, 0.0, __longlong_as_double(-1ll));
+      if (lane_on && j < nv) rec = ld256(f.vpts + j);
+    }
+    const int pix = static_cast<int>(__double_as_longlong(rec.w));
+    const double px = rec.x, py = rec.y, pz = rec.z;
+    if constexpr (!B) {
+      const int j = base + TW * PPW + lane / G;
+      rec = make_double4(0.0, 0.0, 0.0, __longlong_as_double(-1ll));
+      if (lane_on && j < nv) rec = ld256(f.vpts + j);
     }
     const bool act = pix >= 0;
     const int pu = pix % a.W, pv = pix / a.W;
@@ -2094,11 +2103,6 @@ struct ShapeIn {
   float4 n;
   uchar4 lk;
 };
-__device__ __forceinline__ double4 ld256_cg(const double4* p) {
-  double4 v;
-  asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
-  return v;
-}
 template <bool PRE>
 __device__ __forceinline__ ShapeIn shape_gather(const DevModel& m, const DevState& s, const double4* phi_in, int i) {
   ShapeIn in;
