@@ -1111,7 +1111,40 @@ static __global__ void __launch_bounds__(kVThreads, B ? WT_SEARCH_MINB_BATCH : 4
     const int pu = pix % a.W, pv = pix / a.W;
     double best_x = INFINITY;
     int best_i = -1;
-    if (act && sub < (2 * K1 + 1) * SPL) {
+#ifndef WT_SEARCH_CORE_DEAL
+#define WT_SEARCH_CORE_DEAL 1
+#endif
+    // the batch form (3x3 core, 4 lanes): the three core-row spans as one
+    // list dealt round-robin to all 4 lanes (longest lane ~n/4 items, not the
+    // longest row's n/3 with a lane idle)
+    constexpr bool kDeal = WT_SEARCH_CORE_DEAL && B && G == 4 && SPL == 1 && NR == 1;
+    if (kDeal && K1 == 1) {
+      if (act) {
+        const int c0 = max(pu - 1, 0), c1 = min(pu + 1, a.W - 1);
+        int lo[3], n[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int rr = pv - 1 + q;
+          const bool in = rr >= 0 && rr < a.H;
+          lo[q] = in ? __ldg(s.poff + rr * a.W + c0) : 0;
+          n[q] = in ? __ldg(s.poff + rr * a.W + c1 + 1) - lo[q] : 0;
+        }
+        const long long ck = d2_key(a.cut2);
+        long long bk = LLONG_MAX;
+        const int n01 = n[0] + n[1], nt = n01 + n[2];
+        for (int t = sub; t < nt; t += G) {
+          const int e = t < n[0] ? lo[0] + t : (t < n01 ? lo[1] + (t - n[0]) : lo[2] + (t - n01));
+          const double4 it = ld256(s.items + e);
+          const long long xk = d2_key(exact_d2(it, px, py, pz));
+          const int vi = static_cast<int>(__double_as_longlong(it.w));
+          if (xk <= ck && (xk < bk || (xk == bk && vi < best_i))) {
+            bk = xk;
+            best_i = vi;
+          }
+        }
+        if (best_i >= 0) best_x = __longlong_as_double(bk);
+      }
+    } else if (act && sub < (2 * K1 + 1) * SPL) {
       // SPL lanes per core row, each scanning every SPL-th item of its span
       const int rr = pv - K1 + sub / SPL;
       if (rr >= 0 && rr < a.H) {
