@@ -850,6 +850,17 @@ static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, 
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= H) return;
+  // this row's counts first: their loads and the preceding rows' sums below
+  // are in flight together
+  int* cnt = s.pix_cnt + row * W;
+  int* off = s.poff + row * W;
+  const int nch = (W + 31) / 32;
+  int v[kRowChunks];
+#pragma unroll
+  for (int t = 0; t < kRowChunks; ++t) {
+    const int c = t * 32 + lane;
+    v[t] = (t < nch && c < W) ? __ldcg(cnt + c) : 0;
+  }
   int base = 0;
   {
     // sum of the preceding rows' counts: 16 loads in flight per lane
@@ -867,15 +878,6 @@ static __global__ void __launch_bounds__(kVThreads) k_pixoff(DevState s, int W, 
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
-  int* cnt = s.pix_cnt + row * W;
-  int* off = s.poff + row * W;
-  const int nch = (W + 31) / 32;
-  int v[kRowChunks];
-#pragma unroll
-  for (int t = 0; t < kRowChunks; ++t) {
-    const int c = t * 32 + lane;
-    v[t] = (t < nch && c < W) ? __ldcg(cnt + c) : 0;
-  }
   int run = base;
 #pragma unroll
   for (int t = 0; t < kRowChunks; ++t) {
