@@ -2050,24 +2050,28 @@ __device__ __forceinline__ bool solve_vertex3(const double g[3], double r, const
   }
   delta[0] = delta[1] = delta[2] = 0.0;
   if (!finite) return false;
-  // LLT on the lower triangle (Eigen llt_inplace semantics)
-  double l00 = A[0][0];
-  if (!(l00 > 0.0)) return false;
-  l00 = sqrt(l00);
-  const double l10 = A[1][0] / l00, l20 = A[2][0] / l00;
-  double l11 = A[1][1] - l10 * l10;
-  if (!(l11 > 0.0)) return false;
-  l11 = sqrt(l11);
-  const double l21 = (A[2][1] - l20 * l10) / l11;
-  double l22 = A[2][2] - l20 * l20 - l21 * l21;
-  if (!(l22 > 0.0)) return false;
-  l22 = sqrt(l22);
-  const double y0 = b[0] / l00;
-  const double y1 = (b[1] - l10 * y0) / l11;
-  const double y2 = (b[2] - l20 * y0 - l21 * y1) / l22;
-  delta[2] = y2 / l22;
-  delta[1] = (y1 - l21 * delta[2]) / l11;
-  delta[0] = (y0 - l10 * delta[1] - l20 * delta[2]) / l00;
+  // LLT on the lower triangle (Eigen llt_inplace semantics: a pivot <= 0
+  // fails). The factor's diagonal enters only through its reciprocals, so
+  // each is one rsqrt of the pivot: no fp64 division or square root on the
+  // chain (results within an ulp or two of the divided form; C5 shape step
+  // 392 -> 301 us, C3 18.5 -> 15.1 us).
+  const double p0 = A[0][0];
+  if (!(p0 > 0.0)) return false;
+  const double i0 = rsqrt(p0);
+  const double l10 = A[1][0] * i0, l20 = A[2][0] * i0;
+  const double p1 = A[1][1] - l10 * l10;
+  if (!(p1 > 0.0)) return false;
+  const double i1 = rsqrt(p1);
+  const double l21 = (A[2][1] - l20 * l10) * i1;
+  const double p2 = A[2][2] - l20 * l20 - l21 * l21;
+  if (!(p2 > 0.0)) return false;
+  const double i2 = rsqrt(p2);
+  const double y0 = b[0] * i0;
+  const double y1 = (b[1] - l10 * y0) * i1;
+  const double y2 = (b[2] - l20 * y0 - l21 * y1) * i2;
+  delta[2] = y2 * i2;
+  delta[1] = (y1 - l21 * delta[2]) * i1;
+  delta[0] = (y0 - l10 * delta[1] - l20 * delta[2]) * i0;
   return true;
 }
 
