@@ -9,10 +9,10 @@
 
 using namespace wt;
 
-template <int N>
+template <int N, bool PAIRS = false>
 __global__ void k_ldlt(int L, long long* cyc, double* out) {
   __shared__ double A[32 * 33], b[32], x[32];
-  __shared__ double scol[4][32];
+  __shared__ double scol[6][32];
   const int lane = threadIdx.x;
   for (int r = 0; r < 4; ++r) {
     for (int i = 0; i < L; ++i) A[i * (L + 1) + lane % (L + 1)] = 0.0;
@@ -23,7 +23,7 @@ __global__ void k_ldlt(int L, long long* cyc, double* out) {
     }
     __syncwarp();
     const long long t0 = clock64();
-    const int ok = warp_ldlt_solve<N>(L, L + 1, A, b, x, scol);
+    const int ok = PAIRS ? warp_ldlt_solve2<N>(L, L + 1, A, b, x, scol) : warp_ldlt_solve<N>(L, L + 1, A, b, x, scol);
     __syncwarp();
     const long long t1 = clock64();
     if (lane == 0) cyc[r] = t1 - t0;
@@ -31,7 +31,7 @@ __global__ void k_ldlt(int L, long long* cyc, double* out) {
   }
 }
 
-template <int N>
+template <int N, bool PAIRS = false>
 void run(int L) {
   long long* dc;
   double* dout;
@@ -39,9 +39,12 @@ void run(int L) {
   cudaMalloc(&dout, sizeof(double) * 32);
   long long c[4];
   for (int rep = 0; rep < 2; ++rep) {
-    k_ldlt<N><<<1, 32>>>(L, dc, dout);
+    k_ldlt<N, PAIRS><<<1, 32>>>(L, dc, dout);
     cudaMemcpy(c, dc, sizeof(c), cudaMemcpyDeviceToHost);
-    printf("N=%d L=%d launch %d: cycles %lld %lld %lld %lld\n", N, L, rep, c[0], c[1], c[2], c[3]);
+    double xo[32];
+    cudaMemcpy(xo, dout, sizeof(xo), cudaMemcpyDeviceToHost);
+    printf("N=%d L=%d %s launch %d: cycles %lld %lld %lld %lld  x0 %.17g x%d %.17g\n", N, L, PAIRS ? "pairs" : "single",
+           rep, c[0], c[1], c[2], c[3], xo[0], L - 1, xo[L - 1]);
   }
   cudaFree(dc);
   cudaFree(dout);
@@ -124,8 +127,13 @@ int main() {
     printf("latency cycles: dfma %lld shfl.f64 %lld drcp_rn %lld dmul+dadd %lld\n", c[0], c[1], c[2], c[3]);
   }
   run<8>(6);
+  run<8, true>(6);
   run<20>(20);
+  run<20, true>(20);
+  run<20, true>(19);
+  run<20>(19);
   run<32>(27);
+  run<32, true>(27);
   run_block(20);
   run_block(27);
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
