@@ -1386,6 +1386,79 @@ __device__ inline int warp_ldlt_solve(int L, int lda, double* A, const double* b
   return 1;
 }
 
+// warp_ldlt_solve with the pivots taken two at a time: one publish / warp
+// barrier / broadcast round per pair. The pair's second pivot D1 = d1 - e^2/d0
+// comes from the 2x2 determinant, det = d0 d1 - e^2, so its reciprocal
+// d0 / det and 1/d0 are two independent reciprocals, not a chain; the pivot
+// tests are d0 > 0 and det > 0 (D1 > 0). Row i then takes pivot k's and pivot
+// k+1's updates in one pass: a_t -= l_ik c_k[t] + l_i,k+1 w[t], with
+// w[t] = c_k+1[t] - l_k+1,k c_k[t] (column k+1 after pivot k, formed by every
+// lane). The L factors, D^-1 and the substitutions are those of the
+// one-pivot form; the rounding differs by the order of the pivot-k update.
+// scol: three pairs of 32-double buffers (column k, column k+1, rhs), alternating.
+template <int N>
+__device__ inline int warp_ldlt_solve2(int L, int lda, double* A, const double* b, double* x, double (*scol)[32]) {
+  static_assert(N % 2 == 0, "pivot pairs");
+  const int lane = threadIdx.x & 31;
+  const bool row = lane < L;
+  double a[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    a[j] = row ? (j < L ? A[lane * lda + j] : 0.0) : (j == lane ? 1.0 : 0.0);
+  }
+  double bi = row ? b[lane] : 0.0;
+  double dinv = 1.0;
+  int ok = 1;
+#pragma unroll
+  for (int k = 0; k < N; k += 2) {
+    double* ck = scol[3 * ((k >> 1) & 1)];
+    double* ck1 = scol[3 * ((k >> 1) & 1) + 1];
+    double* rhs = scol[3 * ((k >> 1) & 1) + 2];
+    ck[lane] = a[k];
+    ck1[lane] = a[k + 1];
+    rhs[lane] = bi;
+    __syncwarp();
+    const double d0 = ck[k], e = ck[k + 1], d1 = ck1[k + 1];
+    const double z0 = rhs[k], z1 = rhs[k + 1];
+    const double det = __fma_rn(d0, d1, -(e * e));
+    ok &= (d0 > 0.0 && det > 0.0) ? 1 : 0;  // uniform; padded pivots are 1
+    const double inv0 = __drcp_rn(d0);
+    const double inv1 = d0 * __drcp_rn(det);  // 1 / D1
+    const double lk1 = e * inv0;              // l_k+1,k
+    const double lik = a[k] * inv0;
+    const double lik1 = __fma_rn(-lik, e, a[k + 1]) * inv1;
+    const double z1p = __fma_rn(-lk1, z0, z1);  // rhs k+1 after pivot k
+#pragma unroll
+    for (int t = k + 2; t < N; ++t) {
+      const double w = __fma_rn(-lk1, ck[t], ck1[t]);
+      a[t] = __fma_rn(-lik1, w, __fma_rn(-lik, ck[t], a[t]));
+    }
+    if (lane == k) dinv = inv0;
+    if (lane == k + 1) {
+      dinv = inv1;
+      bi = z1p;
+      if (row) A[lane * lda + k] = lk1;
+    }
+    if (lane > k + 1) {
+      bi = __fma_rn(-lik1, z1p, __fma_rn(-lik, z0, bi));
+      if (row) {
+        A[lane * lda + k] = lik;
+        A[lane * lda + k + 1] = lik1;
+      }
+    }
+  }
+  if (!ok) return 0;
+  __syncwarp();
+  double yi = bi * dinv;
+  for (int k = L - 1; k >= 0; --k) {
+    const double xk = __shfl_sync(0xffffffffu, yi, k);
+    if (lane < k) yi = __fma_rn(-A[k * lda + lane], xk, yi);
+  }
+  if (row) x[lane] = yi;
+  __syncwarp();
+  return 1;
+}
+
 // ---------------------------------------------------------------------------
 // K6 + K7 (+K0): pose normal equations (accumulate_normal_system,
 // kinopt.cpp:72-119 with fill_row :29-47) for every associated vertex, then
@@ -1955,12 +2028,23 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
     if (warp == 0) {
       int ok = 0;
       if (s_finite) {
-        __shared__ double scol[4][32];
-        if (L <= 8) ok = warp_ldlt_solve<8>(L, Lp, A, jtr, s_x, scol);
-        else if (L <= 16) ok = warp_ldlt_solve<16>(L, Lp, A, jtr, s_x, scol);
-        else if (L <= 20) ok = warp_ldlt_solve<20>(L, Lp, A, jtr, s_x, scol);
-        else if (L <= 24) ok = warp_ldlt_solve<24>(L, Lp, A, jtr, s_x, scol);
-        else ok = warp_ldlt_solve<32>(L, Lp, A, jtr, s_x, scol);
+#ifndef WT_LDLT_PAIRS
+#define WT_LDLT_PAIRS 1
+#endif
+        __shared__ double scol[6][32];
+        if (WT_LDLT_PAIRS) {
+          if (L <= 8) ok = warp_ldlt_solve2<8>(L, Lp, A, jtr, s_x, scol);
+          else if (L <= 16) ok = warp_ldlt_solve2<16>(L, Lp, A, jtr, s_x, scol);
+          else if (L <= 20) ok = warp_ldlt_solve2<20>(L, Lp, A, jtr, s_x, scol);
+          else if (L <= 24) ok = warp_ldlt_solve2<24>(L, Lp, A, jtr, s_x, scol);
+          else ok = warp_ldlt_solve2<32>(L, Lp, A, jtr, s_x, scol);
+        } else {
+          if (L <= 8) ok = warp_ldlt_solve<8>(L, Lp, A, jtr, s_x, scol);
+          else if (L <= 16) ok = warp_ldlt_solve<16>(L, Lp, A, jtr, s_x, scol);
+          else if (L <= 20) ok = warp_ldlt_solve<20>(L, Lp, A, jtr, s_x, scol);
+          else if (L <= 24) ok = warp_ldlt_solve<24>(L, Lp, A, jtr, s_x, scol);
+          else ok = warp_ldlt_solve<32>(L, Lp, A, jtr, s_x, scol);
+        }
       }
       // theta -= x (kinopt.cpp:161-165), optional clamp, iteration stats
       double xk = 0.0;
