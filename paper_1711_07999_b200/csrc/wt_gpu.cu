@@ -568,9 +568,13 @@ void enq_associate(wt_gpu_ctx* c, const wt::DevState& s, const wt_assoc_config* 
   enq_search(c, s, a, winners);
 }
 
-// 128-thread CTAs, four resident per SM (registers): one wave of 592 CTAs,
-// ~22 vertices per warp at C3 (one scan chunk each)
-int pose_threads(const wt_gpu_ctx*) { return 128; }
+// 256-thread CTAs, two resident per SM (registers): one wave of 296 CTAs,
+// ~43 vertices per warp at C3 (two scan chunks each) and half the per-CTA
+// reduction atomics of 128-thread CTAs (C3 2119 -> 2141 frames/s); 128 when
+// 8 warps' row tiles exceed the shared memory (L > ~50)
+int pose_threads(const wt_gpu_ctx* c) {
+  return wt::pose_smem_bytes(c->L, c->NP, wt::kPoseThreads / 32) <= 227 * 1024 ? wt::kPoseThreads : 128;
+}
 
 // one wave of the pose kernel (occupancy calculator: registers and the
 // dynamic shared memory of this skeleton)

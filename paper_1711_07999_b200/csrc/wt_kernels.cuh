@@ -1480,6 +1480,10 @@ struct PoseArgs {
   double res_scale, res_inv;  // ... of sum r^2
 };
 
+// k_pose_system runs 256-thread CTAs, two per SM (registers), or 128-thread
+// CTAs when a large skeleton's row tiles do not fit 8 warps' shared memory
+// (pose_threads, wt_gpu.cu): fewer CTAs, half the reduction atomics.
+constexpr int kPoseThreads = 256;
 // Shared-memory layout of k_pose_system for L links, NP dchain pairs and
 // W warps: offsets, dchain, per-warp row tiles [W][32][L|1], per-warp
 // residuals, per-warp entry partials [W][NE], pair tables, entry table.
@@ -1509,7 +1513,7 @@ __host__ __device__ inline int pose_tile_edge(int L) {
 // 2T shared loads feed T^2 FMAs. TPL = 0: lane-owned entries
 // e = lane + 32 q (Q of them), any L <= 64.
 template <int Q, int TPL, bool B>
-static __global__ void __launch_bounds__(128, 4) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
+static __global__ void __launch_bounds__(kPoseThreads, 512 / kPoseThreads) k_pose_system(DevModel m, DevState s, const double4* phi, PoseArgs a) {
   // a lone sequence waits after staging the pose tables (pdl_entry_ordered);
   // a batch (thousands of rows per warp) keeps the plain entry
   if constexpr (B) pdl_entry();

@@ -218,10 +218,11 @@ def test_errors_surface():
     t.close()
 
 
-@pytest.mark.parametrize("links", [6, 20, 21, 27, 28, 40])
+@pytest.mark.parametrize("links", [6, 20, 21, 27, 28, 40, 48])
 def test_long_chains_against_oracle(links):
     """Every JtJ accumulation layout (3x3 lane tiles up to 20 links, 4x4 up to
-    27, lane-owned entries beyond) and both solvers (one-warp LDL^T up to 32 links,
+    27, lane-owned entries beyond; 128-thread pose CTAs for the 48-link chain,
+    whose row tiles do not fit 8 warps' shared memory) and both solvers (one-warp LDL^T up to 32 links,
     block LDL^T beyond): normal system and two pose iterations on a cloud vs
     the C oracle."""
     from . import rigs
