@@ -102,6 +102,7 @@ struct wt_gpu_ctx {
   std::string err;
   int V = 0, L = 0, NP = 0, K = 0, T = 0;
   double lever = 1.0;  // max(1, largest template distance vertex <-> joint origin), x4 margin (pose_scales)
+  std::vector<char> theta_prismatic;  // per theta index: its joint is prismatic (row entries <= 1, pose_scales)
   wt_intrinsics intr{};
   wt::DevIntr din{};
   int P = 0;
@@ -606,23 +607,36 @@ void pose_attr(wt_gpu_ctx* c) {
   WT_CUDA(cudaFuncSetAttribute(wt::k_pose_system<Q, TPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-// Fixed-point scales of the pose reduction (wt_kernels.cuh): every row entry
-// is n . dv/dtheta_k, at most the lever arm R (hinges; 1 for a prismatic
-// joint) -- c->lever, the template's with a 4x margin for pose and Phi -- and
-// |r| <= cutoff, so over V vertices JtJ_kk <= V R^2 and |Jtr_k| <= V R
-// cutoff; sum r^2 <= V cutoff^2. The scales keep those below 2^62 (at most
-// 2^-40 / 2^-44, the metre-scale values).
+// Fixed-point scales of the pose reduction (wt_kernels.cuh): row entry k is
+// n . dv/dtheta_k, at most b_k = the lever arm R for a hinge (c->lever, the
+// template's with a 4x margin for pose and Phi) and 1 for a prismatic joint,
+// and |r| <= cutoff = b_L; so over V vertices |JtJ_ab| <= V b_a b_b and
+// |Jtr_a| <= V b_a cutoff. Entry (a, b) is scaled by 2^(x_a + x_b), per-theta
+// exponents with x_k <= floor((62 - e_V) / 2) - e_k (V < 2^e_V, b_k < 2^e_k):
+// every entry stays below 2^62, and a prismatic entry in millimetres keeps
+// its own resolution instead of the hinges' (the widest entry's scale for all,
+// before). x_k <= 20: at most 2^-40, the metre-scale value. sum r^2 <= V
+// cutoff^2 has a scale of its own.
 double pow2_below(double bound, int cap) {
   int ex = 0;
   std::frexp(std::max(bound, 1e-300), &ex);  // bound < 2^ex
   return std::ldexp(1.0, std::min(cap, 62 - ex));
 }
 
+int exp2_above(double b) {  // e with b < 2^e
+  int ex = 0;
+  std::frexp(std::max(b, 1e-300), &ex);
+  return ex;
+}
+
 void pose_scales(const wt_gpu_ctx* c, double cutoff, wt::PoseArgs& pa) {
   const double V = std::max(1, c->V), R = c->lever;
-  pa.sys_scale = pow2_below(V * std::max(R * R, R * cutoff), 40);
+  const int half = (62 - exp2_above(V)) / 2;
+  for (int k = 0; k <= c->L; ++k) {
+    const double b = k == c->L ? cutoff : (c->theta_prismatic[static_cast<size_t>(k)] ? 1.0 : R);
+    pa.fexp[k] = static_cast<signed char>(std::max(-60, std::min(20, half - exp2_above(b))));
+  }
   pa.res_scale = pow2_below(2.0 * V * cutoff * cutoff, 44);
-  pa.sys_inv = 1.0 / pa.sys_scale;  // exact (powers of two)
   pa.res_inv = 1.0 / pa.res_scale;
 }
 
@@ -953,6 +967,9 @@ int create_ctx(int device, const wt_model_desc* d, const wt_intrinsics* intr, in
       for (int k = 0; k < 8; ++k) l.offset[k] = d->parent_offset[8 * j + k];
       theta_to_link[static_cast<size_t>(l.theta_index)] = j;
     }
+    c->theta_prismatic.assign(static_cast<size_t>(L), 0);
+    for (int k = 0; k < L; ++k)
+      c->theta_prismatic[static_cast<size_t>(k)] = d->joint_kind[theta_to_link[static_cast<size_t>(k)]] == WT_JOINT_PRISMATIC;
     std::vector<double> zero(static_cast<size_t>(L), 0.0);
     std::vector<wt::DQ> bind(static_cast<size_t>(L));
     wt::fk_all(c->links.data(), L, zero.data(), bind.data());

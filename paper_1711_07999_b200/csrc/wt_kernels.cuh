@@ -308,6 +308,16 @@ __host__ __device__ inline double obs_scale_of_bits(long long bits, bool inverse
   return u.d;
 }
 
+// 2^n for -1022 <= n <= 1023, from the exponent bits
+__host__ __device__ inline double exp2i(int n) {
+  union {
+    long long i;
+    double d;
+  } u;
+  u.i = static_cast<long long>(n + 1023) << 52;
+  return u.d;
+}
+
 __device__ __forceinline__ double obs_scale(const int* fwords, bool inverse = false) {
   return obs_scale_of_bits(__ldcg(reinterpret_cast<const long long*>(fwords + 2)), inverse);
 }
@@ -1476,7 +1486,8 @@ struct PoseArgs {
   const int* count_in;   // optional association override (stage hook)
   const double* res_in;
   long long* dbg;        // optional timing record of the last CTA (WT_DEBUG_POSE)
-  double sys_scale, sys_inv;  // fixed-point scale of JtJ / Jtr (pose_scales, wt_gpu.cu) and its inverse
+  signed char fexp[68];       // fixed-point exponent per theta (+ [L]: the residual column): entry (a, b)
+                              // of [JtJ | Jtr] is scaled by 2^(fexp[a] + fexp[b]) (pose_scales, wt_gpu.cu)
   double res_scale, res_inv;  // ... of sum r^2
 };
 
@@ -1566,6 +1577,8 @@ static __global__ void __launch_bounds__(kPoseThreads, 512 / kPoseThreads) k_pos
       }
     }
   }
+  __shared__ int s_fexp[68];  // fixed-point exponents (PoseArgs::fexp), one 32-bit word each
+  for (int k = threadIdx.x; k <= L; k += blockDim.x) s_fexp[k] = a.fexp[k];
   for (int k = threadIdx.x; k <= L; k += blockDim.x) s_poff[k] = __ldg(m.pair_off + k);
   for (int k = threadIdx.x; k < m.NP; k += blockDim.x) s_pth[k] = __ldg(m.pair_theta + k);
   if (TPL == 0) {
@@ -1802,7 +1815,16 @@ static __global__ void __launch_bounds__(kPoseThreads, 512 / kPoseThreads) k_pos
         }
 #pragma unroll
         for (int q = 0; q < NACC; ++q)
-          if (eidx[q] >= 0) wpart[eidx[q]] += fix(acc[q], a.sys_scale);
+          if (eidx[q] >= 0) {
+            int ex;
+            if (TPL > 0) {
+              ex = s_fexp[TPL * tbi + q / TPL] + s_fexp[TPL * tbj + q % TPL];  // (row, col), col L = Jtr
+            } else {
+              const int e = lane + 32 * q;
+              ex = s_fexp[ea[e]] + s_fexp[eb[e]];
+            }
+            wpart[eidx[q]] += fix(acc[q], exp2i(ex));
+          }
       }
       if (WT_POSE_SECTIONS && a.dbg) {
         const long long c = clock64();
@@ -1976,7 +1998,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
     ea[e] = static_cast<unsigned short>(ca);
     eb[e] = static_cast<unsigned short>(cb == L ? 0xFFFF : cb);
     if (ca == cb && static_cast<long long>(sum[q]) < 0) wrapped = 1;
-    const double val = unfix(sum[q], a.sys_inv);
+    const double val = unfix(sum[q], exp2i(-(a.fexp[ca] + a.fexp[cb])));
     if (cb == L) {
       jtr[ca] = val;
     } else {
@@ -1995,7 +2017,7 @@ static __global__ void __launch_bounds__(256, 1) k_pose_solve(DevModel m, DevSta
     ea[e] = static_cast<unsigned short>(ca);
     eb[e] = static_cast<unsigned short>(cb == L ? 0xFFFF : cb);
     if (ca == cb && static_cast<long long>(t) < 0) wrapped = 1;
-    const double val = unfix(t, a.sys_inv);
+    const double val = unfix(t, exp2i(-(a.fexp[ca] + a.fexp[cb])));
     if (cb == L) {
       jtr[ca] = val;
     } else {
