@@ -1263,13 +1263,27 @@ static void ingest(wt_gpu_ctx* c, const float* depth_dev, double scale, const do
   check_launch();
 }
 
+// device memory of this context's GPU (a frame the ingest may read in place)
+bool on_device(const wt_gpu_ctx* c, const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice && at.device == c->device;
+}
+
 int wt_gpu_load_depth(wt_gpu_ctx* c, const float* depth, double depth_scale) {
   if (!c || !depth) return WT_EINVAL;
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
     require_single(c);
-    WT_CUDA(cudaMemcpyAsync(c->d_depth, depth, sizeof(float) * c->P, cudaMemcpyDefault, c->stream));
-    ingest(c, c->d_depth, depth_scale, nullptr, nullptr);
+    if (on_device(c, depth)) {
+      ingest(c, depth, depth_scale, nullptr, nullptr);  // read in place: the ingest is its only reader
+    } else {
+      WT_CUDA(cudaMemcpyAsync(c->d_depth, depth, sizeof(float) * c->P, cudaMemcpyDefault, c->stream));
+      ingest(c, c->d_depth, depth_scale, nullptr, nullptr);
+    }
     c->frame_loaded = true;
     c->frame_on_rays = true;
   });
