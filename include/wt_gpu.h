@@ -195,9 +195,11 @@ int wt_gpu_get_state(wt_gpu_ctx* ctx, double* theta, double* phi, int32_t* frame
 /* ---- frames -------------------------------------------------------------- */
 /* Depth frame exactly as SequenceReader::read_depth returns it (row-major
  * float32, 0 = invalid); unprojected on the device like depth_to_cloud
- * (seqio.cpp:419-437). `depth` may be host (pageable or pinned) or device;
- * device memory of the context's GPU is read in place by the stream-ordered
- * ingest (it must stay valid until the next call that syncs the context). */
+ * (seqio.cpp:419-437). `depth` may be host (pageable or pinned) or device.
+ * A device frame of the context's GPU is read by the next call that consumes
+ * the frame (a track call copies and unprojects it inside its frame graph,
+ * overlapped with the first skinning and bucketing), so it must stay valid
+ * and unchanged until that call. */
 int wt_gpu_load_depth(wt_gpu_ctx* ctx, const float* depth, double depth_scale);
 /* Organized CloudFrame (association.hpp:19-29): points [P*3], valid [P]. */
 int wt_gpu_load_cloud(wt_gpu_ctx* ctx, const double* points, const uint8_t* valid);

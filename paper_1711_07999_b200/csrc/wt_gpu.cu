@@ -137,6 +137,12 @@ struct wt_gpu_ctx {
   int* d_nvalid = nullptr;
   int* d_winners = nullptr;
   bool frame_loaded = false;
+  // a device depth frame handed to wt_gpu_load_depth and not yet ingested: the
+  // next track call copies and ingests it on a branch of its frame graph that
+  // joins before the first search (track_frame_overlapped); any other frame
+  // consumer ingests it first (require_frame)
+  const float* pending_depth = nullptr;
+  double pending_scale = 1.0;
   bool frame_on_rays = false;  // depth frame: every point on its pixel's centre ray
 
   // stats
@@ -1263,6 +1269,20 @@ static void ingest(wt_gpu_ctx* c, const float* depth_dev, double scale, const do
   check_launch();
 }
 
+namespace {
+void track_frame_overlapped(wt_gpu_ctx* c, const float* depth, double scale, const wt_track_config* cfg,
+                            bool shape_now, bool device_frame = false);
+}  // namespace
+
+// the pending device frame (wt_gpu_load_depth), for a consumer that is not a
+// track call
+static void flush_pending(wt_gpu_ctx* c) {
+  if (!c->pending_depth) return;
+  const float* d = c->pending_depth;
+  c->pending_depth = nullptr;
+  ingest(c, d, c->pending_scale, nullptr, nullptr);
+}
+
 // device memory of this context's GPU (a frame the ingest may read in place)
 bool on_device(const wt_gpu_ctx* c, const void* p) {
   cudaPointerAttributes at;
@@ -1278,7 +1298,11 @@ int wt_gpu_load_depth(wt_gpu_ctx* c, const float* depth, double depth_scale) {
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
     require_single(c);
-    if (on_device(c, depth)) {
+    c->pending_depth = nullptr;
+    if (on_device(c, depth) && c->nseq == 1 && !getenv("WT_NO_H2D_OVERLAP")) {
+      c->pending_depth = depth;  // ingested by the next track call's graph, or by require_frame
+      c->pending_scale = depth_scale;
+    } else if (on_device(c, depth)) {
       ingest(c, depth, depth_scale, nullptr, nullptr);  // read in place: the ingest is its only reader
     } else {
       WT_CUDA(cudaMemcpyAsync(c->d_depth, depth, sizeof(float) * c->P, cudaMemcpyDefault, c->stream));
@@ -1294,6 +1318,7 @@ int wt_gpu_load_cloud(wt_gpu_ctx* c, const double* points, const uint8_t* valid)
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
     require_single(c);
+    c->pending_depth = nullptr;
     WT_CUDA(cudaMemcpyAsync(c->d_pts_hi, points, sizeof(double) * 3 * c->P, cudaMemcpyDefault, c->stream));
     WT_CUDA(cudaMemcpyAsync(c->d_valid, valid, c->P, cudaMemcpyDefault, c->stream));
     ingest(c, nullptr, 1.0, c->d_pts_hi, c->d_valid);
@@ -1323,10 +1348,16 @@ int wt_gpu_track_loaded(wt_gpu_ctx* c, const wt_track_config* cfg, wt_frame_stat
                   cfg->shape.diag_floor, static_cast<double>(cfg->shape_stats), static_cast<double>(start),
                   c->fk_valid ? 0.0 : 1.0}};
     const bool need_fk = !c->fk_valid;
-    run_graph(c, key, [&] {
-      enq_optimize_pose(c, &cfg->kin, &cfg->assoc, need_fk);
-      if (shape_now) enq_optimize_shape(c, start, &cfg->shape, &cfg->assoc, cfg->shape_stats != 0, false);
-    });
+    if (c->pending_depth) {  // the frame's copy + ingest on a branch of the frame graph
+      const float* d = c->pending_depth;
+      c->pending_depth = nullptr;
+      track_frame_overlapped(c, d, c->pending_scale, cfg, shape_now, true);
+    } else {
+      run_graph(c, key, [&] {
+        enq_optimize_pose(c, &cfg->kin, &cfg->assoc, need_fk);
+        if (shape_now) enq_optimize_shape(c, start, &cfg->shape, &cfg->assoc, cfg->shape_stats != 0, false);
+      });
+    }
     c->fk_valid = true;
     c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
     frame_readback(c, cfg->kin.iterations, shape_now ? cfg->shape.iterations : 0, stats);
@@ -1400,7 +1431,13 @@ int wt_gpu_track_async(wt_gpu_ctx* c, const wt_track_config* cfg) {
                            (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
     ensure_stats(c, cfg->kin.iterations, cfg->shape.iterations);
     const int start = c->cur;
-    run_graph(c, track_key(c, cfg, shape_now, 1.0), [&] { enq_track(c, cfg, shape_now); });
+    if (c->pending_depth) {  // the frame's copy + ingest on a branch of the frame graph
+      const float* d = c->pending_depth;
+      c->pending_depth = nullptr;
+      track_frame_overlapped(c, d, c->pending_scale, cfg, shape_now, true);
+    } else {
+      run_graph(c, track_key(c, cfg, shape_now, 1.0), [&] { enq_track(c, cfg, shape_now); });
+    }
     c->fk_valid = true;
     c->cur = (shape_now && (cfg->shape.iterations % 2)) ? start ^ 1 : start;
     ++c->frame_index;
@@ -1413,6 +1450,7 @@ int wt_gpu_profile_frame(wt_gpu_ctx* c, const wt_track_config* cfg, int32_t* kin
   return guarded(c, [&] {
     WT_CUDA(cudaSetDevice(c->device));
     require_frame(c);
+    flush_pending(c);
     check_assoc(&cfg->assoc);
     const bool shape_now = cfg->mode == WT_MODE_DYNAMIC ||
                            (cfg->mode == WT_MODE_SHAPE_MATCH && c->frame_index == 0);
@@ -1574,12 +1612,13 @@ bool pinned_host(const void* p) {
 // and ingest onto copy_stream at its start and joins them before the first
 // search; only the search and what follows need the frame.
 void track_frame_overlapped(wt_gpu_ctx* c, const float* depth, double scale, const wt_track_config* cfg,
-                            bool shape_now) {
+                            bool shape_now, bool device_frame) {
   if (!c->up_stream) WT_CUDA(cudaStreamCreateWithFlags(&c->up_stream, cudaStreamNonBlocking));
   if (!c->fork_ev) WT_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
   if (!c->join_ev) WT_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
   GraphKey key = track_key(c, cfg, shape_now, 4.0);
   key.v.push_back(scale);
+  key.v.push_back(device_frame ? 1.0 : 0.0);  // the upload node copies from host or device memory
   const size_t bytes = sizeof(float) * c->P;
   auto it = c->h2d_graphs.find(key);
   if (it == c->h2d_graphs.end()) {
@@ -1590,7 +1629,7 @@ void track_frame_overlapped(wt_gpu_ctx* c, const float* depth, double scale, con
       WT_CUDA(cudaStreamWaitEvent(c->up_stream, c->fork_ev, 0));
       for (int b = 0; b < c->nseq; ++b)  // one 1D upload per sequence (re-pointable per launch)
         WT_CUDA(cudaMemcpyAsync(seq_at(c->d_depth, c, b), depth + static_cast<size_t>(b) * c->P, bytes,
-                                cudaMemcpyHostToDevice, c->up_stream));
+                                cudaMemcpyDefault, c->up_stream));  // pinned host or device frames
       ingest(c, c->d_depth, scale, nullptr, nullptr, c->up_stream);
       WT_CUDA(cudaEventRecord(c->join_ev, c->up_stream));
       c->before_search = [c] { WT_CUDA(cudaStreamWaitEvent(c->stream, c->join_ev, 0)); };
@@ -1629,7 +1668,7 @@ void track_frame_overlapped(wt_gpu_ctx* c, const float* depth, double scale, con
     for (int b = 0; b < c->nseq; ++b)
       WT_CUDA(cudaGraphExecMemcpyNodeSetParams1D(it->second.exec, it->second.copy[static_cast<size_t>(b)],
                                                  seq_at(c->d_depth, c, b), depth + static_cast<size_t>(b) * c->P,
-                                                 bytes, cudaMemcpyHostToDevice));
+                                                 bytes, cudaMemcpyDefault));
   }
   WT_CUDA(cudaGraphLaunch(it->second.exec, c->stream));
 }
@@ -1674,6 +1713,7 @@ int wt_gpu_optimize_pose(wt_gpu_ctx* c, const wt_kin_config* kin, const wt_assoc
     WT_CUDA(cudaSetDevice(c->device));
     require_single(c);
     require_frame(c);
+    flush_pending(c);
     check_assoc(assoc);
     if (kin->iterations < 0) fail(WT_EINVAL, "negative iteration count");
     ensure_stats(c, kin->iterations, 0);
@@ -1702,6 +1742,7 @@ int wt_gpu_optimize_shape(wt_gpu_ctx* c, const wt_shape_config* shape, const wt_
     WT_CUDA(cudaSetDevice(c->device));
     require_single(c);
     require_frame(c);
+    flush_pending(c);
     check_assoc(assoc);
     if (shape->iterations < 0) fail(WT_EINVAL, "negative iteration count");
     ensure_stats(c, 0, shape->iterations);
@@ -1772,6 +1813,7 @@ int wt_gpu_recon_error(wt_gpu_ctx* c, double* dist, int32_t* n_visible) {
     WT_CUDA(cudaSetDevice(c->device));
     require_single(c);
     require_frame(c);
+    flush_pending(c);
     ensure_render(c);
     if (!c->rc_obs) {
       c->rc_obs = c->mem.alloc<double>(3 * static_cast<size_t>(c->P));
@@ -1840,6 +1882,7 @@ int wt_gpu_associate(wt_gpu_ctx* c, int32_t window_radius, double cutoff, int32_
     WT_CUDA(cudaSetDevice(c->device));
     require_single(c);
     require_frame(c);
+    flush_pending(c);
     wt_assoc_config a{window_radius, 0, cutoff};
     check_assoc(&a);
     if (winners) WT_CUDA(cudaMemsetAsync(c->d_winners, 0xFF, sizeof(int) * c->P, c->stream));
